@@ -1,0 +1,157 @@
+/*
+ * vs_b200.h — C ABI of the B200-native filtered vector-search operator.
+ *
+ * Drop-in boundary for the reference `sqlvs` vector-search path
+ * (/root/reference/pkg/src/sqlvs). The reference has no FFI: its boundary is
+ * the Python API below, which `paper_2605_15957_b200` keeps verbatim and
+ * implements over this ABI through ctypes (INTEGRATION.md shows the binding):
+ *
+ *   enn_search(queries, data, params, metric)         vecindex.py:109-132
+ *   FlatIndex.build / .search                         vecindex.py:138-162
+ *   IvfIndex.build / .search / .as_layout             vecindex.py:168-270
+ *   save_index / load_index (SVIX)                    vecindex.py:495-579
+ *   vector_search_operator(...)                       vecsearch.py:64-120
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Every data pointer may be HOST or DEVICE
+ *     memory (detected with cudaPointerGetAttributes); host pointers are
+ *     staged through the context stream.
+ *   - Calls are synchronous with respect to the caller (the stream is
+ *     synchronised before returning). A context is not re-entrant.
+ *   - Results follow NeighborTable (vecindex.py:70-88): per query, rows
+ *     ordered by the tie rule (distance ascending then row ascending; inner
+ *     product: score descending then row ascending), out_count[q] =
+ *     min(k', candidates_q), padding ids = -1 and distances = NaN. Distances
+ *     are float64 and are computed with the reference's exact float64
+ *     arithmetic and summation order (bit-identical to numpy's
+ *     np.sum(diff*diff, axis=-1) of distances.py:54-58).
+ *   - Row filters are packed uint32 bitmaps, LSB-first: bit i of word w
+ *     selects base row 32*w + i (nbits = base row count).
+ *   - Status codes mirror the reference exceptions (errors.py:4-54).
+ */
+#ifndef VS_B200_H
+#define VS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum vs_status {
+    VS_OK = 0,
+    VS_ERR_SHAPE = 1,        /* ShapeError: dim mismatch                      */
+    VS_ERR_EMPTY_INPUT = 2,  /* EmptyInputError: exhaustive search, no rows   */
+    VS_ERR_PARAMETER = 3,    /* ParameterError: bad k / nprobe / nlist / ...  */
+    VS_ERR_CAP_EXCEEDED = 4, /* CapExceededError: k' > vs_topk_cap()          */
+    VS_ERR_PLACEMENT = 5,    /* PlacementError: device memory exhausted       */
+    VS_ERR_CUDA = 6,         /* CUDA runtime / launch failure                 */
+    VS_ERR_INTERNAL = 7
+};
+
+enum vs_metric { VS_METRIC_SQUARED_L2 = 0, VS_METRIC_INNER_PRODUCT = 1 };
+enum vs_dtype { VS_DTYPE_F32 = 0, VS_DTYPE_BF16 = 1 };
+
+/* context options (vs_ctx_set_option) */
+enum vs_option {
+    VS_OPT_ENN_KERNEL = 1,   /* 0 auto, 1 SIMT fp32, 2 tcgen05 bf16 GEMM          */
+    VS_OPT_IVF_KERNEL = 2,   /* 0 auto, 1 query-major scan, 2 list-major scan      */
+    VS_OPT_CAND_SLACK = 3,   /* extra candidate-buffer capacity (power-of-2 sized) */
+    VS_OPT_FORCE_RETRY = 4   /* test hook: treat every query as overflowed once    */
+};
+
+/* counters (vs_ctx_stats) */
+enum vs_stat {
+    VS_STAT_LAUNCHES = 0,        /* kernels launched by the library             */
+    VS_STAT_OVERFLOW_QUERIES = 1,/* queries re-run with a larger buffer         */
+    VS_STAT_SURVIVORS = 2,       /* candidates re-ranked in float64 (last call) */
+    VS_STAT_LAST_ENN_KERNEL = 3, /* which phase-A kernel ran last               */
+    VS_STAT_N = 8
+};
+
+typedef struct vs_ctx vs_ctx;
+typedef struct vs_column vs_column;
+typedef struct vs_ivf vs_ivf;
+
+/* thread-local message for the last non-OK status */
+const char* vs_last_error(void);
+/* device top-k cap: k' above it returns VS_ERR_CAP_EXCEEDED
+ * (reference: HardwareProfile.gpu_topk_cap = 2048, placement.py:56;
+ *  vecsearch.py:86-87) */
+int32_t vs_topk_cap(void);
+int32_t vs_version(void);
+
+/* ---- context: one per GPU (one process per GPU) -------------------------- */
+int vs_ctx_create(int32_t device, vs_ctx** out);
+int vs_ctx_destroy(vs_ctx* ctx);
+/* run on a caller stream (cudaStream_t); NULL restores the context stream */
+int vs_ctx_set_stream(vs_ctx* ctx, void* stream);
+int vs_ctx_synchronize(vs_ctx* ctx);
+int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value);
+int vs_ctx_stats(vs_ctx* ctx, int64_t* out, int32_t n);
+
+/* ---- embedding columns (EmbeddingColumn, table.py:91-141) ----------------- */
+/* copy n x d rows (host or device) into library-owned device memory */
+int vs_column_create(vs_ctx* ctx, const void* src, int64_t n, int32_t d,
+                     int32_t dtype, vs_column** out);
+/* borrow caller-owned device rows (must outlive the column) */
+int vs_column_wrap(vs_ctx* ctx, void* dev_ptr, int64_t n, int32_t d,
+                   int32_t dtype, vs_column** out);
+int vs_column_free(vs_column* col);
+int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype);
+
+/* ---- exhaustive search (enn_search, vecindex.py:109-132) -----------------
+ * Filtered: bitmap over the column's rows (nullable = all rows); the result
+ * equals the reference composition rows = flatnonzero(mask);
+ * enn_search(Q, base[rows]); ids = rows[pos] (plans.py:564-569).
+ * out_ids/out_dist: [nq, k] row-major; ids are base row + id_offset (global
+ * row ids when the column is one shard of a larger collection).
+ * out_visited = nq * selected rows (vecindex.py:132). */
+int vs_enn_search(vs_ctx* ctx, const vs_column* data,
+                  const float* queries, int64_t nq, int32_t d,
+                  const uint32_t* bitmap, int64_t nbits,
+                  int32_t k, int32_t metric, int64_t id_offset,
+                  int64_t* out_ids, double* out_dist, int32_t* out_count,
+                  int64_t* out_visited);
+
+/* ---- cross-shard merge (multi-GPU exchange step) --------------
+ * ids/dist: [nparts, nq, k_in], counts: [nparts, nq]; writes the global
+ * top-k under the tie rule. Inputs are per-shard outputs of the searches. */
+int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in,
+                  const int64_t* ids, const double* dist, const int32_t* counts,
+                  int32_t k, int32_t metric,
+                  int64_t* out_ids, double* out_dist, int32_t* out_count);
+
+/* ---- IVF (IvfIndex, vecindex.py:168-270) ----------------------------------
+ * Owning layout: list_payload = list-major rows (the SVIX owning payload,
+ * vecindex.py:526-530), n_total = sum(list_sizes) rows of dtype.
+ * Non-owning layout: list_payload = NULL and base != NULL; the lists are
+ * gathered from the base column into the device list-contiguous layout.
+ * list_owned (nullable): per-list 0/1, lists not owned by this shard are
+ * probed (centroids are replicated) but not scanned (list sharding, §8e).
+ * list_ids are base row ids (ascending within each list). */
+int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
+                  const int64_t* list_sizes, const int64_t* list_ids,
+                  const void* list_payload, int32_t dtype, int32_t metric,
+                  const vs_column* base, const uint8_t* list_owned,
+                  vs_ivf** out);
+/* GPU k-means build with the reference's semantics (vecindex.py:273-318) */
+int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, uint64_t seed,
+                 int32_t metric, int32_t max_iters, vs_ivf** out);
+int vs_ivf_info(const vs_ivf* ivf, int32_t* nlist, int32_t* d, int64_t* n_total,
+                int32_t* metric, int32_t* dtype);
+/* host copies of the structure (any pointer may be NULL) */
+int vs_ivf_export(vs_ivf* ivf, float* centroids, int64_t* list_sizes,
+                  int64_t* list_ids, void* list_payload);
+/* bitmap over base rows (nullable); probes computed without the filter;
+ * out_probes (nullable): [nq, nprobe] probed list ids in rank order. */
+int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                  const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
+                  int64_t* out_ids, double* out_dist, int32_t* out_count,
+                  int32_t* out_probes, int64_t* out_visited);
+int vs_ivf_free(vs_ivf* ivf);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VS_B200_H */

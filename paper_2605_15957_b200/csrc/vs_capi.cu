@@ -1,0 +1,912 @@
+// C ABI (include/vs_b200.h): contexts, columns, IVF structures and the search
+// drivers that sequence the kernels. Every entry point returns a vs_status
+// mirroring the reference exceptions (errors.py) and leaves a message in a
+// thread-local buffer (vs_last_error).
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/vs_b200.h"
+#include "vs_common.cuh"
+#include "vs_kernels.cuh"
+
+#include "vs_internal.h"
+#include "vs_tc.cuh"
+
+using namespace vs_internal;
+
+namespace {
+
+// device view of a caller buffer: device pointers pass through, host
+// pointers are copied into scratch on the context stream
+template <typename T>
+int stage_in(vs_ctx* ctx, const T* src, size_t count, const T** out) {
+    if (!src || count == 0) {
+        *out = src;
+        return VS_OK;
+    }
+    if (is_device_ptr(src)) {
+        *out = src;
+        return VS_OK;
+    }
+    T* d = nullptr;
+    CKS(arena_alloc(ctx, count, &d));
+    CK(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    *out = d;
+    return VS_OK;
+}
+
+// output target: device pointer used directly, host pointer gets scratch +
+// a deferred device->host copy
+struct OutBuf {
+    void* host = nullptr;
+    void* dev = nullptr;
+    size_t bytes = 0;
+};
+template <typename T>
+int stage_out(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& pending) {
+    if (!dst) {
+        *dev = nullptr;
+        return VS_OK;
+    }
+    if (is_device_ptr(dst)) {
+        *dev = dst;
+        return VS_OK;
+    }
+    T* d = nullptr;
+    CKS(arena_alloc(ctx, count, &d));
+    *dev = d;
+    pending.push_back(OutBuf{(void*)dst, (void*)d, count * sizeof(T)});
+    return VS_OK;
+}
+int flush_out(vs_ctx* ctx, std::vector<OutBuf>& pending) {
+    for (auto& o : pending)
+        if (o.bytes) CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return VS_OK;
+}
+
+int ensure_norms(vs_column* col) {
+    if (col->norms_ready) return VS_OK;
+    vs_ctx* ctx = col->ctx;
+    if (!col->norms) {
+        CK(cudaMalloc(&col->norms, std::max<int64_t>(col->n, 1) * sizeof(float)));
+        CK(cudaMalloc(&col->max_norm_bits, sizeof(unsigned)));
+    }
+    CK(cudaMemsetAsync(col->max_norm_bits, 0, sizeof(unsigned), ctx->stream));
+    if (col->dtype == VS_DTYPE_F32)
+        CK(vs::launch_row_norms<float>((const float*)col->data, col->n, col->d, col->norms,
+                                       col->max_norm_bits, ctx->stream));
+    else
+        CK(vs::launch_row_norms<__nv_bfloat16>((const __nv_bfloat16*)col->data, col->n, col->d,
+                                               col->norms, col->max_norm_bits, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    col->norms_ready = true;
+    return VS_OK;
+}
+
+// error-bound constant of the fp32 SIMT scores: margin =
+// 2 x 2 (d + 2) 2^-24 x (|q| + X)^2   (|q| X for inner product)
+float eps_simt(int d) { return 4.0f * (float)(d + 2) / 16777216.0f; }
+
+// ---- shared phase-A/B driver for exhaustive scans (data search and IVF coarse) ---------
+struct EnnJob {
+    const float* q;           // device [nq][d]
+    int64_t nq;
+    int d;
+    const void* rows;         // device base rows
+    int dtype;
+    const int64_t* sel;       // device selection (nullable)
+    int64_t nsel;
+    const float* xnorm;       // per base row (L2)
+    const unsigned* xmax;     // max ||x||^2 bits
+    int ip;
+    int k;
+    int64_t id_offset;
+    // outputs (device, nullable)
+    int64_t* out_ids;
+    double* out_dist;
+    int32_t* out_ids32;
+    int32_t* out_count;
+};
+
+__global__ void k_gather_queries(const float* __restrict__ src, const int32_t* __restrict__ idx,
+                                 int64_t n, int d, float* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t tot = n * (int64_t)d;
+    for (; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / d, c = i - r * d;
+        dst[i] = src[(int64_t)idx[r] * d + c];
+    }
+}
+template <typename T>
+__global__ void k_scatter_rows(const T* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                               int w, T* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t tot = n * (int64_t)w;
+    for (; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / w, c = i - r * w;
+        dst[(int64_t)idx[r] * w + c] = src[i];
+    }
+}
+template <typename T>
+int scatter_rows(vs_ctx* ctx, const T* src, const int32_t* idx, int64_t n, int w, T* dst) {
+    if (!dst || n == 0) return VS_OK;
+    int64_t tot = n * w;
+    int blocks = (int)std::min<int64_t>((tot + 255) / 256, 4096);
+    k_scatter_rows<T><<<blocks, 256, 0, ctx->stream>>>(src, idx, n, w, dst);
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    return VS_OK;
+}
+
+int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force);
+
+// phase A + phase B for the rows [0, nsel) of one job, then re-run overflowed
+// queries with 4x larger candidate buffers (cshift + 2) until none remain.
+int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force) {
+    if (job.nq == 0) return VS_OK;
+    const int64_t qtiles = (job.nq + 127) / 128;
+    const int64_t target = (int64_t)ctx->sm_count * 4;  // 2 CTAs/SM x 2 waves
+    int64_t n_split = std::max<int64_t>(1, (target + qtiles - 1) / qtiles);
+    n_split = std::min<int64_t>(n_split, std::max<int64_t>(1, (job.nsel + 255) / 256));
+    int64_t rps = (job.nsel + n_split - 1) / n_split;
+    rps = (rps + 127) / 128 * 128;
+    n_split = (job.nsel + rps - 1) / rps;
+    const int n_sub = (int)(n_split * 2);
+    int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
+    const int64_t rows_per_sub = (rps + 1) / 2;
+    const bool exhaustive = C >= pow2ceil(rows_per_sub + 64);
+    if (exhaustive) C = pow2ceil(rows_per_sub + 64);
+
+    vs::CandBuf cb;
+    cb.n_sub = n_sub;
+    cb.C = (int)C;
+    const size_t slots = (size_t)job.nq * n_sub * C;
+    CKS(arena_alloc(ctx, slots, &cb.key));
+    CKS(arena_alloc(ctx, slots, &cb.pos));
+    CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
+    CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
+    CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
+
+    vs::EnnScanParams sp;
+    sp.Q = job.q;
+    sp.nq = job.nq;
+    sp.d = job.d;
+    sp.X = job.rows;
+    sp.sel = job.sel;
+    sp.nsel = job.nsel;
+    sp.xnorm = job.xnorm;
+    sp.margin = margin;
+    sp.ip = job.ip;
+    sp.k = job.k;
+    sp.n_split = (int)n_split;
+    sp.rows_per_split = rps;
+    sp.cb = cb;
+    bool used_tc = false;
+    if (ctx->opt_enn_kernel != 1 && vs::tc_supported(job.d, job.dtype, job.ip) &&
+        (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d))) {
+        int st = vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb);
+        if (st != VS_OK) return st;
+        used_tc = true;
+    }
+    if (!used_tc) {
+        if (job.dtype == VS_DTYPE_F32) CK(vs::launch_enn_scan_simt<float>(sp, ctx->stream));
+        else CK(vs::launch_enn_scan_simt<__nv_bfloat16>(sp, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAST_ENN_KERNEL] = used_tc ? 2 : 1;
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+
+    vs::RerankParams rp;
+    rp.Q = job.q;
+    rp.nq = job.nq;
+    rp.d = job.d;
+    rp.ip = job.ip;
+    rp.k = job.k;
+    rp.cb = sp.cb;
+    rp.margin = used_tc ? sp.margin : margin;
+    rp.rows = job.rows;
+    rp.row_map = job.sel;
+    rp.id_map = nullptr;
+    rp.id_offset = job.id_offset;
+    const int64_t all_slots = (int64_t)sp.cb.n_sub * sp.cb.C;
+    rp.s_cap = (exhaustive || (int64_t)job.nq * all_slots * 20 < (int64_t(1) << 30))
+                   ? all_slots
+                   : std::min<int64_t>(all_slots, std::max<int64_t>(8 * (int64_t)sp.cb.C, 4096));
+    CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_pos));
+    CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_key));
+    CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_id));
+    rp.out_ids = job.out_ids;
+    rp.out_dist = job.out_dist;
+    rp.out_ids32 = job.out_ids32;
+    rp.out_count = job.out_count;
+    unsigned long long* d_surv = nullptr;
+    CKS(arena_alloc(ctx, 1, &d_surv));
+    CK(cudaMemsetAsync(d_surv, 0, sizeof(unsigned long long), ctx->stream));
+    rp.n_survivors = d_surv;
+    if (job.dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
+    else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+
+    unsigned long long h_surv = 0;
+    CK(cudaMemcpyAsync(&h_surv, d_surv, sizeof(h_surv), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<int32_t> which;
+    {
+        std::vector<int> h(job.nq);
+        CK(cudaMemcpyAsync(h.data(), cb.overflow, job.nq * sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int64_t i = 0; i < job.nq; ++i)
+            if (h[i] || (allow_force && ctx->opt_force_retry)) which.push_back((int32_t)i);
+    }
+    if (cshift == 0) ctx->stats[VS_STAT_SURVIVORS] = (int64_t)h_surv;
+    if (which.empty()) return VS_OK;
+    if (exhaustive && !(allow_force && ctx->opt_force_retry))
+        return set_err(VS_ERR_INTERNAL, "candidate overflow with exhaustive buffers");
+    ctx->stats[VS_STAT_OVERFLOW_QUERIES] += (int64_t)which.size();
+
+    // re-run the overflowed queries with 4x larger buffers
+    const int64_t m = (int64_t)which.size();
+    int32_t* d_idx = nullptr;
+    float *d_q = nullptr, *d_m = nullptr;
+    CKS(arena_alloc(ctx, m, &d_idx));
+    CKS(arena_alloc(ctx, (size_t)m * job.d, &d_q));
+    CKS(arena_alloc(ctx, (size_t)m, &d_m));
+    CK(cudaMemcpyAsync(d_idx, which.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    {
+        int blocks = (int)std::min<int64_t>((m * job.d + 255) / 256, 4096);
+        k_gather_queries<<<blocks, 256, 0, ctx->stream>>>(job.q, d_idx, m, job.d, d_q);
+        CK(cudaGetLastError());
+        k_gather_queries<<<1, 256, 0, ctx->stream>>>(margin, d_idx, m, 1, d_m);
+        CK(cudaGetLastError());
+        ctx->stats[VS_STAT_LAUNCHES] += 2;
+    }
+    EnnJob sub = job;
+    sub.q = d_q;
+    sub.nq = m;
+    const int k = job.k;
+    if (job.out_ids) CKS(arena_alloc(ctx, (size_t)m * k, &sub.out_ids));
+    if (job.out_dist) CKS(arena_alloc(ctx, (size_t)m * k, &sub.out_dist));
+    if (job.out_ids32) CKS(arena_alloc(ctx, (size_t)m * k, &sub.out_ids32));
+    if (job.out_count) CKS(arena_alloc(ctx, (size_t)m, &sub.out_count));
+    CKS(run_enn(ctx, sub, d_m, exhaustive ? cshift : cshift + 2, false));
+    CKS(scatter_rows(ctx, sub.out_ids, d_idx, m, k, job.out_ids));
+    CKS(scatter_rows(ctx, sub.out_dist, d_idx, m, k, job.out_dist));
+    CKS(scatter_rows(ctx, sub.out_ids32, d_idx, m, k, job.out_ids32));
+    CKS(scatter_rows(ctx, sub.out_count, d_idx, m, 1, job.out_count));
+    return VS_OK;
+}
+
+int validate_metric(int32_t metric) {
+    if (metric != VS_METRIC_SQUARED_L2 && metric != VS_METRIC_INNER_PRODUCT)
+        return set_err(VS_ERR_PARAMETER, "unknown metric %d", metric);
+    return VS_OK;
+}
+int validate_k(int32_t k) {
+    if (k < 1) return set_err(VS_ERR_PARAMETER, "k must be >= 1, got %d", k);
+    if (k > kTopkCap) return set_err(VS_ERR_CAP_EXCEEDED, "k'=%d exceeds device top-k cap %d", k, kTopkCap);
+    return VS_OK;
+}
+
+// bitmap -> selection vector on the device
+int build_selection(vs_ctx* ctx, const uint32_t* d_bm, int64_t nbits, int64_t** sel, int64_t* nsel) {
+    const int64_t nwords = (nbits + 31) / 32;
+    const int64_t nb = vs::select_nblocks(nwords);
+    int64_t* sums = nullptr;
+    int64_t* total = nullptr;
+    CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(nb, 1), &sums));
+    CKS(arena_alloc(ctx, 1, &total));
+    CK(cudaMemsetAsync(total, 0, sizeof(int64_t), ctx->stream));
+    if (nb > 0) {
+        CK(vs::launch_select_count(d_bm, nwords, nbits, sums, nb, ctx->stream));
+        CK(vs::launch_select_scan(sums, nb, total, ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 2;
+    }
+    int64_t h_total = 0;
+    CK(cudaMemcpyAsync(&h_total, total, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *nsel = h_total;
+    int64_t* s = nullptr;
+    CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(h_total, 1), &s));
+    if (h_total > 0) {
+        CK(vs::launch_select_write(d_bm, nwords, nbits, sums, s, ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
+    *sel = s;
+    return VS_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* vs_last_error(void) { return g_err.c_str(); }
+int32_t vs_topk_cap(void) { return kTopkCap; }
+int32_t vs_version(void) { return 1; }
+
+int vs_ctx_create(int32_t device, vs_ctx** out) {
+    if (!out) return set_err(VS_ERR_PARAMETER, "null out");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_err(VS_ERR_PARAMETER, "device %d not present (%d visible)", device, ndev);
+    DevGuard g(device);
+    CK(cudaSetDevice(device));
+    vs_ctx* c = new vs_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_err(e, "cudaStreamCreate");
+    }
+    c->stream = c->own_stream;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    *out = c;
+    return VS_OK;
+}
+
+int vs_ctx_destroy(vs_ctx* ctx) {
+    if (!ctx) return VS_OK;
+    DevGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->arena.release();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return VS_OK;
+}
+
+int vs_ctx_set_stream(vs_ctx* ctx, void* stream) {
+    if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
+    ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+    return VS_OK;
+}
+
+int vs_ctx_synchronize(vs_ctx* ctx) {
+    if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
+    DevGuard g(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return VS_OK;
+}
+
+int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value) {
+    if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
+    switch (key) {
+        case VS_OPT_ENN_KERNEL: ctx->opt_enn_kernel = (int)value; break;
+        case VS_OPT_IVF_KERNEL: ctx->opt_ivf_kernel = (int)value; break;
+        case VS_OPT_CAND_SLACK: ctx->opt_slack = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8)); break;
+        case VS_OPT_FORCE_RETRY: ctx->opt_force_retry = (int)value; break;
+        default: return set_err(VS_ERR_PARAMETER, "unknown option %d", key);
+    }
+    return VS_OK;
+}
+
+int vs_ctx_stats(vs_ctx* ctx, int64_t* out, int32_t n) {
+    if (!ctx || !out) return set_err(VS_ERR_PARAMETER, "null argument");
+    for (int i = 0; i < n && i < VS_STAT_N; ++i) out[i] = ctx->stats[i];
+    return VS_OK;
+}
+
+int vs_column_create(vs_ctx* ctx, const void* src, int64_t n, int32_t d, int32_t dtype,
+                     vs_column** out) {
+    if (!ctx || !out) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (d < 1) return set_err(VS_ERR_SHAPE, "embedding dimension must be >= 1");
+    if (n < 0) return set_err(VS_ERR_SHAPE, "negative row count");
+    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
+    if (n > 0 && !src) return set_err(VS_ERR_PARAMETER, "null source");
+    DevGuard g(ctx->device);
+    vs_column* c = new vs_column();
+    c->ctx = ctx;
+    c->n = n;
+    c->d = d;
+    c->dtype = dtype;
+    c->owned = true;
+    const size_t bytes = (size_t)n * d * elem_size(dtype);
+    cudaError_t e = cudaMalloc(&c->data, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return cuda_err(e, "column allocation");
+    }
+    if (bytes) {
+        e = cudaMemcpyAsync(c->data, src, bytes, cudaMemcpyDefault, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(c->data);
+            delete c;
+            return cuda_err(e, "column upload");
+        }
+    }
+    *out = c;
+    return VS_OK;
+}
+
+int vs_column_wrap(vs_ctx* ctx, void* dev_ptr, int64_t n, int32_t d, int32_t dtype, vs_column** out) {
+    if (!ctx || !out) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (d < 1) return set_err(VS_ERR_SHAPE, "embedding dimension must be >= 1");
+    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
+    if (n > 0 && !is_device_ptr(dev_ptr))
+        return set_err(VS_ERR_PARAMETER, "vs_column_wrap needs device memory");
+    vs_column* c = new vs_column();
+    c->ctx = ctx;
+    c->data = dev_ptr;
+    c->n = n;
+    c->d = d;
+    c->dtype = dtype;
+    c->owned = false;
+    *out = c;
+    return VS_OK;
+}
+
+int vs_column_free(vs_column* col) {
+    if (!col) return VS_OK;
+    DevGuard g(col->ctx->device);
+    cudaStreamSynchronize(col->ctx->stream);
+    if (col->owned && col->data) cudaFree(col->data);
+    if (col->norms) cudaFree(col->norms);
+    if (col->max_norm_bits) cudaFree(col->max_norm_bits);
+    delete col;
+    return VS_OK;
+}
+
+int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype) {
+    if (!col) return set_err(VS_ERR_PARAMETER, "null column");
+    if (n) *n = col->n;
+    if (d) *d = col->d;
+    if (dtype) *dtype = col->dtype;
+    return VS_OK;
+}
+
+int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int64_t nq, int32_t d,
+                  const uint32_t* bitmap, int64_t nbits, int32_t k, int32_t metric, int64_t id_offset,
+                  int64_t* out_ids, double* out_dist, int32_t* out_count, int64_t* out_visited) {
+    if (!ctx || !data) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_metric(metric));
+    CKS(validate_k(k));
+    if (d != data->d) return set_err(VS_ERR_SHAPE, "query dim %d != data dim %d", d, data->d);
+    if (nq < 0) return set_err(VS_ERR_PARAMETER, "negative query count");
+    if (bitmap && nbits != data->n)
+        return set_err(VS_ERR_SHAPE, "bitmap covers %lld rows, column has %lld", (long long)nbits,
+                       (long long)data->n);
+    if (data->n == 0) return set_err(VS_ERR_EMPTY_INPUT, "exhaustive search over empty data side");
+    DevGuard g(ctx->device);
+    vs_column* col = const_cast<vs_column*>(data);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    const float* dq = nullptr;
+    CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+    int64_t* sel = nullptr;
+    int64_t nsel = data->n;
+    if (bitmap) {
+        const uint32_t* dbm = nullptr;
+        CKS(stage_in(ctx, bitmap, (size_t)(nbits + 31) / 32, &dbm));
+        CKS(build_selection(ctx, dbm, nbits, &sel, &nsel));
+        if (nsel == 0) return set_err(VS_ERR_EMPTY_INPUT, "exhaustive search over empty data side");
+    }
+    if (out_visited) *out_visited = nq * nsel;
+    if (nq == 0) return VS_OK;
+    CKS(ensure_norms(col));
+    float* margin = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq, &margin));
+    CK(vs::launch_query_margins(dq, nq, d, col->max_norm_bits, eps_simt(d), metric, margin, nullptr,
+                                ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    EnnJob job;
+    job.q = dq;
+    job.nq = nq;
+    job.d = d;
+    job.rows = col->data;
+    job.dtype = col->dtype;
+    job.sel = sel;
+    job.nsel = nsel;
+    job.xnorm = col->norms;
+    job.xmax = col->max_norm_bits;
+    job.ip = metric;
+    job.k = k;
+    job.id_offset = id_offset;
+    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending));
+    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
+    CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
+    job.out_ids32 = nullptr;
+    CKS(run_enn(ctx, job, margin, 0, true));
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
+int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in, const int64_t* ids,
+                  const double* dist, const int32_t* counts, int32_t k, int32_t metric,
+                  int64_t* out_ids, double* out_dist, int32_t* out_count) {
+    if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
+    CKS(validate_metric(metric));
+    CKS(validate_k(k));
+    if (nparts < 1 || k_in < 1 || nq < 0) return set_err(VS_ERR_PARAMETER, "bad merge shape");
+    if (nq == 0) return VS_OK;
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    vs::MergeParams p;
+    p.nparts = nparts;
+    p.nq = nq;
+    p.k_in = k_in;
+    p.k = k;
+    p.ip = metric;
+    const size_t n_in = (size_t)nparts * nq * k_in;
+    CKS(stage_in(ctx, ids, n_in, &p.ids));
+    CKS(stage_in(ctx, dist, n_in, &p.dist));
+    CKS(stage_in(ctx, counts, (size_t)nparts * nq, &p.counts));
+    CKS(arena_alloc(ctx, n_in, &p.s_key));
+    CKS(arena_alloc(ctx, n_in, &p.s_id));
+    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &p.out_ids, pending));
+    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &p.out_dist, pending));
+    CKS(stage_out(ctx, out_count, (size_t)nq, &p.out_count, pending));
+    CK(vs::launch_merge(p, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
+int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
+                  const int64_t* list_sizes, const int64_t* list_ids, const void* list_payload,
+                  int32_t dtype, int32_t metric, const vs_column* base, const uint8_t* list_owned,
+                  vs_ivf** out) {
+    if (!ctx || !out || !centroids || !list_sizes) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_metric(metric));
+    if (nlist < 1) return set_err(VS_ERR_PARAMETER, "nlist must be >= 1");
+    if (d < 1) return set_err(VS_ERR_SHAPE, "embedding dimension must be >= 1");
+    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
+    if (!list_payload && !base) return set_err(VS_ERR_PARAMETER, "non-owning IVF needs a base column");
+    if (base && base->d != d) return set_err(VS_ERR_SHAPE, "base dim %d != index dim %d", base->d, d);
+    if (!list_payload && base->dtype != dtype) return set_err(VS_ERR_PARAMETER, "base dtype mismatch");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    // sizes may live on either side; read them on the host
+    std::vector<int64_t> sizes(nlist);
+    CK(cudaMemcpy(sizes.data(), list_sizes, nlist * sizeof(int64_t), cudaMemcpyDefault));
+    std::vector<int64_t> off(nlist + 1, 0);
+    for (int i = 0; i < nlist; ++i) {
+        if (sizes[i] < 0) return set_err(VS_ERR_PARAMETER, "negative list size");
+        off[i + 1] = off[i] + sizes[i];
+    }
+    const int64_t n_total = off[nlist];
+    if (n_total > 0 && !list_ids) return set_err(VS_ERR_PARAMETER, "null list ids");
+    vs_ivf* v = new vs_ivf();
+    v->ctx = ctx;
+    v->nlist = nlist;
+    v->d = d;
+    v->metric = metric;
+    v->dtype = dtype;
+    v->n_total = n_total;
+    v->h_off = off;
+    auto fail = [&](cudaError_t e, const char* what) {
+        cudaGetLastError();
+        vs_ivf_free(v);
+        return cuda_err(e, what);
+    };
+    cudaError_t e;
+    const size_t es = elem_size(dtype);
+    if ((e = cudaMalloc(&v->centroids, (size_t)nlist * d * sizeof(float))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->cnorms, (size_t)nlist * sizeof(float))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->cmax, sizeof(unsigned))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->list_off, (size_t)(nlist + 1) * sizeof(int64_t))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->list_ids, std::max<size_t>(n_total, 1) * sizeof(int64_t))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->payload, std::max<size_t>((size_t)n_total * d * es, 16))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->pnorms, std::max<size_t>(n_total, 1) * sizeof(float))) != cudaSuccess) return fail(e, "alloc");
+    if ((e = cudaMalloc(&v->pmax, sizeof(unsigned))) != cudaSuccess) return fail(e, "alloc");
+    cudaStream_t s = ctx->stream;
+    if ((e = cudaMemcpyAsync(v->centroids, centroids, (size_t)nlist * d * sizeof(float), cudaMemcpyDefault, s)) != cudaSuccess) return fail(e, "upload");
+    if ((e = cudaMemcpyAsync(v->list_off, off.data(), (nlist + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e, "upload");
+    if (n_total > 0) {
+        if ((e = cudaMemcpyAsync(v->list_ids, list_ids, n_total * sizeof(int64_t), cudaMemcpyDefault, s)) != cudaSuccess) return fail(e, "upload");
+        if (list_payload) {
+            if ((e = cudaMemcpyAsync(v->payload, list_payload, (size_t)n_total * d * es, cudaMemcpyDefault, s)) != cudaSuccess) return fail(e, "upload");
+        } else {
+            if (dtype == VS_DTYPE_F32)
+                e = vs::launch_gather_rows<float>((const float*)base->data, v->list_ids, n_total, d, (float*)v->payload, s);
+            else
+                e = vs::launch_gather_rows<__nv_bfloat16>((const __nv_bfloat16*)base->data, v->list_ids, n_total, d,
+                                                          (__nv_bfloat16*)v->payload, s);
+            if (e != cudaSuccess) return fail(e, "gather");
+            ctx->stats[VS_STAT_LAUNCHES] += 1;
+        }
+    }
+    if (list_owned) {
+        if ((e = cudaMalloc(&v->owned, nlist)) != cudaSuccess) return fail(e, "alloc");
+        if ((e = cudaMemcpyAsync(v->owned, list_owned, nlist, cudaMemcpyDefault, s)) != cudaSuccess) return fail(e, "upload");
+    }
+    cudaMemsetAsync(v->cmax, 0, sizeof(unsigned), s);
+    cudaMemsetAsync(v->pmax, 0, sizeof(unsigned), s);
+    if ((e = vs::launch_row_norms<float>(v->centroids, nlist, d, v->cnorms, v->cmax, s)) != cudaSuccess) return fail(e, "norms");
+    if (dtype == VS_DTYPE_F32)
+        e = vs::launch_row_norms<float>((const float*)v->payload, n_total, d, v->pnorms, v->pmax, s);
+    else
+        e = vs::launch_row_norms<__nv_bfloat16>((const __nv_bfloat16*)v->payload, n_total, d, v->pnorms, v->pmax, s);
+    if (e != cudaSuccess) return fail(e, "norms");
+    ctx->stats[VS_STAT_LAUNCHES] += 2;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e, "sync");
+    *out = v;
+    return VS_OK;
+}
+
+int vs_ivf_info(const vs_ivf* ivf, int32_t* nlist, int32_t* d, int64_t* n_total, int32_t* metric,
+                int32_t* dtype) {
+    if (!ivf) return set_err(VS_ERR_PARAMETER, "null ivf");
+    if (nlist) *nlist = ivf->nlist;
+    if (d) *d = ivf->d;
+    if (n_total) *n_total = ivf->n_total;
+    if (metric) *metric = ivf->metric;
+    if (dtype) *dtype = ivf->dtype;
+    return VS_OK;
+}
+
+int vs_ivf_export(vs_ivf* ivf, float* centroids, int64_t* list_sizes, int64_t* list_ids,
+                  void* list_payload) {
+    if (!ivf) return set_err(VS_ERR_PARAMETER, "null ivf");
+    DevGuard g(ivf->ctx->device);
+    cudaStream_t s = ivf->ctx->stream;
+    if (centroids) CK(cudaMemcpyAsync(centroids, ivf->centroids, (size_t)ivf->nlist * ivf->d * sizeof(float), cudaMemcpyDefault, s));
+    if (list_sizes) {
+        std::vector<int64_t> sz(ivf->nlist);
+        for (int i = 0; i < ivf->nlist; ++i) sz[i] = ivf->h_off[i + 1] - ivf->h_off[i];
+        CK(cudaMemcpyAsync(list_sizes, sz.data(), ivf->nlist * sizeof(int64_t), cudaMemcpyDefault, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    if (list_ids && ivf->n_total) CK(cudaMemcpyAsync(list_ids, ivf->list_ids, ivf->n_total * sizeof(int64_t), cudaMemcpyDefault, s));
+    if (list_payload && ivf->n_total)
+        CK(cudaMemcpyAsync(list_payload, ivf->payload, (size_t)ivf->n_total * ivf->d * elem_size(ivf->dtype), cudaMemcpyDefault, s));
+    CK(cudaStreamSynchronize(s));
+    return VS_OK;
+}
+
+int vs_ivf_free(vs_ivf* v) {
+    if (!v) return VS_OK;
+    DevGuard g(v->ctx->device);
+    cudaStreamSynchronize(v->ctx->stream);
+    cudaFree(v->centroids);
+    cudaFree(v->cnorms);
+    cudaFree(v->cmax);
+    cudaFree(v->list_off);
+    cudaFree(v->list_ids);
+    cudaFree(v->payload);
+    cudaFree(v->pnorms);
+    cudaFree(v->pmax);
+    if (v->owned) cudaFree(v->owned);
+    delete v;
+    return VS_OK;
+}
+
+}  // extern "C"
+
+// ---- IVF search driver --------------------------------------------------------------------
+namespace {
+
+struct IvfJob {
+    const vs_ivf* ivf;
+    const float* q;
+    int64_t nq;
+    const int32_t* probes;
+    int nprobe;
+    const uint32_t* pbits;
+    int k;
+    int64_t* out_ids;
+    double* out_dist;
+    int32_t* out_count;
+    unsigned long long* visited;  // nullable (retries do not count)
+};
+
+int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift) {
+    if (job.nq == 0) return VS_OK;
+    const vs_ivf* v = job.ivf;
+    const int64_t target = (int64_t)ctx->sm_count * 8;
+    int n_psplit = (int)std::min<int64_t>(job.nprobe, std::max<int64_t>(1, (target + job.nq - 1) / job.nq));
+    const int n_sub = n_psplit * 8;
+    int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
+    // the largest number of rows one warp can see bounds the buffer need
+    int64_t max_list = 0;
+    for (int i = 0; i < v->nlist; ++i) max_list = std::max(max_list, v->h_off[i + 1] - v->h_off[i]);
+    const int64_t per = (job.nprobe + n_psplit - 1) / n_psplit;
+    const int64_t bound = pow2ceil(per * max_list + 64);
+    const bool exhaustive = C >= bound;
+    if (exhaustive) C = bound;
+    vs::CandBuf cb;
+    cb.n_sub = n_sub;
+    cb.C = (int)C;
+    const size_t slots = (size_t)job.nq * n_sub * C;
+    CKS(arena_alloc(ctx, slots, &cb.key));
+    CKS(arena_alloc(ctx, slots, &cb.pos));
+    CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
+    CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
+    CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
+    unsigned long long* vis = job.visited;
+    if (!vis) {
+        CKS(arena_alloc(ctx, 1, &vis));
+        CK(cudaMemsetAsync(vis, 0, sizeof(unsigned long long), ctx->stream));
+    }
+    vs::IvfScanParams sp;
+    sp.Q = job.q;
+    sp.nq = job.nq;
+    sp.d = v->d;
+    sp.payload = v->payload;
+    sp.list_off = v->list_off;
+    sp.probes = job.probes;
+    sp.nprobe = job.nprobe;
+    sp.list_owned = v->owned;
+    sp.pbits = job.pbits;
+    sp.margin = margin;
+    sp.ip = v->metric;
+    sp.k = job.k;
+    sp.n_psplit = n_psplit;
+    sp.cb = cb;
+    sp.visited = vis;
+    if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_qmajor<float>(sp, ctx->stream));
+    else CK(vs::launch_ivf_scan_qmajor<__nv_bfloat16>(sp, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+
+    vs::RerankParams rp;
+    rp.Q = job.q;
+    rp.nq = job.nq;
+    rp.d = v->d;
+    rp.ip = v->metric;
+    rp.k = job.k;
+    rp.cb = cb;
+    rp.margin = margin;
+    rp.rows = v->payload;
+    rp.row_map = nullptr;
+    rp.id_map = v->list_ids;
+    rp.id_offset = 0;
+    const int64_t all_slots = (int64_t)n_sub * C;
+    rp.s_cap = (exhaustive || (int64_t)job.nq * all_slots * 20 < (int64_t(1) << 30))
+                   ? all_slots
+                   : std::min<int64_t>(all_slots, std::max<int64_t>(8 * C, 4096));
+    CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_pos));
+    CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_key));
+    CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_id));
+    rp.out_ids = job.out_ids;
+    rp.out_dist = job.out_dist;
+    rp.out_ids32 = nullptr;
+    rp.out_count = job.out_count;
+    rp.n_survivors = nullptr;
+    if (v->dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
+    else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+
+    std::vector<int32_t> which;
+    {
+        std::vector<int> h(job.nq);
+        CK(cudaMemcpyAsync(h.data(), cb.overflow, job.nq * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int64_t i = 0; i < job.nq; ++i)
+            if (h[i] || (cshift == 0 && ctx->opt_force_retry)) which.push_back((int32_t)i);
+    }
+    if (which.empty()) return VS_OK;
+    if (exhaustive && !(cshift == 0 && ctx->opt_force_retry))
+        return set_err(VS_ERR_INTERNAL, "IVF candidate overflow with exhaustive buffers");
+    ctx->stats[VS_STAT_OVERFLOW_QUERIES] += (int64_t)which.size();
+    const int64_t m = (int64_t)which.size();
+    int32_t* d_idx = nullptr;
+    float *d_q = nullptr, *d_m = nullptr;
+    int32_t* d_pr = nullptr;
+    CKS(arena_alloc(ctx, m, &d_idx));
+    CKS(arena_alloc(ctx, (size_t)m * v->d, &d_q));
+    CKS(arena_alloc(ctx, (size_t)m, &d_m));
+    CKS(arena_alloc(ctx, (size_t)m * job.nprobe, &d_pr));
+    CK(cudaMemcpyAsync(d_idx, which.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    int blocks = (int)std::min<int64_t>((m * v->d + 255) / 256, 4096);
+    k_gather_queries<<<blocks, 256, 0, ctx->stream>>>(job.q, d_idx, m, v->d, d_q);
+    k_gather_queries<<<1, 256, 0, ctx->stream>>>(margin, d_idx, m, 1, d_m);
+    k_gather_queries<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const float*>(job.probes), d_idx, m,
+                                                      job.nprobe, reinterpret_cast<float*>(d_pr));
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 3;
+    IvfJob sub = job;
+    sub.q = d_q;
+    sub.nq = m;
+    sub.probes = d_pr;
+    sub.visited = nullptr;
+    CKS(arena_alloc(ctx, (size_t)m * job.k, &sub.out_ids));
+    CKS(arena_alloc(ctx, (size_t)m * job.k, &sub.out_dist));
+    CKS(arena_alloc(ctx, (size_t)m, &sub.out_count));
+    CKS(run_ivf_scan(ctx, sub, d_m, exhaustive ? cshift : cshift + 2));
+    CKS(scatter_rows(ctx, sub.out_ids, d_idx, m, job.k, job.out_ids));
+    CKS(scatter_rows(ctx, sub.out_dist, d_idx, m, job.k, job.out_dist));
+    CKS(scatter_rows(ctx, sub.out_count, d_idx, m, 1, job.out_count));
+    return VS_OK;
+}
+
+}  // namespace
+
+extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                             const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
+                             int64_t* out_ids, double* out_dist, int32_t* out_count, int32_t* out_probes,
+                             int64_t* out_visited) {
+    if (!ctx || !ivf) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_k(k));
+    if (nprobe < 1) return set_err(VS_ERR_PARAMETER, "nprobe must be >= 1");
+    if (nprobe > ivf->nlist) return set_err(VS_ERR_PARAMETER, "nprobe %d > nlist %d", nprobe, ivf->nlist);
+    if (nprobe > kTopkCap) return set_err(VS_ERR_CAP_EXCEEDED, "nprobe %d exceeds device cap", nprobe);
+    if (nq < 0) return set_err(VS_ERR_PARAMETER, "negative query count");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    if (out_visited) *out_visited = 0;
+    if (nq == 0) return VS_OK;
+    const int d = ivf->d;
+    const float* dq = nullptr;
+    CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+    // coarse quantizer: exact tie-rule top-nprobe over float32 centroids, always
+    // squared L2 (vecindex.py:238-243)
+    float* cm = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq, &cm));
+    CK(vs::launch_query_margins(dq, nq, d, ivf->cmax, eps_simt(d), 0, cm, nullptr, ctx->stream));
+    int32_t* probes = nullptr;
+    CKS(stage_out(ctx, out_probes, (size_t)nq * nprobe, &probes, pending));
+    if (!probes) CKS(arena_alloc(ctx, (size_t)nq * nprobe, &probes));
+    EnnJob cj;
+    cj.q = dq;
+    cj.nq = nq;
+    cj.d = d;
+    cj.rows = ivf->centroids;
+    cj.dtype = VS_DTYPE_F32;
+    cj.sel = nullptr;
+    cj.nsel = ivf->nlist;
+    cj.xnorm = ivf->cnorms;
+    cj.xmax = ivf->cmax;
+    cj.ip = 0;
+    cj.k = nprobe;
+    cj.id_offset = 0;
+    cj.out_ids = nullptr;
+    cj.out_dist = nullptr;
+    cj.out_ids32 = probes;
+    cj.out_count = nullptr;
+    CKS(run_enn(ctx, cj, cm, 0, false));
+    // permuted bitmap over payload positions
+    uint32_t* pbits = nullptr;
+    if (bitmap) {
+        const uint32_t* dbm = nullptr;
+        CKS(stage_in(ctx, bitmap, (size_t)(nbits + 31) / 32, &dbm));
+        CKS(arena_alloc(ctx, (size_t)(ivf->n_total + 31) / 32 + 2, &pbits));
+        CK(cudaMemsetAsync(pbits, 0, ((ivf->n_total + 31) / 32 + 2) * sizeof(uint32_t), ctx->stream));
+        CK(vs::launch_permute_bitmap(dbm, nbits, ivf->list_ids, ivf->n_total, pbits, ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
+    float* sm = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq, &sm));
+    CK(vs::launch_query_margins(dq, nq, d, ivf->pmax, eps_simt(d), ivf->metric, sm, nullptr, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 2;
+    unsigned long long* vis = nullptr;
+    CKS(arena_alloc(ctx, 1, &vis));
+    CK(cudaMemsetAsync(vis, 0, sizeof(unsigned long long), ctx->stream));
+    IvfJob job;
+    job.ivf = ivf;
+    job.q = dq;
+    job.nq = nq;
+    job.probes = probes;
+    job.nprobe = nprobe;
+    job.pbits = pbits;
+    job.k = k;
+    job.visited = vis;
+    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending));
+    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
+    CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
+    if (!job.out_ids) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_ids));
+    if (!job.out_dist) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_dist));
+    if (!job.out_count) CKS(arena_alloc(ctx, (size_t)nq, &job.out_count));
+    CKS(run_ivf_scan(ctx, job, sm, 0));
+    unsigned long long h_vis = 0;
+    CK(cudaMemcpyAsync(&h_vis, vis, sizeof(h_vis), cudaMemcpyDeviceToHost, ctx->stream));
+    CKS(flush_out(ctx, pending));
+    if (out_visited) *out_visited = (int64_t)h_vis;
+    return VS_OK;
+}
+
+extern "C" int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, uint64_t seed,
+                            int32_t metric, int32_t max_iters, vs_ivf** out) {
+    return vs::ivf_build_gpu(ctx, data, nlist, seed, metric, max_iters, out);
+}

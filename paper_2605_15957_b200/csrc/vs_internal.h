@@ -1,0 +1,182 @@
+// Internal (non-ABI) structures shared by the C-ABI driver and the kernel
+// drivers: context, column and IVF objects, error plumbing, scratch arena.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/vs_b200.h"
+
+namespace vs_internal {
+
+inline thread_local std::string g_err;
+
+inline int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+inline int cuda_err(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return set_err(VS_ERR_PLACEMENT, "%s: device memory exhausted (%s)", what, cudaGetErrorString(e));
+    return set_err(VS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) { cudaGetLastError(); return cuda_err(_e, #call); } \
+    } while (0)
+#define CKS(call)                                     \
+    do {                                              \
+        int _s = (call);                              \
+        if (_s != VS_OK) return _s;                   \
+    } while (0)
+
+constexpr int kTopkCap = 2048;  // placement.py:56 gpu_topk_cap default
+
+inline int64_t pow2ceil(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+inline size_t elem_size(int dtype) { return dtype == VS_DTYPE_BF16 ? 2 : 4; }
+
+inline bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Per-call device scratch: a bump allocator over one buffer that grows to the
+// high-water mark of previous calls (calls are synchronous, so reset() runs
+// with no kernel in flight).
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0, used = 0, need = 0;
+    std::vector<void*> extra;
+    cudaError_t reset() {
+        for (void* p : extra) cudaFree(p);
+        extra.clear();
+        if (need > cap) {
+            if (base) cudaFree(base);
+            base = nullptr;
+            cap = 0;
+            cudaError_t e = cudaMalloc(&base, need);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                base = nullptr;
+                need = 0;
+            } else {
+                cap = need;
+            }
+        }
+        used = 0;
+        need = 0;
+        return cudaSuccess;
+    }
+    cudaError_t alloc(size_t n, void** out) {
+        n = (n + 255) & ~size_t(255);
+        need += n;
+        if (used + n <= cap) {
+            *out = base + used;
+            used += n;
+            return cudaSuccess;
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e != cudaSuccess) return e;
+        extra.push_back(p);
+        *out = p;
+        return cudaSuccess;
+    }
+    void release() {
+        reset();
+        if (base) cudaFree(base);
+        base = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace vs_internal
+
+struct vs_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    vs_internal::Arena arena;
+    int64_t stats[VS_STAT_N] = {0};
+    int opt_enn_kernel = 0;
+    int opt_ivf_kernel = 0;
+    int opt_slack = 0;
+    int opt_force_retry = 0;
+};
+
+struct vs_column {
+    vs_ctx* ctx = nullptr;
+    void* data = nullptr;
+    int64_t n = 0;
+    int d = 0;
+    int dtype = VS_DTYPE_F32;
+    bool owned = false;
+    float* norms = nullptr;          // ||x||^2 per row (lazy)
+    unsigned* max_norm_bits = nullptr;
+    bool norms_ready = false;
+};
+
+struct vs_ivf {
+    vs_ctx* ctx = nullptr;
+    int nlist = 0, d = 0, metric = 0, dtype = VS_DTYPE_F32;
+    int64_t n_total = 0;
+    float* centroids = nullptr;
+    float* cnorms = nullptr;
+    unsigned* cmax = nullptr;
+    int64_t* list_off = nullptr;     // device [nlist+1]
+    std::vector<int64_t> h_off;
+    int64_t* list_ids = nullptr;     // device [n_total]
+    void* payload = nullptr;         // device [n_total][d]
+    float* pnorms = nullptr;
+    unsigned* pmax = nullptr;
+    uint8_t* owned = nullptr;        // device [nlist] or null
+};
+
+
+namespace vs_internal {
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+int arena_alloc(vs_ctx* ctx, size_t count, T** out) {
+    void* p = nullptr;
+    cudaError_t e = ctx->arena.alloc(count * sizeof(T) + 16, &p);
+    if (e != cudaSuccess) return cuda_err(e, "scratch allocation");
+    *out = reinterpret_cast<T*>(p);
+    return VS_OK;
+}
+
+}  // namespace vs_internal

@@ -1,0 +1,140 @@
+// Kernel parameter blocks and launchers shared between the kernel translation
+// units and the C-ABI driver (vs_capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace vs {
+
+// Candidate buffers ("phase A" output): per (query, sub) C slots of
+// (approximate key, position), counts [nq][n_sub], overflow flag per query.
+struct CandBuf {
+    float* key;        // [nq][n_sub][C]
+    uint32_t* pos;     // [nq][n_sub][C]
+    int* cnt;          // [nq][n_sub]
+    int* overflow;     // [nq]
+    int n_sub;
+    int C;
+};
+
+// ---- bitmap -> ascending selection vector -------------------------------------------
+// rows with their bit set, ascending (the order-preserving gather of
+// table.py:326-331 / relops.py:112-113)
+cudaError_t launch_select_count(const uint32_t* bitmap, int64_t nwords, int64_t nbits,
+                                int64_t* block_sums, int64_t nblocks, cudaStream_t s);
+cudaError_t launch_select_scan(int64_t* block_sums, int64_t nblocks, int64_t* total,
+                               cudaStream_t s);
+cudaError_t launch_select_write(const uint32_t* bitmap, int64_t nwords, int64_t nbits,
+                                const int64_t* block_offsets, int64_t* sel, cudaStream_t s);
+int64_t select_nblocks(int64_t nwords);
+
+// permuted bitmap over list-major payload positions: bit(pos) = bitmap[ids[pos]]
+cudaError_t launch_permute_bitmap(const uint32_t* bitmap, int64_t nbits, const int64_t* ids,
+                                  int64_t n_total, uint32_t* pbits, cudaStream_t s);
+
+// ---- norms / margins ------------------------------------------------------------------
+// row squared norms (fp32) and the max row norm (orderable bits, atomicMax)
+template <typename T>
+cudaError_t launch_row_norms(const T* x, int64_t n, int d, float* norms,
+                             unsigned* max_norm_bits, cudaStream_t s);
+// per-query admission margin = 2 x rigorous error bound of the approximate key
+// (DESIGN.md §4): eps * (|q| + X)^2 for squared L2, eps * |q| * X for IP
+cudaError_t launch_query_margins(const float* q, int64_t nq, int d, const unsigned* max_norm_bits,
+                                 float eps, int ip, float* margin, float* qnorm, cudaStream_t s);
+
+// ---- phase A: exhaustive scan (SIMT fp32) ----------------------------------------------
+struct EnnScanParams {
+    const float* Q;
+    int64_t nq;
+    int d;
+    const void* X;          // base rows
+    const int64_t* sel;     // selection positions -> base rows (nullable: identity)
+    int64_t nsel;
+    const float* xnorm;     // per base row ||x||^2 (squared L2)
+    const float* margin;    // [nq]
+    int ip;
+    int k;
+    int n_split;
+    int64_t rows_per_split;
+    CandBuf cb;
+};
+template <typename T>
+cudaError_t launch_enn_scan_simt(const EnnScanParams& p, cudaStream_t s);
+
+// ---- phase A: IVF list scan (query-major) -----------------------------------------------
+struct IvfScanParams {
+    const float* Q;
+    int64_t nq;
+    int d;
+    const void* payload;        // list-major rows
+    const int64_t* list_off;    // [nlist + 1]
+    const int32_t* probes;      // [nq][nprobe]
+    int nprobe;
+    const uint8_t* list_owned;  // nullable
+    const uint32_t* pbits;      // nullable (unfiltered)
+    const float* margin;
+    int ip;
+    int k;
+    int n_psplit;
+    CandBuf cb;
+    unsigned long long* visited;
+};
+template <typename T>
+cudaError_t launch_ivf_scan_qmajor(const IvfScanParams& p, cudaStream_t s);
+
+// ---- phase B: exact float64 re-rank + tie-rule top-k ------------------------------------
+struct RerankParams {
+    const float* Q;
+    int64_t nq;
+    int d;
+    int ip;
+    int k;
+    CandBuf cb;
+    const float* margin;
+    const void* rows;           // exact-scoring row source
+    const int64_t* row_map;     // pos -> row index in `rows` (nullable: identity)
+    const int64_t* id_map;      // pos -> output id (nullable: row index)
+    int64_t id_offset;
+    int64_t s_cap;              // survivor capacity per query
+    uint32_t* s_pos;            // [nq][s_cap]
+    uint64_t* s_key;            // [nq][s_cap]
+    int64_t* s_id;              // [nq][s_cap]
+    int64_t* out_ids;           // [nq][k] (nullable)
+    double* out_dist;           // [nq][k] (nullable)
+    int32_t* out_ids32;         // [nq][k] (nullable; IVF probes)
+    int32_t* out_count;         // [nq] (nullable)
+    unsigned long long* n_survivors;
+};
+template <typename T>
+cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s);
+
+// ---- cross-shard merge ---------------------------------------------------------------------
+struct MergeParams {
+    int nparts;
+    int64_t nq;
+    int k_in;
+    const int64_t* ids;      // [nparts][nq][k_in]
+    const double* dist;
+    const int32_t* counts;   // [nparts][nq]
+    int k;
+    int ip;
+    uint64_t* s_key;         // [nq][nparts*k_in]
+    int64_t* s_id;
+    int64_t* out_ids;
+    double* out_dist;
+    int32_t* out_count;
+};
+cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
+
+// ---- IVF structure helpers ----------------------------------------------------------------
+template <typename T>
+cudaError_t launch_gather_rows(const T* src, const int64_t* ids, int64_t n, int d, T* dst,
+                               cudaStream_t s);
+cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe,
+                                 const int64_t* list_off, const uint8_t* list_owned,
+                                 const uint32_t* pbits, unsigned long long* visited,
+                                 cudaStream_t s);
+
+}  // namespace vs
