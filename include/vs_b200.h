@@ -57,7 +57,22 @@ enum vs_option {
     VS_OPT_ENN_KERNEL = 1,   /* 0 auto, 1 SIMT fp32, 2 tcgen05 bf16 GEMM          */
     VS_OPT_IVF_KERNEL = 2,   /* 0 auto, 1 query-major scan, 2 list-major scan      */
     VS_OPT_CAND_SLACK = 3,   /* extra candidate-buffer capacity (power-of-2 sized) */
-    VS_OPT_FORCE_RETRY = 4   /* test hook: treat every query as overflowed once    */
+    VS_OPT_FORCE_RETRY = 4,  /* test hook: treat every query as overflowed once    */
+    VS_OPT_TIMING = 5        /* 1: record CUDA events around every kernel class    */
+};
+
+/* kernel classes reported by vs_ctx_kernel_times (CUDA-event durations on the
+ * launching stream, accumulated while VS_OPT_TIMING is on) */
+enum vs_kernel_class {
+    VS_K_SELECT = 0,      /* bitmap -> selection vector / permuted bitmap       */
+    VS_K_ENN_SCAN = 1,    /* phase A of the exhaustive search                   */
+    VS_K_RERANK = 2,      /* phase B (exact float64 re-rank + top-k)            */
+    VS_K_COARSE = 3,      /* IVF coarse quantizer (phase A + B over centroids)  */
+    VS_K_IVF_SCAN = 4,    /* IVF list scan (phase A)                            */
+    VS_K_IVF_RERANK = 5,  /* IVF phase B                                        */
+    VS_K_MERGE = 6,       /* cross-shard merge                                  */
+    VS_K_STAGE = 7,       /* tensor-core operand staging (bf16 compaction)      */
+    VS_K_N = 8
 };
 
 /* counters (vs_ctx_stats) */
@@ -89,6 +104,8 @@ int vs_ctx_set_stream(vs_ctx* ctx, void* stream);
 int vs_ctx_synchronize(vs_ctx* ctx);
 int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value);
 int vs_ctx_stats(vs_ctx* ctx, int64_t* out, int32_t n);
+/* accumulated per-class kernel time (ns) and launch counts; reset=1 zeroes */
+int vs_ctx_kernel_times(vs_ctx* ctx, int64_t* ns, int64_t* launches, int32_t n, int32_t reset);
 
 /* ---- embedding columns (EmbeddingColumn, table.py:91-141) ----------------- */
 /* copy n x d rows (host or device) into library-owned device memory */

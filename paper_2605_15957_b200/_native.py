@@ -23,7 +23,8 @@ VS_OK, VS_ERR_SHAPE, VS_ERR_EMPTY_INPUT, VS_ERR_PARAMETER = 0, 1, 2, 3
 VS_ERR_CAP_EXCEEDED, VS_ERR_PLACEMENT, VS_ERR_CUDA, VS_ERR_INTERNAL = 4, 5, 6, 7
 METRIC_CODE = {"squared_l2": 0, "inner_product": 1}
 DTYPE_F32, DTYPE_BF16 = 0, 1
-OPT_ENN_KERNEL, OPT_IVF_KERNEL, OPT_CAND_SLACK, OPT_FORCE_RETRY = 1, 2, 3, 4
+OPT_ENN_KERNEL, OPT_IVF_KERNEL, OPT_CAND_SLACK, OPT_FORCE_RETRY, OPT_TIMING = 1, 2, 3, 4, 5
+KERNEL_CLASSES = ("select", "enn_scan", "rerank", "coarse", "ivf_scan", "ivf_rerank", "merge", "stage")
 STAT_LAUNCHES, STAT_OVERFLOW_QUERIES, STAT_SURVIVORS, STAT_LAST_ENN_KERNEL = 0, 1, 2, 3
 
 _vp = C.c_void_p
@@ -41,6 +42,7 @@ SIGNATURES = {
     "vs_ctx_synchronize": (C.c_int, [_vp]),
     "vs_ctx_set_option": (C.c_int, [_vp, _i32, _i64]),
     "vs_ctx_stats": (C.c_int, [_vp, _vp, _i32]),
+    "vs_ctx_kernel_times": (C.c_int, [_vp, _vp, _vp, _i32, _i32]),
     "vs_column_create": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
     "vs_column_wrap": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
     "vs_column_free": (C.c_int, [_vp]),
@@ -164,6 +166,13 @@ class Context:
 
     def set_option(self, key: int, value: int) -> None:
         check(load().vs_ctx_set_option(self.handle, key, int(value)))
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        """{class: (total_ns, launches)} of CUDA-event-timed kernel classes."""
+        ns = np.zeros(8, np.int64)
+        cnt = np.zeros(8, np.int64)
+        check(load().vs_ctx_kernel_times(self.handle, ns.ctypes.data, cnt.ctypes.data, 8, int(reset)))
+        return {name: (int(ns[i]), int(cnt[i])) for i, name in enumerate(KERNEL_CLASSES)}
 
     def stats(self) -> list:
         out = np.zeros(8, np.int64)

@@ -70,6 +70,7 @@ int flush_out(vs_ctx* ctx, std::vector<OutBuf>& pending) {
     for (auto& o : pending)
         if (o.bytes) CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    resolve_timers(ctx);
     return VS_OK;
 }
 
@@ -115,6 +116,8 @@ struct EnnJob {
     double* out_dist;
     int32_t* out_ids32;
     int32_t* out_count;
+    int cls_scan = VS_K_ENN_SCAN;
+    int cls_rerank = VS_K_RERANK;
 };
 
 __global__ void k_gather_queries(const float* __restrict__ src, const int32_t* __restrict__ idx,
@@ -191,6 +194,8 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     sp.rows_per_split = rps;
     sp.cb = cb;
     bool used_tc = false;
+    {
+    KTimer kt(ctx, job.cls_scan);
     if (ctx->opt_enn_kernel != 1 && vs::tc_supported(job.d, job.dtype, job.ip) &&
         (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d))) {
         int st = vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb);
@@ -200,6 +205,7 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     if (!used_tc) {
         if (job.dtype == VS_DTYPE_F32) CK(vs::launch_enn_scan_simt<float>(sp, ctx->stream));
         else CK(vs::launch_enn_scan_simt<__nv_bfloat16>(sp, ctx->stream));
+    }
     }
     ctx->stats[VS_STAT_LAST_ENN_KERNEL] = used_tc ? 2 : 1;
     ctx->stats[VS_STAT_LAUNCHES] += 1;
@@ -231,8 +237,11 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     CKS(arena_alloc(ctx, 1, &d_surv));
     CK(cudaMemsetAsync(d_surv, 0, sizeof(unsigned long long), ctx->stream));
     rp.n_survivors = d_surv;
-    if (job.dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
-    else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
+    {
+        KTimer kt(ctx, job.cls_rerank);
+        if (job.dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
+        else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
+    }
     ctx->stats[VS_STAT_LAUNCHES] += 1;
 
     unsigned long long h_surv = 0;
@@ -304,6 +313,7 @@ int build_selection(vs_ctx* ctx, const uint32_t* d_bm, int64_t nbits, int64_t** 
     CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(nb, 1), &sums));
     CKS(arena_alloc(ctx, 1, &total));
     CK(cudaMemsetAsync(total, 0, sizeof(int64_t), ctx->stream));
+    KTimer kt(ctx, VS_K_SELECT);
     if (nb > 0) {
         CK(vs::launch_select_count(d_bm, nwords, nbits, sums, nb, ctx->stream));
         CK(vs::launch_select_scan(sums, nb, total, ctx->stream));
@@ -358,6 +368,8 @@ int vs_ctx_destroy(vs_ctx* ctx) {
     DevGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     ctx->arena.release();
+    resolve_timers(ctx);
+    for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return VS_OK;
@@ -383,6 +395,7 @@ int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value) {
         case VS_OPT_IVF_KERNEL: ctx->opt_ivf_kernel = (int)value; break;
         case VS_OPT_CAND_SLACK: ctx->opt_slack = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8)); break;
         case VS_OPT_FORCE_RETRY: ctx->opt_force_retry = (int)value; break;
+        case VS_OPT_TIMING: ctx->opt_timing = (int)value; break;
         default: return set_err(VS_ERR_PARAMETER, "unknown option %d", key);
     }
     return VS_OK;
@@ -391,6 +404,17 @@ int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value) {
 int vs_ctx_stats(vs_ctx* ctx, int64_t* out, int32_t n) {
     if (!ctx || !out) return set_err(VS_ERR_PARAMETER, "null argument");
     for (int i = 0; i < n && i < VS_STAT_N; ++i) out[i] = ctx->stats[i];
+    return VS_OK;
+}
+
+int vs_ctx_kernel_times(vs_ctx* ctx, int64_t* ns, int64_t* launches, int32_t n, int32_t reset) {
+    if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
+    for (int i = 0; i < n && i < VS_K_N; ++i) {
+        if (ns) ns[i] = ctx->kt_ns[i];
+        if (launches) launches[i] = ctx->kt_count[i];
+    }
+    if (reset)
+        for (int i = 0; i < VS_K_N; ++i) ctx->kt_ns[i] = ctx->kt_count[i] = 0;
     return VS_OK;
 }
 
@@ -547,7 +571,10 @@ int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in, const i
     CKS(stage_out(ctx, out_ids, (size_t)nq * k, &p.out_ids, pending));
     CKS(stage_out(ctx, out_dist, (size_t)nq * k, &p.out_dist, pending));
     CKS(stage_out(ctx, out_count, (size_t)nq, &p.out_count, pending));
-    CK(vs::launch_merge(p, ctx->stream));
+    {
+        KTimer kt(ctx, VS_K_MERGE);
+        CK(vs::launch_merge(p, ctx->stream));
+    }
     ctx->stats[VS_STAT_LAUNCHES] += 1;
     CKS(flush_out(ctx, pending));
     return VS_OK;
@@ -745,8 +772,11 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     sp.n_psplit = n_psplit;
     sp.cb = cb;
     sp.visited = vis;
-    if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_qmajor<float>(sp, ctx->stream));
-    else CK(vs::launch_ivf_scan_qmajor<__nv_bfloat16>(sp, ctx->stream));
+    {
+        KTimer kt(ctx, VS_K_IVF_SCAN);
+        if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_qmajor<float>(sp, ctx->stream));
+        else CK(vs::launch_ivf_scan_qmajor<__nv_bfloat16>(sp, ctx->stream));
+    }
     ctx->stats[VS_STAT_LAUNCHES] += 1;
 
     vs::RerankParams rp;
@@ -773,8 +803,11 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     rp.out_ids32 = nullptr;
     rp.out_count = job.out_count;
     rp.n_survivors = nullptr;
-    if (v->dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
-    else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
+    {
+        KTimer kt(ctx, VS_K_IVF_RERANK);
+        if (v->dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
+        else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
+    }
     ctx->stats[VS_STAT_LAUNCHES] += 1;
 
     std::vector<int32_t> which;
@@ -865,6 +898,8 @@ extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* querie
     cj.out_dist = nullptr;
     cj.out_ids32 = probes;
     cj.out_count = nullptr;
+    cj.cls_scan = VS_K_COARSE;
+    cj.cls_rerank = VS_K_COARSE;
     CKS(run_enn(ctx, cj, cm, 0, false));
     // permuted bitmap over payload positions
     uint32_t* pbits = nullptr;
@@ -873,6 +908,7 @@ extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* querie
         CKS(stage_in(ctx, bitmap, (size_t)(nbits + 31) / 32, &dbm));
         CKS(arena_alloc(ctx, (size_t)(ivf->n_total + 31) / 32 + 2, &pbits));
         CK(cudaMemsetAsync(pbits, 0, ((ivf->n_total + 31) / 32 + 2) * sizeof(uint32_t), ctx->stream));
+        KTimer kt(ctx, VS_K_SELECT);
         CK(vs::launch_permute_bitmap(dbm, nbits, ivf->list_ids, ivf->n_total, pbits, ctx->stream));
         ctx->stats[VS_STAT_LAUNCHES] += 1;
     }

@@ -124,6 +124,16 @@ struct vs_ctx {
     int opt_ivf_kernel = 0;
     int opt_slack = 0;
     int opt_force_retry = 0;
+    int opt_timing = 0;
+    // CUDA-event timing of kernel classes (resolved after each call's final sync)
+    struct PendingTimer {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<PendingTimer> timers;
+    std::vector<cudaEvent_t> event_pool;
+    int64_t kt_ns[VS_K_N] = {0};
+    int64_t kt_count[VS_K_N] = {0};
 };
 
 struct vs_column {
@@ -177,6 +187,55 @@ int arena_alloc(vs_ctx* ctx, size_t count, T** out) {
     if (e != cudaSuccess) return cuda_err(e, "scratch allocation");
     *out = reinterpret_cast<T*>(p);
     return VS_OK;
+}
+
+}  // namespace vs_internal
+
+namespace vs_internal {
+
+// RAII scope that brackets the launches of one kernel class with CUDA events
+// on the context stream (only while VS_OPT_TIMING is on).
+struct KTimer {
+    vs_ctx* ctx;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    KTimer(vs_ctx* c, int k) : ctx(c), cls(k) {
+        if (!ctx->opt_timing) return;
+        a = take();
+        b = take();
+        cudaEventRecord(a, ctx->stream);
+    }
+    ~KTimer() {
+        if (!a) return;
+        cudaEventRecord(b, ctx->stream);
+        ctx->timers.push_back({cls, a, b});
+    }
+    cudaEvent_t take() {
+        cudaEvent_t e;
+        if (!ctx->event_pool.empty()) {
+            e = ctx->event_pool.back();
+            ctx->event_pool.pop_back();
+        } else {
+            cudaEventCreate(&e);
+        }
+        return e;
+    }
+};
+
+// after the stream is synchronised: fold recorded intervals into the totals
+inline void resolve_timers(vs_ctx* ctx) {
+    for (auto& t : ctx->timers) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+            ctx->kt_ns[t.cls] += (int64_t)(ms * 1e6);
+            ctx->kt_count[t.cls] += 1;
+        } else {
+            cudaGetLastError();
+        }
+        ctx->event_pool.push_back(t.a);
+        ctx->event_pool.push_back(t.b);
+    }
+    ctx->timers.clear();
 }
 
 }  // namespace vs_internal
