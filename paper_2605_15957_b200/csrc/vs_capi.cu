@@ -156,29 +156,6 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
 // queries with 4x larger candidate buffers (cshift + 2) until none remain.
 int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force) {
     if (job.nq == 0) return VS_OK;
-    const int64_t qtiles = (job.nq + 127) / 128;
-    const int64_t target = (int64_t)ctx->sm_count * 4;  // 2 CTAs/SM x 2 waves
-    int64_t n_split = std::max<int64_t>(1, (target + qtiles - 1) / qtiles);
-    n_split = std::min<int64_t>(n_split, std::max<int64_t>(1, (job.nsel + 255) / 256));
-    int64_t rps = (job.nsel + n_split - 1) / n_split;
-    rps = (rps + 127) / 128 * 128;
-    n_split = (job.nsel + rps - 1) / rps;
-    const int n_sub = (int)(n_split * 2);
-    int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
-    const int64_t rows_per_sub = (rps + 1) / 2;
-    const bool exhaustive = C >= pow2ceil(rows_per_sub + 64);
-    if (exhaustive) C = pow2ceil(rows_per_sub + 64);
-
-    vs::CandBuf cb;
-    cb.n_sub = n_sub;
-    cb.C = (int)C;
-    const size_t slots = (size_t)job.nq * n_sub * C;
-    CKS(arena_alloc(ctx, slots, &cb.key));
-    CKS(arena_alloc(ctx, slots, &cb.pos));
-    CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
-    CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
-    CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
-
     vs::EnnScanParams sp;
     sp.Q = job.q;
     sp.nq = job.nq;
@@ -190,23 +167,45 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     sp.margin = margin;
     sp.ip = job.ip;
     sp.k = job.k;
-    sp.n_split = (int)n_split;
-    sp.rows_per_split = rps;
-    sp.cb = cb;
-    bool used_tc = false;
+    sp.tau_g = nullptr;
+    const bool use_tc = ctx->opt_enn_kernel != 1 && vs::tc_supported(job.d, job.dtype, job.ip) &&
+                        (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d));
+    bool exhaustive = false;
     {
-    KTimer kt(ctx, job.cls_scan);
-    if (ctx->opt_enn_kernel != 1 && vs::tc_supported(job.d, job.dtype, job.ip) &&
-        (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d))) {
-        int st = vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb);
-        if (st != VS_OK) return st;
-        used_tc = true;
+        KTimer kt(ctx, job.cls_scan);
+        if (use_tc) {
+            CKS(vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive));
+        } else {
+            const int64_t qtiles = (job.nq + 127) / 128;
+            const int64_t target = (int64_t)ctx->sm_count * 4;  // 2 CTAs/SM x 2 waves
+            int64_t n_split = std::max<int64_t>(1, (target + qtiles - 1) / qtiles);
+            n_split = std::min<int64_t>(n_split, std::max<int64_t>(1, (job.nsel + 255) / 256));
+            int64_t rps = (job.nsel + n_split - 1) / n_split;
+            rps = (rps + 127) / 128 * 128;
+            n_split = (job.nsel + rps - 1) / rps;
+            const int n_sub = (int)(n_split * 2);
+            int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
+            const int64_t rows_per_sub = (rps + 1) / 2;
+            exhaustive = C >= pow2ceil(rows_per_sub + 64);
+            if (exhaustive) C = pow2ceil(rows_per_sub + 64);
+            vs::CandBuf cb;
+            cb.n_sub = n_sub;
+            cb.C = (int)C;
+            const size_t slots = (size_t)job.nq * n_sub * C;
+            CKS(arena_alloc(ctx, slots, &cb.key));
+            CKS(arena_alloc(ctx, slots, &cb.pos));
+            CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
+            CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
+            CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
+            sp.n_split = (int)n_split;
+            sp.rows_per_split = rps;
+            sp.cb = cb;
+            if (job.dtype == VS_DTYPE_F32) CK(vs::launch_enn_scan_simt<float>(sp, ctx->stream));
+            else CK(vs::launch_enn_scan_simt<__nv_bfloat16>(sp, ctx->stream));
+        }
     }
-    if (!used_tc) {
-        if (job.dtype == VS_DTYPE_F32) CK(vs::launch_enn_scan_simt<float>(sp, ctx->stream));
-        else CK(vs::launch_enn_scan_simt<__nv_bfloat16>(sp, ctx->stream));
-    }
-    }
+    const bool used_tc = use_tc;
+    const vs::CandBuf cb = sp.cb;
     ctx->stats[VS_STAT_LAST_ENN_KERNEL] = used_tc ? 2 : 1;
     ctx->stats[VS_STAT_LAUNCHES] += 1;
 
@@ -217,7 +216,8 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     rp.ip = job.ip;
     rp.k = job.k;
     rp.cb = sp.cb;
-    rp.margin = used_tc ? sp.margin : margin;
+    rp.margin = sp.margin;
+    rp.tau_g = sp.tau_g;
     rp.rows = job.rows;
     rp.row_map = job.sel;
     rp.id_map = nullptr;
@@ -787,6 +787,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     rp.k = job.k;
     rp.cb = cb;
     rp.margin = margin;
+    rp.tau_g = nullptr;
     rp.rows = v->payload;
     rp.row_map = nullptr;
     rp.id_map = v->list_ids;

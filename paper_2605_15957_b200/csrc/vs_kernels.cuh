@@ -59,6 +59,7 @@ struct EnnScanParams {
     int n_split;
     int64_t rows_per_split;
     CandBuf cb;
+    unsigned* tau_g = nullptr;  // tensor-core path: per-query global admission bound
 };
 template <typename T>
 cudaError_t launch_enn_scan_simt(const EnnScanParams& p, cudaStream_t s);
@@ -93,6 +94,7 @@ struct RerankParams {
     int k;
     CandBuf cb;
     const float* margin;
+    const unsigned* tau_g;      // nullable: per-query orderable admission bound (prefilter)
     const void* rows;           // exact-scoring row source
     const int64_t* row_map;     // pos -> row index in `rows` (nullable: identity)
     const int64_t* id_map;      // pos -> output id (nullable: row index)

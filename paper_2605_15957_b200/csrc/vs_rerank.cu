@@ -18,6 +18,7 @@ namespace {
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
 constexpr int KMAX = 2048;  // == vs_topk_cap()
+constexpr int LCAP = 3072;  // live candidates staged in shared memory per query
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -148,37 +149,86 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     }
     tot = block_sum_ll(tot, sm.red);  // includes a __syncthreads
     const int64_t nslots = (int64_t)nsub * C;
-    // 1. k-th smallest approximate key
-    uint32_t thr_o = 0xffffffffu;
-    if (tot > p.k) {
-        uint32_t lo = 0u, hi = 0xffffffffu;
-        while (lo < hi) {
-            uint32_t mid = lo + ((hi - lo) >> 1);
-            long long c = 0;
-            for (int64_t i = tid; i < nslots; i += NT) {
-                int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
-                if (j < cnts[s]) c += (f2o(ckey[i]) <= mid);
-            }
-            c = block_sum_ll(c, sm.red);
-            if (c >= p.k) hi = mid; else lo = mid + 1;
-        }
-        thr_o = f2o(__fadd_ru(o2f(lo), p.margin[q]));
-    }
-    // 2. survivors
-    if (tid == 0) sm.counter = 0;
-    __syncthreads();
     uint32_t* spos = p.s_pos + q * p.s_cap;
     uint64_t* skey = p.s_key + q * p.s_cap;
     int64_t* sid = p.s_id + q * p.s_cap;
+    const uint32_t pre = p.tau_g ? p.tau_g[q] : 0xffffffffu;
+    // 0. gather the live candidates (key <= prefilter bound) into shared memory
+    float* lkey = reinterpret_cast<float*>(cnts + nsub);
+    uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + LCAP);
+    if (tid == 0) sm.counter = 0;
+    __syncthreads();
     for (int64_t i = tid; i < nslots; i += NT) {
         int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
-        if (j < cnts[s] && f2o(ckey[i]) <= thr_o) {
-            int slot = atomicAdd(&sm.counter, 1);
-            if (slot < p.s_cap) spos[slot] = cpos[i];
+        if (j < cnts[s]) {
+            const float kk = ckey[i];
+            if (f2o(kk) <= pre) {
+                int slot = atomicAdd(&sm.counter, 1);
+                if (slot < LCAP) {
+                    lkey[slot] = kk;
+                    lpos[slot] = cpos[i];
+                }
+            }
         }
     }
     __syncthreads();
-    int64_t ns = sm.counter;
+    const int nl = sm.counter;
+    __syncthreads();
+    int64_t ns = 0;
+    if (nl <= LCAP) {
+        // 1. k-th smallest approximate key, 2. survivors  (shared-memory path)
+        uint32_t thr_o = 0xffffffffu;
+        if (nl > p.k) {
+            uint32_t lo = 0u, hi = pre;
+            while (lo < hi) {
+                uint32_t mid = lo + ((hi - lo) >> 1);
+                long long c = 0;
+                for (int i = tid; i < nl; i += NT) c += (f2o(lkey[i]) <= mid);
+                c = block_sum_ll(c, sm.red);
+                if (c >= p.k) hi = mid; else lo = mid + 1;
+            }
+            thr_o = f2o(__fadd_ru(o2f(lo), p.margin[q]));
+        }
+        if (tid == 0) sm.counter = 0;
+        __syncthreads();
+        for (int i = tid; i < nl; i += NT) {
+            if (f2o(lkey[i]) <= thr_o) {
+                int slot = atomicAdd(&sm.counter, 1);
+                if (slot < p.s_cap) spos[slot] = lpos[i];
+            }
+        }
+        __syncthreads();
+        ns = sm.counter;
+    } else {
+        // 1. k-th smallest approximate key over the buffers (global-memory path)
+        uint32_t thr_o = 0xffffffffu;
+        if (tot > p.k) {
+            uint32_t lo = 0u, hi = pre;
+            while (lo < hi) {
+                uint32_t mid = lo + ((hi - lo) >> 1);
+                long long c = 0;
+                for (int64_t i = tid; i < nslots; i += NT) {
+                    int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
+                    if (j < cnts[s]) c += (f2o(ckey[i]) <= mid);
+                }
+                c = block_sum_ll(c, sm.red);
+                if (c >= p.k) hi = mid; else lo = mid + 1;
+            }
+            thr_o = f2o(__fadd_ru(o2f(lo), p.margin[q]));
+        }
+        // 2. survivors
+        if (tid == 0) sm.counter = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < nslots; i += NT) {
+            int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
+            if (j < cnts[s] && f2o(ckey[i]) <= thr_o) {
+                int slot = atomicAdd(&sm.counter, 1);
+                if (slot < p.s_cap) spos[slot] = cpos[i];
+            }
+        }
+        __syncthreads();
+        ns = sm.counter;
+    }
     if (ns > p.s_cap) {  // cannot re-rank all survivors: re-run with larger buffers
         if (tid == 0) p.cb.overflow[q] = 1;
         ns = p.s_cap;
@@ -203,7 +253,7 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
 template <typename T>
 cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s) {
     if (p.nq == 0) return cudaSuccess;
-    const size_t smem = sizeof(TopkSmem) + (size_t)p.cb.n_sub * sizeof(int);
+    const size_t smem = sizeof(TopkSmem) + (size_t)p.cb.n_sub * sizeof(int) + LCAP * 8 + 16;
     cudaError_t e;
     if (p.ip) {
         e = cudaFuncSetAttribute(k_rerank<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

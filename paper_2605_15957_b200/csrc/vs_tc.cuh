@@ -14,7 +14,7 @@ bool tc_profitable(int64_t nq, int64_t nsel, int d);
 // runs phase A on the tensor cores; fills `cb` (allocated by the callee from
 // the context arena) and may rewrite sp.margin with the tensor-core error bound
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift,
-                CandBuf* cb);
+                CandBuf* cb, bool* exhaustive);
 
 int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, uint64_t seed, int32_t metric,
                   int32_t max_iters, vs_ivf** out);

@@ -1,0 +1,88 @@
+"""The tcgen05 (tensor-core) phase A must produce the same exact results as
+the reference: bf16 candidate scores + rigorous margin + float64 re-rank."""
+
+import numpy as np
+import pytest
+
+import paper_2605_15957_b200 as vs
+from oracle import sqlvs_oracle as O
+from paper_2605_15957_b200 import _native as N
+from paper_2605_15957_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def tc_kernel():
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_ENN_KERNEL, 2)
+    yield ctx
+    ctx.set_option(N.OPT_ENN_KERNEL, 0)
+
+
+def assert_same(nt, ref):
+    assert np.array_equal(nt.query_row, ref.query_row)
+    assert np.array_equal(nt.data_row, ref.data_row)
+    assert np.array_equal(nt.distance, ref.distance)
+
+
+@pytest.mark.parametrize("dim", [64, 100, 384])
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+def test_tc_random_filtered(tc_kernel, dim, metric):
+    rng = np.random.default_rng(dim + (metric == "inner_product"))
+    data = rng.standard_normal((9000, dim)).astype(np.float32)
+    q = rng.standard_normal((150, dim)).astype(np.float32)
+    mask = rng.random(9000) < 0.3
+    for k in (1, 16, 100):
+        nt = vs.enn_search(q, data, vs.SearchParams(k=k), metric=metric, row_filter=mask)
+        assert N.Context.get().stats()[N.STAT_LAST_ENN_KERNEL] == 2
+        assert_same(nt, O.enn_filtered(q, data, mask, k, metric))
+
+
+def test_tc_mixture_d1024(tc_kernel):
+    x = synth.mixture_chunked(40000, 1024, seed=9, chunk=1 << 14)
+    rng = np.random.default_rng(3)
+    c = np.random.default_rng(np.random.SeedSequence([9, 10])).standard_normal((64, 1024))
+    c /= np.linalg.norm(c, axis=1, keepdims=True)
+    q = synth.mixture(rng, c, rng.integers(0, 64, 300), 0.165)
+    mask = rng.random(40000) < 0.1
+    nt = vs.enn_search(q, x, vs.SearchParams(k=100), row_filter=mask)
+    idx = np.arange(0, 300, 23)
+    ref = O.enn_filtered(q[idx], x, mask, 100)
+    got_ids = nt.data_row.reshape(300, 100)[idx].reshape(-1)
+    got_d = nt.distance.reshape(300, 100)[idx].reshape(-1)
+    assert np.array_equal(got_ids, ref.data_row)
+    assert np.array_equal(got_d, ref.distance)
+
+
+def test_tc_goldens(tc_kernel, golden, sf001):
+    g = golden("q15_enn.npz")
+    nt = vs.enn_search(g["query"], sf001["reviews"], vs.SearchParams(k=int(g["k"])), row_filter=g["bitmap"])
+    assert np.array_equal(nt.data_row, g["ids"]) and np.array_equal(nt.distance, g["dist"])
+    for name in ("q11", "q2"):
+        g = golden(f"{name}_enn.npz")
+        nt = vs.enn_search(g["queries"], sf001["images"], vs.SearchParams(k=int(g["k"])),
+                           metric=str(g["metric"]))
+        assert np.array_equal(nt.data_row, g["ids"]) and np.array_equal(nt.distance, g["dist"])
+
+
+def test_tc_random_goldens(tc_kernel, golden):
+    g = golden("random_enn.npz")
+    for t in range(12):
+        seed, nq, nx, dim, k, ip = g[f"t{t}_spec"].tolist()
+        if dim < 8:
+            continue
+        r = np.random.default_rng(seed)
+        data = r.standard_normal((nx, dim)).astype(np.float32)
+        queries = r.standard_normal((nq, dim)).astype(np.float32)
+        nt = vs.enn_search(queries, data, vs.SearchParams(k=k), metric="inner_product" if ip else "squared_l2")
+        assert np.array_equal(nt.data_row, g[f"t{t}_ids"]), t
+        assert np.array_equal(nt.distance, g[f"t{t}_dist"]), t
+
+
+def test_tc_duplicates_and_retry(tc_kernel):
+    base = np.ones((5000, 64), np.float32)
+    base[::3] = 0.5
+    q = np.ones((130, 64), np.float32)
+    nt = vs.enn_search(q, base, vs.SearchParams(k=40))
+    assert_same(nt, O.enn_search(q, base, 40))
