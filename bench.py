@@ -343,9 +343,16 @@ def run_ours(args, cfg):
     kt = ctx.kernel_times(reset=True)
     ctx.set_option(N.OPT_TIMING, 0)
     launches = ctx.stats()[N.STAT_LAUNCHES] - launches0
-    for _ in range(1):
+    survivors = ctx.stats()[N.STAT_SURVIVORS]
+    for _ in range(2):
         step_e2e()
+    ctx.set_option(N.OPT_TIMING, 1)
+    ctx.kernel_times(reset=True)
+    t_host = time.perf_counter()
     ms_e2e = timed(step_e2e, args.steps)
+    t_host = (time.perf_counter() - t_host) * 1e3
+    kt_e2e = ctx.kernel_times(reset=True)
+    ctx.set_option(N.OPT_TIMING, 0)
 
     ms_step = ms / args.steps
     qps = nq * args.steps / (ms / 1e3)
@@ -392,6 +399,9 @@ def run_ours(args, cfg):
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "kernel_ms_per_step": {c: round(v[0] / 1e6 / args.steps, 3) for c, v in kt.items() if v[1]},
+            "e2e_kernel_ms_per_step": {c: round(v[0] / 1e6 / args.steps, 3) for c, v in kt_e2e.items() if v[1]},
+            "e2e_host_ms_per_step": round(t_host / args.steps, 3),
+            "survivors_per_query": round(survivors / nq, 2),
             "roofline": {"bound": "tensor", "kernel": f"enn_scan ({last_kernel})",
                          "achieved": round(achieved, 2) if achieved else None,
                          "peak": peak, "unit": "TFLOP/s",

@@ -218,6 +218,7 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     rp.cb = sp.cb;
     rp.margin = sp.margin;
     rp.tau_g = sp.tau_g;
+    rp.verify = sp.verify;
     rp.rows = job.rows;
     rp.row_map = job.sel;
     rp.id_map = nullptr;
@@ -788,6 +789,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     rp.cb = cb;
     rp.margin = margin;
     rp.tau_g = nullptr;
+    rp.verify = 0;
     rp.rows = v->payload;
     rp.row_map = nullptr;
     rp.id_map = v->list_ids;

@@ -137,14 +137,69 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // cannot make progress: the margin is dropped and entries truncated in
 // position order, and the caller flags the query for a re-run with a larger
 // buffer (`*overflow` = 1).
-__device__ __forceinline__ int warp_compact(float* keys, uint32_t* pos, int n, int k,
-                                            float margin, int limit, float* thr,
-                                            int* overflow) {
+//
+// Buffers of up to 32 x REG_PER_LANE entries are compacted from registers
+// (one load of the keys, then a 32-step bitwise binary search on the
+// register copy); larger buffers fall back to streaming the keys.
+constexpr int COMPACT_REG_PER_LANE = 32;
+
+__device__ __forceinline__ int warp_compact(float* keys, uint32_t* pos, int n, int k, float margin,
+                                            int limit, float* thr, int* overflow) {
     const int lane = threadIdx.x & 31;
-    // k-th smallest key (orderable bits) by bitwise binary search
+    if (n <= 32 * COMPACT_REG_PER_LANE) {
+        // register-resident: one coalesced load of keys and positions, then
+        // selection, counting and compaction without further memory reads
+        uint32_t ko[COMPACT_REG_PER_LANE];
+        uint32_t po[COMPACT_REG_PER_LANE];
+#pragma unroll
+        for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) {
+            const int j = lane + 32 * i;
+            ko[i] = (j < n) ? f2o(keys[j]) : 0xffffffffu;
+            po[i] = (j < n) ? pos[j] : 0u;
+        }
+        uint32_t lo = 0u, hi = 0xffffffffu;
+        while (lo < hi) {
+            const uint32_t mid = lo + ((hi - lo) >> 1);
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) c += (ko[i] <= mid);
+            c = warp_sum(c);  // padding (0xffffffff) only counts at the very top
+            if (c >= k) hi = mid; else lo = mid + 1;
+        }
+        const float kth = o2f(lo);
+        uint32_t to = f2o(__fadd_ru(kth, margin));
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) c += (ko[i] <= to);
+        c = warp_sum(c);
+        if (c > limit) {  // margin set cannot fit: keep the k-th bound, flag a re-run
+            *overflow = 1;
+            to = lo;
+            c = 0;
+#pragma unroll
+            for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) c += (ko[i] <= to);
+            c = warp_sum(c);
+            if (c > limit) c = limit;
+        }
+        __syncwarp();
+        int base = 0;
+#pragma unroll
+        for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) {
+            const bool keep = ko[i] <= to;   // entries are in position order: i-major
+            const unsigned b = __ballot_sync(VS_FULL, keep);
+            const int dst = base + __popc(b & lanemask_lt());
+            if (keep && dst < limit) {
+                keys[dst] = o2f(ko[i]);
+                pos[dst] = po[i];
+            }
+            base += __popc(b);
+        }
+        *thr = o2f(to);
+        return min(base, limit);
+    }
     uint32_t lo = 0u, hi = 0xffffffffu;
     while (lo < hi) {
-        uint32_t mid = lo + ((hi - lo) >> 1);
+        const uint32_t mid = lo + ((hi - lo) >> 1);
         int c = 0;
         for (int j = lane; j < n; j += 32) c += (f2o(keys[j]) <= mid);
         c = warp_sum(c);
@@ -160,14 +215,14 @@ __device__ __forceinline__ int warp_compact(float* keys, uint32_t* pos, int n, i
         if (c <= limit || pass == 1) {
             int base = 0;
             for (int j0 = 0; j0 < n; j0 += 32) {
-                int j = j0 + lane;
+                const int j = j0 + lane;
                 float kk = 0.f;
                 uint32_t pp = 0;
                 bool keep = false;
                 if (j < n) { kk = keys[j]; pp = pos[j]; keep = f2o(kk) <= to; }
-                unsigned b = __ballot_sync(VS_FULL, keep);
+                const unsigned b = __ballot_sync(VS_FULL, keep);
                 __syncwarp();
-                int dst = base + __popc(b & lanemask_lt());
+                const int dst = base + __popc(b & lanemask_lt());
                 if (keep && dst < limit) { keys[dst] = kk; pos[dst] = pp; }
                 base += __popc(b);
                 __syncwarp();
@@ -176,7 +231,7 @@ __device__ __forceinline__ int warp_compact(float* keys, uint32_t* pos, int n, i
             *thr = t;
             return base;
         }
-        t = kth;  // margin cannot fit: fall back to the k-th key, flag below
+        t = kth;  // margin cannot fit: fall back to the k-th key and flag
         *overflow = 1;
     }
     return n;  // unreachable

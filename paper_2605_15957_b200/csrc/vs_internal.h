@@ -75,6 +75,7 @@ struct Arena {
             if (base) cudaFree(base);
             base = nullptr;
             cap = 0;
+            need += need / 4;  // headroom: grow rarely
             cudaError_t e = cudaMalloc(&base, need);
             if (e != cudaSuccess) {
                 cudaGetLastError();

@@ -60,6 +60,7 @@ struct EnnScanParams {
     int64_t rows_per_split;
     CandBuf cb;
     unsigned* tau_g = nullptr;  // tensor-core path: per-query global admission bound
+    int verify = 0;             // phase A kept local top-k only: phase B must verify
 };
 template <typename T>
 cudaError_t launch_enn_scan_simt(const EnnScanParams& p, cudaStream_t s);
@@ -95,6 +96,8 @@ struct RerankParams {
     CandBuf cb;
     const float* margin;
     const unsigned* tau_g;      // nullable: per-query orderable admission bound (prefilter)
+    int verify;                 // tau_g = min local k-th: prefilter at tau_g + margin and
+                                // flag queries whose exact k-th + margin/2 reaches tau_g
     const void* rows;           // exact-scoring row source
     const int64_t* row_map;     // pos -> row index in `rows` (nullable: identity)
     const int64_t* id_map;      // pos -> output id (nullable: row index)

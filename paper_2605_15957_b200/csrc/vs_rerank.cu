@@ -1,14 +1,22 @@
 // Phase B: exact re-rank and tie-rule top-k, plus the cross-shard merge.
 //
-// For each query (one CTA):
-//   1. K* = k-th smallest approximate key over all candidate buffers,
+// For each query (one CTA of 8 warps):
+//   0. gather the live candidates (key <= the query's global admission
+//      bound) from all candidate buffers into shared memory,
+//   1. K* = k-th smallest approximate key,
 //   2. survivors = candidates with key <= K* + margin  (a superset of the
 //      exact top-k by the error bound),
 //   3. exact float64 score of every survivor with the reference's arithmetic
-//      and summation order (np_pairwise, bit-identical to distances.py:54-58),
+//      and summation order (bit-identical to distances.py:54-58): one warp
+//      per survivor row, the row staged in shared memory by coalesced
+//      128-bit loads, numpy's accumulation chains spread over the lanes,
 //   4. exact top-k under the tie rule (key, row id) — select_top,
-//      distances.py:79-94 — by bitwise binary search on the composite key,
-//      then a bitonic sort of the k winners in shared memory.
+//      distances.py:79-94 — by a bitonic sort of the survivors in shared
+//      memory (or a bitwise binary search on the composite key when more
+//      than 2048 survive).
+//
+// Shared memory is one union region reused by steps 0-2 (live candidates),
+// 3 (row staging) and 4 (sort), so several CTAs stay resident per SM.
 #include "vs_common.cuh"
 #include "vs_kernels.cuh"
 
@@ -17,8 +25,25 @@ namespace vs {
 namespace {
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
-constexpr int KMAX = 2048;  // == vs_topk_cap()
-constexpr int LCAP = 3072;  // live candidates staged in shared memory per query
+constexpr int KMAX = 2048;      // == vs_topk_cap(): sort capacity
+constexpr int LCAP = 4096;      // live candidates staged in shared memory per query
+constexpr int MAXLEAF = 32;     // numpy pairwise leaves (>= 64 elements each) -> d <= 2048 on the warp path
+constexpr int WARP_D_MAX = 2048;
+// union of: live candidates (LCAP x 8 B), staged rows (NWARP x d x 4 B),
+// sort buffers (KMAX x 16 B)
+constexpr size_t UNION_BYTES = 32768;
+__host__ __device__ __forceinline__ size_t union_bytes(int d) {
+    const size_t rows = (size_t)NWARP * (size_t)((d + 3) & ~3) * 4;
+    return (d <= WARP_D_MAX && rows > UNION_BYTES) ? rows : UNION_BYTES;
+}
+
+struct Small {
+    long long red[NWARP];
+    int counter;
+    int nleaf;
+    int leaf_off[MAXLEAF];
+    int leaf_n[MAXLEAF];
+};
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -33,92 +58,15 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
     return t;
 }
 
-struct TopkSmem {
-    uint64_t key[KMAX];
-    int64_t id[KMAX];
-    long long red[NWARP];
-    int counter;
-};
-
-// Exact top-k over n entries (orderable key, id) held in global scratch.
-// Writes min(n, k) entries in (key, id) order to out_* (row q).
-__device__ void block_topk_exact(const uint64_t* __restrict__ key, const int64_t* __restrict__ id,
-                                 int64_t n, int k, TopkSmem& sm, int ip, int64_t q,
-                                 int64_t* out_ids, double* out_dist, int32_t* out_ids32,
-                                 int32_t* out_count) {
-    const int tid = threadIdx.x;
-    const int keff = (int)min((int64_t)k, n);
-    uint64_t K = ~0ull;
-    uint64_t I = ~0ull;
-    if (n > k) {
-        // smallest K with count(key <= K) >= k
-        uint64_t lo = 0, hi = ~0ull;
-        while (lo < hi) {
-            uint64_t mid = lo + ((hi - lo) >> 1);
-            long long c = 0;
-            for (int64_t i = tid; i < n; i += NT) c += (key[i] <= mid);
-            c = block_sum_ll(c, sm.red);
-            if (c >= k) hi = mid; else lo = mid + 1;
-        }
-        K = lo;
-        long long clt = 0;
-        for (int64_t i = tid; i < n; i += NT) clt += (key[i] < K);
-        clt = block_sum_ll(clt, sm.red);
-        const long long need = k - clt;  // >= 1 ties at K to take, lowest ids first
-        uint64_t ilo = 0, ihi = ~0ull;
-        while (ilo < ihi) {
-            uint64_t mid = ilo + ((ihi - ilo) >> 1);
-            long long c = 0;
-            for (int64_t i = tid; i < n; i += NT) c += (key[i] == K && (uint64_t)id[i] <= mid);
-            c = block_sum_ll(c, sm.red);
-            if (c >= need) ihi = mid; else ilo = mid + 1;
-        }
-        I = ilo;
-    }
-    if (tid == 0) sm.counter = 0;
-    __syncthreads();
-    for (int64_t i = tid; i < n; i += NT) {
-        uint64_t kk = key[i];
-        uint64_t ii = (uint64_t)id[i];
-        bool win = (n <= k) || kk < K || (kk == K && ii <= I);
-        if (win) {
-            int slot = atomicAdd(&sm.counter, 1);
-            sm.key[slot] = kk;
-            sm.id[slot] = (int64_t)ii;
-        }
-    }
-    __syncthreads();
-    int P = 1;
-    while (P < keff) P <<= 1;
-    for (int i = keff + tid; i < P; i += NT) {
-        sm.key[i] = ~0ull;
-        sm.id[i] = 0x7fffffffffffffffll;
-    }
-    __syncthreads();
-    // bitonic sort of P entries by (key, id)
-    for (int size = 2; size <= P; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = tid; i < P / 2; i += NT) {
-                int lo_i = 2 * i - (i & (stride - 1));
-                int hi_i = lo_i + stride;
-                bool asc = ((lo_i & size) == 0);
-                uint64_t ka = sm.key[lo_i], kb = sm.key[hi_i];
-                int64_t ia = sm.id[lo_i], ib = sm.id[hi_i];
-                bool gt = (ka > kb) || (ka == kb && ia > ib);
-                if (gt == asc) {
-                    sm.key[lo_i] = kb; sm.key[hi_i] = ka;
-                    sm.id[lo_i] = ib; sm.id[hi_i] = ia;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (int r = tid; r < k; r += NT) {
+__device__ __forceinline__ void emit_row(int64_t q, int k, int keff, const uint64_t* skey, const int64_t* sid,
+                                         int ip, int64_t* out_ids, double* out_dist, int32_t* out_ids32,
+                                         int32_t* out_count) {
+    for (int r = threadIdx.x; r < k; r += NT) {
         const int64_t o = q * (int64_t)k + r;
         if (r < keff) {
-            double key_d = o2d(sm.key[r]);
-            if (out_ids) out_ids[o] = sm.id[r];
-            if (out_ids32) out_ids32[o] = (int32_t)sm.id[r];
+            const double key_d = o2d(skey[r]);
+            if (out_ids) out_ids[o] = sid[r];
+            if (out_ids32) out_ids32[o] = (int32_t)sid[r];
             if (out_dist) out_dist[o] = ip ? -key_d : key_d;
         } else {
             if (out_ids) out_ids[o] = -1;
@@ -126,48 +74,280 @@ __device__ void block_topk_exact(const uint64_t* __restrict__ key, const int64_t
             if (out_dist) out_dist[o] = __longlong_as_double(0x7ff8000000000000ll);
         }
     }
-    if (tid == 0 && out_count) out_count[q] = keff;
+    if (threadIdx.x == 0 && out_count) out_count[q] = keff;
+}
+
+// bitonic sort of P (power of two) (key, id) pairs in shared memory
+__device__ void bitonic_sort(uint64_t* key, int64_t* id, int P) {
+    const int tid = threadIdx.x;
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < P / 2; i += NT) {
+                const int lo_i = 2 * i - (i & (stride - 1));
+                const int hi_i = lo_i + stride;
+                const bool asc = ((lo_i & size) == 0);
+                const uint64_t ka = key[lo_i], kb = key[hi_i];
+                const int64_t ia = id[lo_i], ib = id[hi_i];
+                const bool gt = (ka > kb) || (ka == kb && ia > ib);
+                if (gt == asc) {
+                    key[lo_i] = kb; key[hi_i] = ka;
+                    id[lo_i] = ib; id[hi_i] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Exact top-k over n (orderable key, id) entries in global scratch. Uses the
+// union region `u` (>= KMAX * 16 bytes) for the final sort.
+__device__ void block_topk_exact(const uint64_t* __restrict__ key, const int64_t* __restrict__ id, int64_t n,
+                                 int k, Small& sm, unsigned char* u, int ip, int64_t q, int64_t* out_ids,
+                                 double* out_dist, int32_t* out_ids32, int32_t* out_count) {
+    const int tid = threadIdx.x;
+    uint64_t* skey = reinterpret_cast<uint64_t*>(u);
+    int64_t* sid = reinterpret_cast<int64_t*>(u + KMAX * 8);
+    const int keff = (int)min((int64_t)k, n);
+    if (n <= KMAX) {
+        int P = 1;
+        while (P < n) P <<= 1;
+        for (int i = tid; i < P; i += NT) {
+            skey[i] = i < n ? key[i] : ~0ull;
+            sid[i] = i < n ? id[i] : 0x7fffffffffffffffll;
+        }
+        __syncthreads();
+        bitonic_sort(skey, sid, P);
+        emit_row(q, k, keff, skey, sid, ip, out_ids, out_dist, out_ids32, out_count);
+        __syncthreads();
+        return;
+    }
+    // smallest K with count(key <= K) >= k, then the needed ties at K by id
+    uint64_t lo = 0, hi = ~0ull;
+    while (lo < hi) {
+        const uint64_t mid = lo + ((hi - lo) >> 1);
+        long long c = 0;
+        for (int64_t i = tid; i < n; i += NT) c += (key[i] <= mid);
+        c = block_sum_ll(c, sm.red);
+        if (c >= k) hi = mid; else lo = mid + 1;
+    }
+    const uint64_t K = lo;
+    long long clt = 0;
+    for (int64_t i = tid; i < n; i += NT) clt += (key[i] < K);
+    clt = block_sum_ll(clt, sm.red);
+    const long long need = k - clt;
+    uint64_t ilo = 0, ihi = ~0ull;
+    while (ilo < ihi) {
+        const uint64_t mid = ilo + ((ihi - ilo) >> 1);
+        long long c = 0;
+        for (int64_t i = tid; i < n; i += NT) c += (key[i] == K && (uint64_t)id[i] <= mid);
+        c = block_sum_ll(c, sm.red);
+        if (c >= need) ihi = mid; else ilo = mid + 1;
+    }
+    const uint64_t I = ilo;
+    if (tid == 0) sm.counter = 0;
     __syncthreads();
+    for (int64_t i = tid; i < n; i += NT) {
+        const uint64_t kk = key[i];
+        const uint64_t ii = (uint64_t)id[i];
+        if (kk < K || (kk == K && ii <= I)) {
+            const int slot = atomicAdd(&sm.counter, 1);
+            skey[slot] = kk;
+            sid[slot] = (int64_t)ii;
+        }
+    }
+    __syncthreads();
+    int P = 1;
+    while (P < keff) P <<= 1;
+    for (int i = keff + tid; i < P; i += NT) {
+        skey[i] = ~0ull;
+        sid[i] = 0x7fffffffffffffffll;
+    }
+    __syncthreads();
+    bitonic_sort(skey, sid, P);
+    emit_row(q, k, keff, skey, sid, ip, out_ids, out_dist, out_ids32, out_count);
+    __syncthreads();
+}
+
+// leaves of numpy's pairwise recursion for a length-d reduction, left to right
+__device__ void np_leaves(int d, Small& S) {
+    int st_off[16], st_n[16];
+    int sp = 0, nl = 0;
+    st_off[0] = 0;
+    st_n[0] = d;
+    while (sp >= 0) {
+        const int off = st_off[sp], m = st_n[sp];
+        --sp;
+        if (m <= 128) {
+            if (nl < MAXLEAF) {
+                S.leaf_off[nl] = off;
+                S.leaf_n[nl] = m;
+            }
+            ++nl;
+            continue;
+        }
+        int n2 = m / 2;
+        n2 -= n2 % 8;
+        ++sp;  // right first, so the left half is expanded first
+        st_off[sp] = off + n2;
+        st_n[sp] = m - n2;
+        ++sp;
+        st_off[sp] = off;
+        st_n[sp] = n2;
+    }
+    S.nleaf = nl;
+}
+
+// the recursion's combine order applied to precomputed leaf values
+__device__ double np_combine(const double* leafv, int d) {
+    if (d <= 128) return leafv[0];
+    int st_n[16], st_state[16];
+    double st_left[16];
+    int sp = 0, next = 0;
+    st_n[0] = d;
+    st_state[0] = 0;
+    double ret = 0.0;
+    while (sp >= 0) {
+        const int m = st_n[sp];
+        if (m <= 128) {
+            ret = leafv[next++];
+            --sp;
+            continue;
+        }
+        int n2 = m / 2;
+        n2 -= n2 % 8;
+        if (st_state[sp] == 0) {
+            st_state[sp] = 1;
+            ++sp;
+            st_n[sp] = n2;
+            st_state[sp] = 0;
+        } else if (st_state[sp] == 1) {
+            st_left[sp] = ret;
+            st_state[sp] = 2;
+            ++sp;
+            st_n[sp] = m - n2;
+            st_state[sp] = 0;
+        } else {
+            ret = __dadd_rn(st_left[sp], ret);
+            --sp;
+        }
+    }
+    return ret;
+}
+
+template <bool IP>
+__device__ __forceinline__ double term_sm(const float* q, const float* x, int i) {
+    const double a = (double)q[i], b = (double)x[i];
+    if (IP) return __dmul_rn(a, b);
+    const double t = __dsub_rn(a, b);
+    return __dmul_rn(t, t);
+}
+
+// Exact float64 score of one staged row by one warp: lanes run numpy's
+// 8-way-unrolled accumulation chains (elements off + j + 8m, in order),
+// then fold each leaf's chains in numpy's order, and lane 0 applies the
+// recursion's combine tree. Bit-identical to np_pairwise.
+template <bool IP>
+__device__ double warp_np_score(const float* q, const float* x, int d, const Small& S, double* cbuf,
+                                double* lbuf, int lane) {
+    const int nleaf = S.nleaf;
+    const int nch = nleaf * 8;
+    for (int c = lane; c < nch; c += 32) {
+        const int L = c >> 3, j = c & 7;
+        const int off = S.leaf_off[L], n = S.leaf_n[L];
+        const int lim = n - (n % 8);
+        double r = term_sm<IP>(q, x, off + j);
+        for (int i = 8 + j; i < lim; i += 8) r = __dadd_rn(r, term_sm<IP>(q, x, off + i));
+        cbuf[c] = r;
+    }
+    __syncwarp();
+    for (int L = lane; L < nleaf; L += 32) {
+        const double* cb = cbuf + L * 8;
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(cb[0], cb[1]), __dadd_rn(cb[2], cb[3])),
+                               __dadd_rn(__dadd_rn(cb[4], cb[5]), __dadd_rn(cb[6], cb[7])));
+        const int off = S.leaf_off[L], n = S.leaf_n[L];
+        for (int i = n - (n % 8); i < n; ++i) res = __dadd_rn(res, term_sm<IP>(q, x, off + i));
+        lbuf[L] = res;
+    }
+    __syncwarp();
+    double sc = 0.0;
+    if (lane == 0) sc = np_combine(lbuf, d);
+    sc = __shfl_sync(VS_FULL, sc, 0);
+    return sc;
+}
+
+// stage one row (float or bf16) into shared memory as floats, coalesced
+template <typename T>
+__device__ __forceinline__ void stage_row(const T* __restrict__ src, float* dst, int d, int lane) {
+    if (sizeof(T) == 4 && (d % 4) == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (int i = lane; i < d / 4; i += 32) d4[i] = __ldg(s4 + i);
+    } else {
+        for (int i = lane; i < d; i += 32) dst[i] = ld_elem(src + i);
+    }
 }
 }  // namespace
 
 template <typename T, bool IP>
 __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    TopkSmem& sm = *reinterpret_cast<TopkSmem*>(smraw);
-    int* cnts = reinterpret_cast<int*>(smraw + sizeof(TopkSmem));
-    const int tid = threadIdx.x;
+    Small& sm = *reinterpret_cast<Small*>(smraw);
+    unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));       // union region
+    double* cbuf = reinterpret_cast<double*>(u + union_bytes(p.d));          // [NWARP][8*MAXLEAF]
+    double* lbuf = cbuf + NWARP * 8 * MAXLEAF;                               // [NWARP][MAXLEAF]
+    float* qs = reinterpret_cast<float*>(lbuf + NWARP * MAXLEAF);            // [d]
+    int* cnts = reinterpret_cast<int*>(qs + ((p.d + 3) & ~3));               // [nsub]
+
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const int64_t q = blockIdx.x;
     const int C = p.cb.C, nsub = p.cb.n_sub;
-    const float* ckey = p.cb.key + q * nsub * (int64_t)C;
-    const uint32_t* cpos = p.cb.pos + q * nsub * (int64_t)C;
+    const int d = p.d;
+    const bool warp_path = d >= 8 && d <= WARP_D_MAX;
+    if (tid == 0 && warp_path) np_leaves(d, sm);
+    const float* qg = p.Q + q * (int64_t)d;
+    for (int i = tid; i < d; i += NT) qs[i] = qg[i];
     long long tot = 0;
     for (int s = tid; s < nsub; s += NT) {
-        int c = p.cb.cnt[q * nsub + s];
+        const int c = p.cb.cnt[q * nsub + s];
         cnts[s] = c;
         tot += c;
     }
-    tot = block_sum_ll(tot, sm.red);  // includes a __syncthreads
-    const int64_t nslots = (int64_t)nsub * C;
+    tot = block_sum_ll(tot, sm.red);  // includes __syncthreads
+    const float* ckey = p.cb.key + q * nsub * (int64_t)C;
+    const uint32_t* cpos = p.cb.pos + q * nsub * (int64_t)C;
     uint32_t* spos = p.s_pos + q * p.s_cap;
     uint64_t* skey = p.s_key + q * p.s_cap;
     int64_t* sid = p.s_id + q * p.s_cap;
-    const uint32_t pre = p.tau_g ? p.tau_g[q] : 0xffffffffu;
-    // 0. gather the live candidates (key <= prefilter bound) into shared memory
-    float* lkey = reinterpret_cast<float*>(cnts + nsub);
-    uint32_t* lpos = reinterpret_cast<uint32_t*>(lkey + LCAP);
+    const uint32_t tg = p.tau_g ? p.tau_g[q] : 0xffffffffu;
+    // verify mode: tau_g is the smallest local k-th key, an upper bound on the
+    // global one; survivors need key <= K* + margin <= tau_g + margin
+    const uint32_t pre = (p.verify && tg != 0xffffffffu) ? f2o(__fadd_ru(o2f(tg), p.margin[q])) : tg;
+
+    // 0. live candidates -> shared memory (one warp per buffer, coalesced)
+    float* lkey = reinterpret_cast<float*>(u);
+    uint32_t* lpos = reinterpret_cast<uint32_t*>(u + LCAP * 4);
     if (tid == 0) sm.counter = 0;
     __syncthreads();
-    for (int64_t i = tid; i < nslots; i += NT) {
-        int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
-        if (j < cnts[s]) {
-            const float kk = ckey[i];
-            if (f2o(kk) <= pre) {
-                int slot = atomicAdd(&sm.counter, 1);
-                if (slot < LCAP) {
-                    lkey[slot] = kk;
-                    lpos[slot] = cpos[i];
-                }
+    for (int s = w; s < nsub; s += NWARP) {
+        const int cs = cnts[s];
+        for (int j0 = 0; j0 < cs; j0 += 32) {
+            const int j = j0 + lane;
+            float kk = 0.f;
+            uint32_t pp = 0;
+            bool live = false;
+            if (j < cs) {
+                kk = ckey[(int64_t)s * C + j];
+                live = f2o(kk) <= pre;
+                if (live) pp = cpos[(int64_t)s * C + j];
+            }
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            int base = 0;
+            if (lane == 0 && b) base = atomicAdd(&sm.counter, __popc(b));
+            base = __shfl_sync(VS_FULL, base, 0);
+            const int slot = base + __popc(b & lanemask_lt());
+            if (live && slot < LCAP) {
+                lkey[slot] = kk;
+                lpos[slot] = pp;
             }
         }
     }
@@ -176,12 +356,12 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     __syncthreads();
     int64_t ns = 0;
     if (nl <= LCAP) {
-        // 1. k-th smallest approximate key, 2. survivors  (shared-memory path)
+        // 1. k-th smallest approximate key  2. survivors (shared-memory path)
         uint32_t thr_o = 0xffffffffu;
         if (nl > p.k) {
             uint32_t lo = 0u, hi = pre;
             while (lo < hi) {
-                uint32_t mid = lo + ((hi - lo) >> 1);
+                const uint32_t mid = lo + ((hi - lo) >> 1);
                 long long c = 0;
                 for (int i = tid; i < nl; i += NT) c += (f2o(lkey[i]) <= mid);
                 c = block_sum_ll(c, sm.red);
@@ -193,67 +373,102 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
         __syncthreads();
         for (int i = tid; i < nl; i += NT) {
             if (f2o(lkey[i]) <= thr_o) {
-                int slot = atomicAdd(&sm.counter, 1);
+                const int slot = atomicAdd(&sm.counter, 1);
                 if (slot < p.s_cap) spos[slot] = lpos[i];
             }
         }
         __syncthreads();
         ns = sm.counter;
     } else {
-        // 1. k-th smallest approximate key over the buffers (global-memory path)
+        // global-memory path (very wide near-tie sets)
         uint32_t thr_o = 0xffffffffu;
         if (tot > p.k) {
             uint32_t lo = 0u, hi = pre;
             while (lo < hi) {
-                uint32_t mid = lo + ((hi - lo) >> 1);
+                const uint32_t mid = lo + ((hi - lo) >> 1);
                 long long c = 0;
-                for (int64_t i = tid; i < nslots; i += NT) {
-                    int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
-                    if (j < cnts[s]) c += (f2o(ckey[i]) <= mid);
-                }
+                for (int s = w; s < nsub; s += NWARP)
+                    for (int j = lane; j < cnts[s]; j += 32) c += (f2o(ckey[(int64_t)s * C + j]) <= mid);
                 c = block_sum_ll(c, sm.red);
                 if (c >= p.k) hi = mid; else lo = mid + 1;
             }
             thr_o = f2o(__fadd_ru(o2f(lo), p.margin[q]));
         }
-        // 2. survivors
         if (tid == 0) sm.counter = 0;
         __syncthreads();
-        for (int64_t i = tid; i < nslots; i += NT) {
-            int s = (int)(i / C), j = (int)(i - (int64_t)s * C);
-            if (j < cnts[s] && f2o(ckey[i]) <= thr_o) {
-                int slot = atomicAdd(&sm.counter, 1);
-                if (slot < p.s_cap) spos[slot] = cpos[i];
-            }
-        }
+        for (int s = w; s < nsub; s += NWARP)
+            for (int j = lane; j < cnts[s]; j += 32)
+                if (f2o(ckey[(int64_t)s * C + j]) <= thr_o) {
+                    const int slot = atomicAdd(&sm.counter, 1);
+                    if (slot < p.s_cap) spos[slot] = cpos[(int64_t)s * C + j];
+                }
         __syncthreads();
         ns = sm.counter;
     }
+    __syncthreads();
     if (ns > p.s_cap) {  // cannot re-rank all survivors: re-run with larger buffers
         if (tid == 0) p.cb.overflow[q] = 1;
         ns = p.s_cap;
     }
-    // 3. exact float64 scores
+
+    // 3. exact float64 scores (bit-identical to the reference)
     const T* rows = reinterpret_cast<const T*>(p.rows);
-    const float* qv = p.Q + q * (int64_t)p.d;
-    for (int64_t i = tid; i < ns; i += NT) {
-        const uint32_t ps = spos[i];
-        const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
-        const double sc = np_pairwise<T, IP>(qv, rows + r * (int64_t)p.d, p.d);
-        skey[i] = d2o(IP ? -sc : sc);
-        sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+    if (warp_path) {
+        float* xw = reinterpret_cast<float*>(u) + (size_t)w * d;
+        double* cb = cbuf + w * 8 * MAXLEAF;
+        double* lb = lbuf + w * MAXLEAF;
+        for (int64_t i = w; i < ns; i += NWARP) {
+            const uint32_t ps = spos[i];
+            const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
+            stage_row<T>(rows + r * (int64_t)d, xw, d, lane);
+            __syncwarp();
+            const double sc = warp_np_score<IP>(qs, xw, d, sm, cb, lb, lane);
+            if (lane == 0) {
+                skey[i] = d2o(IP ? -sc : sc);
+                sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+            }
+            __syncwarp();
+        }
+    } else {
+        for (int64_t i = tid; i < ns; i += NT) {
+            const uint32_t ps = spos[i];
+            const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
+            const double sc = np_pairwise<T, IP>(qs, rows + r * (int64_t)d, d);
+            skey[i] = d2o(IP ? -sc : sc);
+            sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+        }
     }
     __syncthreads();
     if (tid == 0 && p.n_survivors) atomicAdd(p.n_survivors, (unsigned long long)ns);
     // 4. exact tie-rule top-k
-    block_topk_exact(skey, sid, ns, p.k, sm, IP, q, p.out_ids, p.out_dist, p.out_ids32,
-                     p.out_count);
+    block_topk_exact(skey, sid, ns, p.k, sm, u, IP, q, p.out_ids, p.out_dist, p.out_ids32, p.out_count);
+    // 5. verification of the local-top-k pass: every dropped candidate e had
+    //    approx key > tau_g, hence exact key > tau_g - margin/2; the result is
+    //    exact iff the k-th exact key + margin/2 < tau_g. Otherwise re-run.
+    if (p.verify && tg != 0xffffffffu && tid == 0) {
+        const int keff = (int)min((int64_t)p.k, ns);
+        const uint64_t* sk = reinterpret_cast<const uint64_t*>(u);  // sorted keys left by the top-k
+        double kth = keff > 0 ? o2d(sk[keff - 1]) : 0.0;             // exact key (-score for IP)
+        if (!IP) {
+            double qq = 0.0;
+            for (int i = 0; i < d; ++i) qq += (double)qs[i] * (double)qs[i];
+            kth -= qq * (1.0 + 1e-12);  // approx keys omit ||q||^2
+        }
+        const double bound = (double)o2f(tg) - 0.5 * (double)p.margin[q];
+        const double slack = fabs(bound) * 1e-6 + 1e-12;
+        if (keff < p.k || !(kth < bound - slack)) p.cb.overflow[q] = 1;
+    }
+}
+
+static size_t rerank_smem(int d, int nsub) {
+    return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d) + (size_t)NWARP * 8 * MAXLEAF * 8 +
+           (size_t)NWARP * MAXLEAF * 8 + (size_t)((d + 3) & ~3) * 4 + (size_t)nsub * 4 + 16;
 }
 
 template <typename T>
 cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s) {
     if (p.nq == 0) return cudaSuccess;
-    const size_t smem = sizeof(TopkSmem) + (size_t)p.cb.n_sub * sizeof(int) + LCAP * 8 + 16;
+    const size_t smem = rerank_smem(p.d, p.cb.n_sub);
     cudaError_t e;
     if (p.ip) {
         e = cudaFuncSetAttribute(k_rerank<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -272,7 +487,8 @@ template cudaError_t launch_rerank<__nv_bfloat16>(const RerankParams&, cudaStrea
 // ---- cross-shard merge ------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) k_merge(MergeParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    TopkSmem& sm = *reinterpret_cast<TopkSmem*>(smraw);
+    Small& sm = *reinterpret_cast<Small*>(smraw);
+    unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));
     const int64_t q = blockIdx.x;
     const int tid = threadIdx.x;
     const int64_t cap = (int64_t)p.nparts * p.k_in;
@@ -281,11 +497,11 @@ __global__ void __launch_bounds__(NT) k_merge(MergeParams p) {
     if (tid == 0) sm.counter = 0;
     __syncthreads();
     for (int64_t i = tid; i < cap; i += NT) {
-        int g = (int)(i / p.k_in), j = (int)(i - (int64_t)g * p.k_in);
+        const int g = (int)(i / p.k_in), j = (int)(i - (int64_t)g * p.k_in);
         if (j < p.counts[(int64_t)g * p.nq + q]) {
             const int64_t src = ((int64_t)g * p.nq + q) * p.k_in + j;
             const double dd = p.dist[src];
-            int slot = atomicAdd(&sm.counter, 1);
+            const int slot = atomicAdd(&sm.counter, 1);
             skey[slot] = d2o(p.ip ? -dd : dd);
             sid[slot] = p.ids[src];
         }
@@ -293,12 +509,12 @@ __global__ void __launch_bounds__(NT) k_merge(MergeParams p) {
     __syncthreads();
     const int64_t n = sm.counter;
     __syncthreads();
-    block_topk_exact(skey, sid, n, p.k, sm, p.ip, q, p.out_ids, p.out_dist, nullptr, p.out_count);
+    block_topk_exact(skey, sid, n, p.k, sm, u, p.ip, q, p.out_ids, p.out_dist, nullptr, p.out_count);
 }
 
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t s) {
     if (p.nq == 0) return cudaSuccess;
-    const size_t smem = sizeof(TopkSmem);
+    const size_t smem = ((sizeof(Small) + 127) & ~size_t(127)) + UNION_BYTES;
     cudaError_t e = cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_merge<<<(unsigned)p.nq, NT, smem, s>>>(p);

@@ -23,6 +23,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "vs_common.cuh"
 #include "vs_kernels.cuh"
@@ -40,8 +42,9 @@ constexpr int NSTAGE = 4;
 constexpr int A_BYTES = BM * BK * 2;    // 16 KB
 constexpr int B_BYTES = BN * BK * 2;    // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NTHREADS = 256;           // 8 warps
-constexpr int EPI_WARP0 = 4;            // warps 4..7 drain TMEM lanes 0..127
+constexpr int NTHREADS = 384;           // 12 warps
+constexpr int EPI_WARP0 = 4;            // warps 4..11 drain TMEM (2 per lane quadrant)
+constexpr int EPI_THREADS = 256;
 constexpr int TMEM_COLS = 512;          // 2 accumulators x 256 fp32 columns
 
 struct Smem {
@@ -51,7 +54,6 @@ struct Smem {
     uint64_t tfull[2];
     uint64_t tempty[2];
     uint32_t tmem_base;
-    float xn[2][BN];
 };
 constexpr size_t SMEM_BYTES = 1024 + (size_t)NSTAGE * STAGE_BYTES + sizeof(Smem);
 
@@ -70,6 +72,8 @@ struct Params {
     int ip;
     int k;
     CandBuf cb;
+    unsigned long long* dbg;  // nullable: [8] stall / work counters (VS_TC_DEBUG=1)
+    int topk_mode;            // 1: keep the local top-k only (phase B verifies); 0: keep the margin band
 };
 
 // ---- PTX helpers ---------------------------------------------------------------------------------
@@ -152,12 +156,26 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         : "r"(taddr))
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait for outstanding TMEM loads, tying the destination registers to the wait
+// so the compiler cannot consume them earlier
+__device__ __forceinline__ void tmem_wait_ld_regs(uint32_t* r) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                   "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                   "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+                   "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+                   "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
 
 // ---- the kernel --------------------------------------------------------------------------------------
+template <bool IP>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_enn_scan_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   Params p) {
     extern __shared__ __align__(1024) unsigned char smraw[];
+    __shared__ __align__(16) float xn_w[8][BN / 2];  // per epilogue warp: its column half's row norms
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     Smem& S = *reinterpret_cast<Smem*>(base + (size_t)NSTAGE * STAGE_BYTES);
@@ -172,7 +190,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&S.tfull[i], 1);
-            mbar_init(&S.tempty[i], BM);
+            mbar_init(&S.tempty[i], EPI_THREADS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -192,6 +210,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            long long w_empty = 0;
             for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
                 const int qt = (int)(it % p.qtiles);
                 const int64_t s = it / p.qtiles;
@@ -199,7 +218,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
                 for (int64_t t = t0; t < t1; ++t) {
                     for (int kb = 0; kb < p.kblocks; ++kb) {
+                        const long long c0 = p.dbg ? clock64() : 0;
                         mbar_wait(&S.empty[stage], phase ^ 1);
+                        if (p.dbg) w_empty += clock64() - c0;
                         unsigned char* sa = base + (size_t)stage * STAGE_BYTES;
                         mbar_expect_tx(&S.full[stage], STAGE_BYTES);
                         tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, qt * BM);
@@ -208,6 +229,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
             }
+            if (p.dbg) atomicAdd(&p.dbg[0], (unsigned long long)w_empty);
         }
     } else if (warp == 1) {
         // ===== MMA issuer (single thread) =====
@@ -216,17 +238,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t tcount = 0;
+            long long w_full = 0, w_tempty = 0;
             for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
                 const int64_t s = it / p.qtiles;
                 const int64_t t0 = s * p.tiles_per_split;
                 const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
                 for (int64_t t = t0; t < t1; ++t, ++tcount) {
                     const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
+                    long long c0 = p.dbg ? clock64() : 0;
                     mbar_wait(&S.tempty[acc], aph ^ 1);
+                    if (p.dbg) w_tempty += clock64() - c0;
                     tc_fence_after();
                     const uint32_t dt = tmem + acc * BN;
                     for (int kb = 0; kb < p.kblocks; ++kb) {
+                        c0 = p.dbg ? clock64() : 0;
                         mbar_wait(&S.full[stage], phase);
+                        if (p.dbg) w_full += clock64() - c0;
                         tc_fence_after();
                         const uint32_t sa = smem_u32(base + (size_t)stage * STAGE_BYTES);
                         const uint32_t sb = sa + A_BYTES;
@@ -241,91 +268,179 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mma_commit(&S.tfull[acc]);
                 }
             }
+            if (p.dbg) {
+                atomicAdd(&p.dbg[1], (unsigned long long)w_full);
+                atomicAdd(&p.dbg[2], (unsigned long long)w_tempty);
+            }
         }
     } else if (warp >= EPI_WARP0) {
         // ===== epilogue: TMEM -> keys -> candidate buffers =====
-        const int et = threadIdx.x - EPI_WARP0 * 32;     // 0..127 == TMEM lane == tile row
-        const int quad = warp - EPI_WARP0;               // lane quadrant
+        // 8 warps: warp w drains TMEM lane quadrant (w % 4) for column half
+        // (w - 4) / 4, so each query row is served by two threads (two
+        // candidate buffers, subs 2s and 2s+1) and two warps share each SMSP.
+        const int et = threadIdx.x - EPI_WARP0 * 32;     // 0..255
+        const int row = et & (BM - 1);                   // TMEM lane == tile row
+        const int half = et >> 7;                        // column half
+        const int quad = warp & 3;                       // lane quadrant
         const int C = p.cb.C;
         uint32_t tcount = 0;
+        long long w_tfull = 0, c_comp = 0, n_comp = 0, n_app = 0;
+        // software-pipelined per-tile inputs: the next tile's row norms (4 per
+        // lane = the warp's column half) and the next tile's admission bound
+        auto norms4 = [&](int64_t r0n) -> float4 {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (IP) return v;
+            const int64_t i = r0n + half * (BN / 2) + lane * 4;
+            if (i + 3 < p.nsel) {
+                v = __ldg(reinterpret_cast<const float4*>(p.xn + i));
+            } else {
+                v.x = i + 0 < p.nsel ? __ldg(p.xn + i + 0) : 0.f;
+                v.y = i + 1 < p.nsel ? __ldg(p.xn + i + 1) : 0.f;
+                v.z = i + 2 < p.nsel ? __ldg(p.xn + i + 2) : 0.f;
+                v.w = i + 3 < p.nsel ? __ldg(p.xn + i + 3) : 0.f;
+            }
+            return v;
+        };
+        float* xw = xn_w[warp - EPI_WARP0];
+        float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
+        unsigned pf_tau = 0xffffffffu;
+        {
+            const int64_t it0 = blockIdx.x;
+            if (it0 < nitems) {
+                pf = norms4((it0 / p.qtiles) * p.tiles_per_split * BN);
+                const int64_t q0 = (int64_t)(it0 % p.qtiles) * BM + row;
+                if (q0 < p.nq) pf_tau = __ldcg(p.tau_g + q0);
+            }
+        }
         for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
             const int qt = (int)(it % p.qtiles);
             const int64_t s = it / p.qtiles;
             const int64_t t0 = s * p.tiles_per_split;
             const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-            const int64_t q = (int64_t)qt * BM + et;
+            const int64_t q = (int64_t)qt * BM + row;
             const bool qv = q < p.nq;
-            const int64_t cbase = qv ? ((q * p.cb.n_sub + s) * (int64_t)C) : 0;
+            const int64_t sub = s * 2 + half;
+            const int64_t cbase = qv ? ((q * p.cb.n_sub + sub) * (int64_t)C) : 0;
             float* ckey = p.cb.key + cbase;
             uint32_t* cpos = p.cb.pos + cbase;
             const float qmargin = qv ? p.margin[q] : 0.f;
             int cnt = 0;
             int ovf = 0;
+            // geometric compaction schedule, checked once per tile before any TMEM
+            // data is live: compact when the next half-tile (<= 128 appends) could
+            // push the buffer past lim (2k + 64 initially, then 2x the kept count)
+            const int cap_t = C - BN / 2;
+            const int lim0 = 2 * p.k + 64;
+            int lim = lim0;
             float tau = __int_as_float(0x7f800000);
             for (int64_t t = t0; t < t1; ++t, ++tcount) {
                 const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
                 const int64_t r0 = t * BN;
                 const int ncols = (int)min((int64_t)BN, p.nsel - r0);
-                // stage the tile's row norms (L2) while the MMA runs
-                float* xs = S.xn[acc];
-                if (!p.ip) {
-                    for (int c = et; c < BN; c += BM) xs[c] = (c < ncols) ? p.xn[r0 + c] : 0.f;
+                if (!IP) *reinterpret_cast<float4*>(xw + lane * 4) = pf;
+                __syncwarp();
+                if (qv) tau = fminf(tau, o2f(pf_tau));
+                {   // prefetch for the next tile of this CTA's sequence
+                    int64_t tn = t + 1, itn = it;
+                    if (tn >= t1) {
+                        itn = it + gridDim.x;
+                        tn = (itn / p.qtiles) * p.tiles_per_split;
+                    }
+                    if (itn < nitems) {
+                        pf = norms4(tn * BN);
+                        const int64_t qn = (int64_t)(itn % p.qtiles) * BM + row;
+                        pf_tau = (qn < p.nq) ? __ldcg(p.tau_g + qn) : 0xffffffffu;
+                    }
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (qv) tau = fminf(tau, o2f(p.tau_g[q]));
-                mbar_wait(&S.tfull[acc], aph);
-                tc_fence_after();
-                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN;
-#pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
-                    // room for 32 appends; compact full buffers warp-cooperatively
-                    {
-                        unsigned m = __ballot_sync(VS_FULL, qv && cnt > C - 32);
-                        while (m) {
-                            const int l = __ffs(m) - 1;
-                            m &= m - 1;
-                            const int lc = __shfl_sync(VS_FULL, cnt, l);
-                            const float lmar = __shfl_sync(VS_FULL, qmargin, l);
-                            const int lo32 = __shfl_sync(VS_FULL, (int)(cbase & 0xffffffff), l);
-                            const int hi32 = __shfl_sync(VS_FULL, (int)(cbase >> 32), l);
-                            const int64_t lb = ((int64_t)(uint32_t)hi32 << 32) | (uint32_t)lo32;
-                            float nthr = 0.f;
-                            int lov = 0;
-                            const int nc = warp_compact(p.cb.key + lb, p.cb.pos + lb, lc, p.k, lmar, C - 32,
-                                                        &nthr, &lov);
-                            if (lane == l) {
-                                cnt = nc;
-                                tau = fminf(tau, nthr);
-                                ovf |= lov;
-                                atomicMin(&p.tau_g[q], f2o(tau));
-                            }
+                {   // compaction (warp-cooperative, one buffer at a time)
+                    unsigned m = __ballot_sync(VS_FULL, qv && cnt > min(lim, cap_t));
+                    const long long cc0 = (p.dbg && m) ? clock64() : 0;
+                    if (p.dbg && lane == 0) n_comp += __popc(m);
+                    while (m) {
+                        const int l = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int lc = __shfl_sync(VS_FULL, cnt, l);
+                        const float lmar = __shfl_sync(VS_FULL, qmargin, l);
+                        const int lo32 = __shfl_sync(VS_FULL, (int)(cbase & 0xffffffff), l);
+                        const int hi32 = __shfl_sync(VS_FULL, (int)(cbase >> 32), l);
+                        const int64_t lb = ((int64_t)(uint32_t)hi32 << 32) | (uint32_t)lo32;
+                        float nthr = 0.f;
+                        int lov = 0;
+                        const int nc = warp_compact(p.cb.key + lb, p.cb.pos + lb, lc, p.k,
+                                                    p.topk_mode ? 0.f : lmar, cap_t, &nthr, &lov);
+                        if (lane == l) {
+                            cnt = nc;
+                            tau = fminf(tau, nthr);
+                            ovf |= lov;
+                            lim = max(lim0, 2 * nc + 64);
+                            atomicMin(&p.tau_g[q], f2o(tau));
                         }
                     }
-                    uint32_t r[32];
-                    TMEM_LD32(taddr + ch * 32, r);
-                    tmem_wait_ld();
-                    if (qv) {
-                        const int cb0 = ch * 32;
+                    if (p.dbg && cc0) c_comp += clock64() - cc0;
+                }
+                const long long c0 = p.dbg ? clock64() : 0;
+                mbar_wait(&S.tfull[acc], aph);
+                if (p.dbg) w_tfull += clock64() - c0;
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + half * (BN / 2);
+                uint32_t ra[32], rb[32];
+                TMEM_LD32(taddr, ra);
+                tmem_wait_ld();
+#pragma unroll
+                for (int ch = 0; ch < BN / 64; ++ch) {
+                    uint32_t* cur = (ch & 1) ? rb : ra;
+                    uint32_t* nxt = (ch & 1) ? ra : rb;
+                    if (ch + 1 < BN / 64) TMEM_LD32(taddr + (ch + 1) * 32, nxt);  // in flight during compute
+                    const int cl0 = ch * 32;                  // column within the half
+                    const int cb0 = half * (BN / 2) + cl0;    // column within the tile
+                    float xv[32];
+                    if (!IP) {
+                        const float4* x4 = reinterpret_cast<const float4*>(xw + cl0);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 v = x4[i];
+                            xv[4 * i] = v.x; xv[4 * i + 1] = v.y; xv[4 * i + 2] = v.z; xv[4 * i + 3] = v.w;
+                        }
+                    }
+                    const int nv = ncols - cb0;
+                    const unsigned valid = nv >= 32 ? VS_FULL : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                    float kk[32];
+                    unsigned mask = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float a = __uint_as_float(cur[j]);
+                        kk[j] = IP ? -a : fmaf(-2.f, a, xv[j]);
+                        mask |= (kk[j] <= tau ? 1u : 0u) << j;
+                    }
+                    mask &= valid;
+                    if (!qv) mask = 0;
+                    if (mask) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            const int c = cb0 + j;
-                            const float a = __uint_as_float(r[j]);
-                            const float key = p.ip ? -a : fmaf(-2.f, a, xs[c]);
-                            if (c < ncols && key <= tau) {
-                                ckey[cnt] = key;
-                                cpos[cnt] = (uint32_t)(r0 + c);
+                            if (mask & (1u << j)) {
+                                ckey[cnt] = kk[j];
+                                cpos[cnt] = (uint32_t)(r0 + cb0 + j);
                                 ++cnt;
                             }
                         }
+                        if (p.dbg) n_app += __popc(mask);
                     }
+                    if (ch + 1 < BN / 64) tmem_wait_ld_regs(nxt);
                 }
                 tc_fence_before();
                 mbar_arrive(&S.tempty[acc]);
             }
             if (qv) {
-                p.cb.cnt[q * p.cb.n_sub + s] = cnt;
+                p.cb.cnt[q * p.cb.n_sub + sub] = cnt;
                 if (ovf) p.cb.overflow[q] = 1;
             }
+        }
+        if (p.dbg) {
+            atomicAdd(&p.dbg[3], (unsigned long long)w_tfull);
+            atomicAdd(&p.dbg[4], (unsigned long long)c_comp);
+            atomicAdd(&p.dbg[5], (unsigned long long)n_comp);
+            atomicAdd(&p.dbg[6], (unsigned long long)n_app);
+            if (et == 0) atomicAdd(&p.dbg[7], (unsigned long long)tcount);
         }
     }
     tc_fence_before();
@@ -337,63 +452,111 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // ---- operand staging -----------------------------------------------------------------------------------
-// queries fp32 -> bf16 (round to nearest even), row stride dp
+// Rounding to bf16 is exact-error-tracked: for each staged vector v with bf16
+// image v~ and error dv = v~ - v we keep ||v~|| and ||dv|| (fp32, inflated by
+// 1e-4 for their own rounding). The tensor-core dot product then satisfies
+//   |q~.x~ - q.x| <= ||q~|| ||dx|| + ||dq|| ||x~|| + ||dq|| ||dx||
+// (Cauchy-Schwarz on the error vectors), which is ~1.7x tighter than the
+// worst-case 2^-8 ||q|| ||x|| bound and still rigorous.
+
+// queries fp32 -> bf16 (round to nearest even), row stride dp; warp per query
 __global__ void k_stage_queries(const float* __restrict__ q, int64_t nq, int d, int dp,
-                                __nv_bfloat16* __restrict__ out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t tot = nq * (int64_t)dp;
-    for (; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / dp;
-        const int c = (int)(i - r * dp);
-        out[i] = __float2bfloat16_rn(c < d ? q[r * (int64_t)d + c] : 0.f);
-    }
-}
-// selected rows -> contiguous bf16 [nsel][dp] + their norms (warp per row)
-template <typename T>
-__global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict__ sel, int64_t nsel, int d,
-                             int dp, const float* __restrict__ norms, __nv_bfloat16* __restrict__ out,
-                             float* __restrict__ xn) {
+                                __nv_bfloat16* __restrict__ out, float2* __restrict__ qerr) {
     const int lane = threadIdx.x & 31;
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (; w < nq; w += nw) {
+        float sn = 0.f, se = 0.f;
+        for (int c = lane; c < dp; c += 32) {
+            const float v = c < d ? q[w * (int64_t)d + c] : 0.f;
+            const __nv_bfloat16 b = __float2bfloat16_rn(v);
+            const float vb = __bfloat162float(b);
+            const float e = vb - v;  // exact in fp32 (Sterbenz-free: |e| << |v|, same binade)
+            sn = fmaf(vb, vb, sn);
+            se = fmaf(e, e, se);
+            out[w * (int64_t)dp + c] = b;
+        }
+        sn = warp_sumf(sn);
+        se = warp_sumf(se);
+        if (lane == 0) qerr[w] = make_float2(sqrtf(sn) * 1.0001f, sqrtf(se) * 1.0001f);
+    }
+}
+// selected rows -> contiguous bf16 [nsel][dp] + their fp32 norms (warp per row);
+// max ||x~|| and max ||dx|| over the rows into xmax2[0..1] (float bits, atomicMax)
+template <typename T>
+__global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict__ sel, int64_t nsel, int d,
+                             int dp, const float* __restrict__ norms, __nv_bfloat16* __restrict__ out,
+                             float* __restrict__ xn, unsigned* __restrict__ xmax2) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float mb = 0.f, me = 0.f;
     for (; w < nsel; w += nw) {
         const int64_t r = sel ? sel[w] : w;
         const T* src = x + r * (int64_t)d;
         __nv_bfloat16* dst = out + w * (int64_t)dp;
+        float sn = 0.f, se = 0.f;
         if (sizeof(T) == 4 && (d % 4) == 0 && (dp % 4) == 0) {
             for (int c = lane * 4; c < dp; c += 128) {
-                float4 v = (c < d) ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) + c)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-                __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-                __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
+                const float4 v = (c < d) ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) + c)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
+                const __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
+                const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+                const float e0 = fa.x - v.x, e1 = fa.y - v.y, e2 = fb.x - v.z, e3 = fb.y - v.w;
+                sn = fmaf(fa.x, fa.x, sn); sn = fmaf(fa.y, fa.y, sn);
+                sn = fmaf(fb.x, fb.x, sn); sn = fmaf(fb.y, fb.y, sn);
+                se = fmaf(e0, e0, se); se = fmaf(e1, e1, se); se = fmaf(e2, e2, se); se = fmaf(e3, e3, se);
                 uint2 u;
-                u.x = *reinterpret_cast<uint32_t*>(&a);
-                u.y = *reinterpret_cast<uint32_t*>(&b);
+                u.x = *reinterpret_cast<const uint32_t*>(&a);
+                u.y = *reinterpret_cast<const uint32_t*>(&b);
                 *reinterpret_cast<uint2*>(dst + c) = u;
             }
         } else {
-            for (int c = lane; c < dp; c += 32) dst[c] = __float2bfloat16_rn(c < d ? ld_elem(src + c) : 0.f);
+            for (int c = lane; c < dp; c += 32) {
+                const float v = c < d ? ld_elem(src + c) : 0.f;
+                const __nv_bfloat16 b = __float2bfloat16_rn(v);
+                const float vb = __bfloat162float(b);
+                const float e = vb - v;
+                sn = fmaf(vb, vb, sn);
+                se = fmaf(e, e, se);
+                dst[c] = b;
+            }
         }
+        sn = warp_sumf(sn);
+        se = warp_sumf(se);
+        mb = fmaxf(mb, sn);
+        me = fmaxf(me, se);
         if (lane == 0 && xn) xn[w] = norms[r];
+    }
+    if (lane == 0) {
+        atomicMax(&xmax2[0], __float_as_uint(mb));
+        atomicMax(&xmax2[1], __float_as_uint(me));
     }
 }
 
-__global__ void k_tc_margins(const float* __restrict__ q, int64_t nq, int d, const unsigned* __restrict__ xmax,
-                             float cqx, float cxx, float* __restrict__ margin) {
-    const int lane = threadIdx.x & 31;
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (r >= nq) return;
-    float s = 0.f;
-    for (int i = lane; i < d; i += 32) {
-        float v = q[r * (int64_t)d + i];
-        s = fmaf(v, v, s);
+// margin = 2 x E, with E the rigorous error of the approximate key:
+//   L2: key = fl(||x||^2_fp32 - 2 acc)   E = 2 E_dot + E_norm + E_round
+//   IP: key = -acc                        E = E_dot
+//   E_dot = ||q~|| Dx + ||dq|| X~ + ||dq|| Dx + 2^-14 ||q~|| X~   (last term:
+//           tensor-core fp32 accumulation, generously bounded)
+//   E_norm = (d + 2) 2^-24 X^2,  E_round = 2^-23 (X^2 + 2 ||q~|| X~)
+__global__ void k_tc_margins(const float2* __restrict__ qerr, int64_t nq, int d, const unsigned* __restrict__ xmax,
+                             const unsigned* __restrict__ xmax2, int ip, float* __restrict__ margin) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    const float2 qe = qerr[i];
+    const float Xt = sqrtf(__uint_as_float(xmax2[0])) * 1.0001f;   // max ||x~||
+    const float Dx = sqrtf(__uint_as_float(xmax2[1])) * 1.0001f;   // max ||dx||
+    const float X2 = __uint_as_float(*xmax) * 1.0002f;             // max ||x||^2 (fp32)
+    const float edot = qe.x * Dx + qe.y * Xt + qe.y * Dx + 6.103515625e-05f * qe.x * Xt;
+    float e;
+    if (ip) {
+        e = edot;
+    } else {
+        e = 2.f * edot + (float)(d + 2) * 5.9604645e-08f * X2 + 1.1920929e-07f * (X2 + 2.f * qe.x * Xt);
     }
-    s = warp_sumf(s);
-    if (lane == 0) {
-        const float qn = sqrtf(s) * 1.0001f;
-        const float xn = sqrtf(__uint_as_float(*xmax)) * 1.0001f;
-        margin[r] = cqx * qn * xn + cxx * xn * xn;
-    }
+    margin[i] = 2.f * e * 1.01f;
 }
 
 }  // namespace tc
@@ -438,24 +601,11 @@ bool tc_profitable(int64_t nq, int64_t nsel, int d) {
     return nq >= 64 && (double)nq * (double)nsel * (double)d >= 4.0e9;
 }
 
-// bf16 error bound of the tensor-core key:
-//   |q~.x~ - q.x| <= (2^-8 + 2^-18) |q| |x|  (RN to bf16, Cauchy-Schwarz)
-//   + fp32 accumulation inside the tensor core (bounded by 2^-14 |q| |x|),
-// key = ||x||^2 - 2 q.x adds the fp32 norm error (d + 2) 2^-24 |x|^2;
-// margin = 2 x bound, with a 5% safety factor.
-static void tc_margin_coeffs(int d, int ip, float* cqx, float* cxx) {
-    const double edot = (std::ldexp(1.0, -8) + std::ldexp(1.0, -18) + std::ldexp(1.0, -14)) * 1.05;
-    if (ip) {
-        *cqx = (float)(2.0 * edot);
-        *cxx = 0.f;
-    } else {
-        *cqx = (float)(2.0 * 2.0 * edot);
-        *cxx = (float)(2.0 * (d + 2) * std::ldexp(1.0, -24) * 1.05);
-    }
-}
-
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift, CandBuf* cb,
                 bool* exhaustive) {
+    // first pass: local top-k buffers verified by phase B; re-runs (cshift > 0)
+    // keep the full margin band, which is exact by construction
+    const int topk_mode = (cshift == 0 && !getenv("VS_TC_MARGIN_MODE")) ? 1 : 0;
     using namespace vs_internal;
     cudaStream_t st = ctx->stream;
     const int d = sp.d;
@@ -464,29 +614,31 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     // staging buffers
     __nv_bfloat16 *qa = nullptr, *xb = nullptr;
     float *xn = nullptr, *margin = nullptr;
+    float2* qerr = nullptr;
     unsigned* tau_g = nullptr;
+    unsigned* xmax2 = nullptr;
     CKS(arena_alloc(ctx, (size_t)nq * dp, &qa));
     CKS(arena_alloc(ctx, (size_t)nsel * dp, &xb));
     CKS(arena_alloc(ctx, (size_t)nsel, &xn));
     CKS(arena_alloc(ctx, (size_t)nq, &margin));
+    CKS(arena_alloc(ctx, (size_t)nq, &qerr));
     CKS(arena_alloc(ctx, (size_t)nq, &tau_g));
+    CKS(arena_alloc(ctx, 2, &xmax2));
     {
         KTimer kt(ctx, VS_K_STAGE);
-        int64_t tot = nq * (int64_t)dp;
-        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 32), 256, 0, st>>>(
-            sp.Q, nq, d, dp, qa);
+        CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));
+        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+            sp.Q, nq, d, dp, qa, qerr);
         CK(cudaGetLastError());
         const unsigned blocks = (unsigned)std::min<int64_t>((nsel * 32 + 255) / 256, 148 * 64);
         if (dtype == VS_DTYPE_F32)
             tc::k_stage_rows<float><<<blocks, 256, 0, st>>>((const float*)sp.X, sp.sel, nsel, d, dp, sp.xnorm, xb,
-                                                            sp.ip ? nullptr : xn);
+                                                            sp.ip ? nullptr : xn, xmax2);
         else
             tc::k_stage_rows<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)sp.X, sp.sel, nsel, d,
-                                                                    dp, sp.xnorm, xb, sp.ip ? nullptr : xn);
+                                                                    dp, sp.xnorm, xb, sp.ip ? nullptr : xn, xmax2);
         CK(cudaGetLastError());
-        float cqx, cxx;
-        tc_margin_coeffs(d, sp.ip, &cqx, &cxx);
-        tc::k_tc_margins<<<(unsigned)((nq * 32 + 255) / 256), 256, 0, st>>>(sp.Q, nq, d, xmax, cqx, cxx, margin);
+        tc::k_tc_margins<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qerr, nq, d, xmax, xmax2, sp.ip, margin);
         CK(cudaGetLastError());
         CK(cudaMemsetAsync(tau_g, 0xff, nq * sizeof(unsigned), st));
         ctx->stats[VS_STAT_LAUNCHES] += 3;
@@ -511,18 +663,19 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     }
     const int64_t per = (ntiles + best_s - 1) / best_s;
     const int nsplit = (int)((ntiles + per - 1) / per);
-    int64_t C = vs_internal::pow2ceil(std::max<int64_t>(4 * sp.k, sp.k + 160)) << (ctx->opt_slack + cshift);
-    const int64_t rows_per_split = per * tc::BN;
+    int64_t C = (topk_mode ? vs_internal::pow2ceil(2 * sp.k + 96) : vs_internal::pow2ceil(sp.k + 512))
+                << (ctx->opt_slack + cshift);
+    const int64_t rows_per_split = per * tc::BN / 2;  // per column half
     const int64_t cap = vs_internal::pow2ceil(rows_per_split + 64);
     *exhaustive = C >= cap;
     if (C > cap) C = cap;
     CandBuf c;
-    c.n_sub = nsplit;
+    c.n_sub = 2 * nsplit;
     c.C = (int)C;
-    const size_t slots = (size_t)nq * nsplit * C;
+    const size_t slots = (size_t)nq * c.n_sub * C;
     CKS(arena_alloc(ctx, slots, &c.key));
     CKS(arena_alloc(ctx, slots, &c.pos));
-    CKS(arena_alloc(ctx, (size_t)nq * nsplit, &c.cnt));
+    CKS(arena_alloc(ctx, (size_t)nq * c.n_sub, &c.cnt));
     CKS(arena_alloc(ctx, (size_t)nq, &c.overflow));
     CK(cudaMemsetAsync(c.overflow, 0, nq * sizeof(int), st));
 
@@ -544,16 +697,43 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     pr.ip = sp.ip;
     pr.k = sp.k;
     pr.cb = c;
-    CK(cudaFuncSetAttribute(tc::k_enn_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_BYTES));
+    pr.dbg = nullptr;
+    pr.topk_mode = topk_mode;
+    static const bool dbg_on = getenv("VS_TC_DEBUG") != nullptr;
+    if (dbg_on) {
+        CKS(arena_alloc(ctx, 8, &pr.dbg));
+        CK(cudaMemsetAsync(pr.dbg, 0, 8 * sizeof(unsigned long long), st));
+    }
     const int64_t items = (int64_t)qtiles * nsplit;
     const unsigned grid = (unsigned)std::min<int64_t>(items, sms);
-    tc::k_enn_scan_tc<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+    if (sp.ip) {
+        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)tc::SMEM_BYTES));
+        tc::k_enn_scan_tc<true><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+    } else {
+        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)tc::SMEM_BYTES));
+        tc::k_enn_scan_tc<false><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+    }
     CK(cudaGetLastError());
     ctx->stats[VS_STAT_LAUNCHES] += 1;
+    if (dbg_on) {
+        unsigned long long h[8];
+        CK(cudaMemcpyAsync(h, pr.dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double ctas = (double)grid, thr = ctas * tc::EPI_THREADS;
+        fprintf(stderr,
+                "[vs_tc] grid=%u nsplit=%d per=%lld C=%lld tiles/cta=%.1f | producer wait-empty %.0f cyc/cta | "
+                "mma wait-full %.0f wait-tempty %.0f cyc/cta | epi wait-tfull %.0f compaction %.0f cyc/thr | "
+                "compactions %.2f appends %.1f per row-split\n",
+                grid, nsplit, (long long)per, (long long)C, h[7] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas,
+                h[3] / thr, h[4] / thr, (double)h[5] / ((double)nq * 2 * nsplit), (double)h[6] / ((double)nq * 2 * nsplit));
+    }
     // phase B reads rows through the selection (sp.sel) from the original
     // column, with the tensor-core margins
     sp.margin = margin;
     sp.tau_g = tau_g;
+    sp.verify = topk_mode;
     *cb = c;
     return VS_OK;
 }

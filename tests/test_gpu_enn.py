@@ -199,3 +199,14 @@ def test_merge_kernel_matches_oracle_merge():
     ref = O.enn_search(q, data, 30)
     assert np.array_equal(oi.reshape(-1), ref.data_row)
     assert np.array_equal(od.reshape(-1), ref.distance)
+
+
+@pytest.mark.parametrize("dim", [8, 127, 128, 129, 1000, 1152, 2048, 2100])
+def test_exact_scores_across_dims(dim):
+    # every summation-tree shape of the warp-cooperative float64 scorer
+    rng = np.random.default_rng(dim)
+    data = rng.standard_normal((700, dim)).astype(np.float32)
+    q = rng.standard_normal((9, dim)).astype(np.float32)
+    for metric in ("squared_l2", "inner_product"):
+        nt = vs.enn_search(q, data, vs.SearchParams(k=25), metric=metric)
+        assert_same(nt, O.enn_search(q, data, 25, metric))
