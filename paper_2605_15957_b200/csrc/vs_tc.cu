@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                   Params p) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ __align__(16) float xn_w[8][BN / 2];  // per epilogue warp: its column half's row norms
+    __shared__ __align__(16) float app_w[8][32];     // per epilogue warp: one lane's chunk keys (appends)
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     Smem& S = *reinterpret_cast<Smem*>(base + (size_t)NSTAGE * STAGE_BYTES);
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int quad = warp & 3;                       // lane quadrant
         const int C = p.cb.C;
         uint32_t tcount = 0;
-        long long w_tfull = 0, c_comp = 0, n_comp = 0, n_app = 0;
+        long long w_tfull = 0, c_comp = 0, n_comp = 0, n_app = 0, c_ldw = 0, c_loop = 0;
         // software-pipelined per-tile inputs: the next tile's row norms (4 per
         // lane = the warp's column half) and the next tile's admission bound
         auto norms4 = [&](int64_t r0n) -> float4 {
@@ -384,8 +385,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + half * (BN / 2);
                 uint32_t ra[32], rb[32];
+                const long long cl0 = p.dbg ? clock64() : 0;
                 TMEM_LD32(taddr, ra);
                 tmem_wait_ld();
+                if (p.dbg) c_ldw += clock64() - cl0;
 #pragma unroll
                 for (int ch = 0; ch < BN / 64; ++ch) {
                     uint32_t* cur = (ch & 1) ? rb : ra;
@@ -414,19 +417,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     mask &= valid;
                     if (!qv) mask = 0;
-                    if (mask) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            if (mask & (1u << j)) {
-                                ckey[cnt] = kk[j];
-                                cpos[cnt] = (uint32_t)(r0 + cb0 + j);
-                                ++cnt;
-                            }
-                        }
+                    // warp-cooperative append: lanes with admitted keys take turns
+                    // staging their 32 keys in shared memory; the warp then writes
+                    // only the admitted (key, position) pairs, in column order
+                    unsigned am = __ballot_sync(VS_FULL, mask != 0);
+                    if (am) {
+                        float* st = app_w[warp - EPI_WARP0];
                         if (p.dbg) n_app += __popc(mask);
+                        while (am) {
+                            const int l = __ffs(am) - 1;
+                            am &= am - 1;
+                            if (lane == l) {
+                                float4* st4 = reinterpret_cast<float4*>(st);
+#pragma unroll
+                                for (int i = 0; i < 8; ++i)
+                                    st4[i] = make_float4(kk[4 * i], kk[4 * i + 1], kk[4 * i + 2], kk[4 * i + 3]);
+                            }
+                            __syncwarp();
+                            const unsigned ml = __shfl_sync(VS_FULL, mask, l);
+                            const int cl = __shfl_sync(VS_FULL, cnt, l);
+                            const int lo32 = __shfl_sync(VS_FULL, (int)(cbase & 0xffffffff), l);
+                            const int hi32 = __shfl_sync(VS_FULL, (int)(cbase >> 32), l);
+                            if ((ml >> lane) & 1u) {
+                                const int64_t lb = ((int64_t)(uint32_t)hi32 << 32) | (uint32_t)lo32;
+                                const int dst = cl + __popc(ml & lanemask_lt());
+                                p.cb.key[lb + dst] = st[lane];
+                                p.cb.pos[lb + dst] = (uint32_t)(r0 + cb0 + lane);
+                            }
+                            __syncwarp();
+                            if (lane == l) cnt += __popc(ml);
+                        }
                     }
-                    if (ch + 1 < BN / 64) tmem_wait_ld_regs(nxt);
+                    if (ch + 1 < BN / 64) {
+                        const long long cw = p.dbg ? clock64() : 0;
+                        tmem_wait_ld_regs(nxt);
+                        if (p.dbg) c_ldw += clock64() - cw;
+                    }
                 }
+                if (p.dbg) c_loop += clock64() - cl0;
                 tc_fence_before();
                 mbar_arrive(&S.tempty[acc]);
             }
@@ -441,6 +469,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             atomicAdd(&p.dbg[5], (unsigned long long)n_comp);
             atomicAdd(&p.dbg[6], (unsigned long long)n_app);
             if (et == 0) atomicAdd(&p.dbg[7], (unsigned long long)tcount);
+            atomicAdd(&p.dbg[8], (unsigned long long)c_ldw);
+            atomicAdd(&p.dbg[9], (unsigned long long)c_loop);
         }
     }
     tc_fence_before();
@@ -701,8 +731,8 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     pr.topk_mode = topk_mode;
     static const bool dbg_on = getenv("VS_TC_DEBUG") != nullptr;
     if (dbg_on) {
-        CKS(arena_alloc(ctx, 8, &pr.dbg));
-        CK(cudaMemsetAsync(pr.dbg, 0, 8 * sizeof(unsigned long long), st));
+        CKS(arena_alloc(ctx, 16, &pr.dbg));
+        CK(cudaMemsetAsync(pr.dbg, 0, 16 * sizeof(unsigned long long), st));
     }
     const int64_t items = (int64_t)qtiles * nsplit;
     const unsigned grid = (unsigned)std::min<int64_t>(items, sms);
@@ -718,16 +748,17 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     CK(cudaGetLastError());
     ctx->stats[VS_STAT_LAUNCHES] += 1;
     if (dbg_on) {
-        unsigned long long h[8];
+        unsigned long long h[16];
         CK(cudaMemcpyAsync(h, pr.dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         const double ctas = (double)grid, thr = ctas * tc::EPI_THREADS;
         fprintf(stderr,
                 "[vs_tc] grid=%u nsplit=%d per=%lld C=%lld tiles/cta=%.1f | producer wait-empty %.0f cyc/cta | "
                 "mma wait-full %.0f wait-tempty %.0f cyc/cta | epi wait-tfull %.0f compaction %.0f cyc/thr | "
-                "compactions %.2f appends %.1f per row-split\n",
+                "compactions %.2f appends %.1f per row-split | tmem-ld wait %.0f chunk-loop %.0f cyc/thr\n",
                 grid, nsplit, (long long)per, (long long)C, h[7] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas,
-                h[3] / thr, h[4] / thr, (double)h[5] / ((double)nq * 2 * nsplit), (double)h[6] / ((double)nq * 2 * nsplit));
+                h[3] / thr, h[4] / thr, (double)h[5] / ((double)nq * 2 * nsplit), (double)h[6] / ((double)nq * 2 * nsplit),
+                h[8] / thr, h[9] / thr);
     }
     // phase B reads rows through the selection (sp.sel) from the original
     // column, with the tensor-core margins
