@@ -56,13 +56,18 @@ def all_gather_topk(ids, dist, counts, group=None):
     import torch.distributed as dist_
 
     world = dist_.get_world_size(group)
-    out_ids = torch.empty((world,) + tuple(ids.shape), dtype=ids.dtype, device=ids.device)
-    out_dist = torch.empty((world,) + tuple(dist.shape), dtype=dist.dtype, device=dist.device)
-    out_cnt = torch.empty((world,) + tuple(counts.shape), dtype=counts.dtype, device=counts.device)
-    dist_.all_gather_into_tensor(out_ids, ids.contiguous(), group=group)
-    dist_.all_gather_into_tensor(out_dist, dist.contiguous(), group=group)
-    dist_.all_gather_into_tensor(out_cnt, counts.contiguous(), group=group)
-    return out_ids, out_dist, out_cnt
+    outs = []
+    for t in (ids, dist, counts):
+        t = t.contiguous()
+        if dist_.get_backend(group) == "nccl":
+            o = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            dist_.all_gather_into_tensor(o, t, group=group)
+        else:  # gloo (CPU tests): list form
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist_.all_gather(parts, t, group=group)
+            o = torch.stack(parts)
+        outs.append(o)
+    return tuple(outs)
 
 
 def gpu_merge(ids, dist, counts, k: int, metric: str, device=None, out=None):
