@@ -152,9 +152,15 @@ int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
                   const void* list_payload, int32_t dtype, int32_t metric,
                   const vs_column* base, const uint8_t* list_owned,
                   vs_ivf** out);
-/* GPU k-means build with the reference's semantics (vecindex.py:273-318) */
-int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, uint64_t seed,
-                 int32_t metric, int32_t max_iters, vs_ivf** out);
+/* GPU k-means build with the reference's semantics (vecindex.py:273-318):
+ * init_rows = the nlist ascending initial rows (the reference draws them with
+ * np.sort(default_rng(seed).choice(n, nlist, replace=False)); the Python
+ * shim passes exactly those), nullable -> a seeded library sample; <= max_iters
+ * Lloyd iterations or max centroid shift < 1e-4, first-min assignment, empty
+ * lists reseeded to the farthest member of the largest list, float64 means,
+ * final reassignment; lists hold ascending row ids (owning layout). */
+int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows,
+                 uint64_t seed, int32_t metric, int32_t max_iters, vs_ivf** out);
 int vs_ivf_info(const vs_ivf* ivf, int32_t* nlist, int32_t* d, int64_t* n_total,
                 int32_t* metric, int32_t* dtype);
 /* host copies of the structure (any pointer may be NULL) */

@@ -581,23 +581,14 @@ int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in, const i
     return VS_OK;
 }
 
-int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
-                  const int64_t* list_sizes, const int64_t* list_ids, const void* list_payload,
-                  int32_t dtype, int32_t metric, const vs_column* base, const uint8_t* list_owned,
-                  vs_ivf** out) {
-    if (!ctx || !out || !centroids || !list_sizes) return set_err(VS_ERR_PARAMETER, "null argument");
-    CKS(validate_metric(metric));
-    if (nlist < 1) return set_err(VS_ERR_PARAMETER, "nlist must be >= 1");
-    if (d < 1) return set_err(VS_ERR_SHAPE, "embedding dimension must be >= 1");
-    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
-    if (!list_payload && !base) return set_err(VS_ERR_PARAMETER, "non-owning IVF needs a base column");
-    if (base && base->d != d) return set_err(VS_ERR_SHAPE, "base dim %d != index dim %d", base->d, d);
-    if (!list_payload && base->dtype != dtype) return set_err(VS_ERR_PARAMETER, "base dtype mismatch");
-    DevGuard g(ctx->device);
-    CK(ctx->arena.reset());
-    // sizes may live on either side; read them on the host
-    std::vector<int64_t> sizes(nlist);
-    CK(cudaMemcpy(sizes.data(), list_sizes, nlist * sizeof(int64_t), cudaMemcpyDefault));
+}  // extern "C"
+
+// Build the device IVF structure. centroids / list_ids / list_payload may be
+// host or device pointers; sizes are host. Non-owning (payload == nullptr):
+// rows are gathered from `base` into the list-contiguous layout.
+int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, const std::vector<int64_t>& sizes,
+             const int64_t* list_ids, const void* list_payload, int32_t dtype, int32_t metric,
+             const vs_column* base, const uint8_t* list_owned, vs_ivf** out) {
     std::vector<int64_t> off(nlist + 1, 0);
     for (int i = 0; i < nlist; ++i) {
         if (sizes[i] < 0) return set_err(VS_ERR_PARAMETER, "negative list size");
@@ -661,6 +652,27 @@ int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e, "sync");
     *out = v;
     return VS_OK;
+}
+
+extern "C" {
+
+int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
+                  const int64_t* list_sizes, const int64_t* list_ids, const void* list_payload,
+                  int32_t dtype, int32_t metric, const vs_column* base, const uint8_t* list_owned,
+                  vs_ivf** out) {
+    if (!ctx || !out || !centroids || !list_sizes) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_metric(metric));
+    if (nlist < 1) return set_err(VS_ERR_PARAMETER, "nlist must be >= 1");
+    if (d < 1) return set_err(VS_ERR_SHAPE, "embedding dimension must be >= 1");
+    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
+    if (!list_payload && !base) return set_err(VS_ERR_PARAMETER, "non-owning IVF needs a base column");
+    if (base && base->d != d) return set_err(VS_ERR_SHAPE, "base dim %d != index dim %d", base->d, d);
+    if (!list_payload && base->dtype != dtype) return set_err(VS_ERR_PARAMETER, "base dtype mismatch");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<int64_t> sizes(nlist);
+    CK(cudaMemcpy(sizes.data(), list_sizes, nlist * sizeof(int64_t), cudaMemcpyDefault));
+    return ivf_make(ctx, centroids, nlist, d, sizes, list_ids, list_payload, dtype, metric, base, list_owned, out);
 }
 
 int vs_ivf_info(const vs_ivf* ivf, int32_t* nlist, int32_t* d, int64_t* n_total, int32_t* metric,
@@ -945,7 +957,14 @@ extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* querie
     return VS_OK;
 }
 
-extern "C" int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, uint64_t seed,
-                            int32_t metric, int32_t max_iters, vs_ivf** out) {
-    return vs::ivf_build_gpu(ctx, data, nlist, seed, metric, max_iters, out);
+extern "C" int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows,
+                            uint64_t seed, int32_t metric, int32_t max_iters, vs_ivf** out) {
+    if (!ctx || !data || !out) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_metric(metric));
+    if (nlist < 1 || nlist > data->n)
+        return set_err(VS_ERR_PARAMETER, "nlist must be in [1, %lld], got %d", (long long)data->n, nlist);
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    CKS(ensure_norms(const_cast<vs_column*>(data)));
+    return vs::ivf_build_gpu(ctx, data, nlist, init_rows, seed, metric, max_iters, out);
 }

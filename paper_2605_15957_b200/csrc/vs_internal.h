@@ -240,3 +240,7 @@ inline void resolve_timers(vs_ctx* ctx) {
 }
 
 }  // namespace vs_internal
+
+int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, const std::vector<int64_t>& sizes,
+             const int64_t* list_ids, const void* list_payload, int32_t dtype, int32_t metric,
+             const vs_column* base, const uint8_t* list_owned, vs_ivf** out);

@@ -74,6 +74,7 @@ struct Params {
     CandBuf cb;
     unsigned long long* dbg;  // nullable: [8] stall / work counters (VS_TC_DEBUG=1)
     int topk_mode;            // 1: keep the local top-k only (phase B verifies); 0: keep the margin band
+    unsigned long long* argmin_out;  // MODE 1: per query row packed (orderable key << 32 | column)
 };
 
 // ---- PTX helpers ---------------------------------------------------------------------------------
@@ -170,7 +171,7 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t* r) {
 }
 
 // ---- the kernel --------------------------------------------------------------------------------------
-template <bool IP>
+template <bool IP, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_enn_scan_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   Params p) {
@@ -273,6 +274,61 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 atomicAdd(&p.dbg[1], (unsigned long long)w_full);
                 atomicAdd(&p.dbg[2], (unsigned long long)w_tempty);
             }
+        }
+    } else if (warp >= EPI_WARP0 && MODE == 1) {
+        // ===== epilogue (argmin mode): first-min column per query row =====
+        // (k-means assignment: queries = data rows, columns = centroids)
+        const int et = threadIdx.x - EPI_WARP0 * 32;
+        const int row = et & (BM - 1);
+        const int half = et >> 7;
+        const int quad = warp & 3;
+        float* xw = xn_w[warp - EPI_WARP0];
+        uint32_t tcount = 0;
+        for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int qt = (int)(it % p.qtiles);
+            const int64_t s = it / p.qtiles;
+            const int64_t t0 = s * p.tiles_per_split;
+            const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
+            const int64_t q = (int64_t)qt * BM + row;
+            uint32_t best_o = 0xffffffffu, best_i = 0u;
+            for (int64_t t = t0; t < t1; ++t, ++tcount) {
+                const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
+                const int64_t r0 = t * BN;
+                const int ncols = (int)min((int64_t)BN, p.nsel - r0);
+                {
+                    const int64_t i = r0 + half * (BN / 2) + lane * 4;
+                    float4 v;
+                    v.x = i + 0 < p.nsel ? __ldg(p.xn + i + 0) : 0.f;
+                    v.y = i + 1 < p.nsel ? __ldg(p.xn + i + 1) : 0.f;
+                    v.z = i + 2 < p.nsel ? __ldg(p.xn + i + 2) : 0.f;
+                    v.w = i + 3 < p.nsel ? __ldg(p.xn + i + 3) : 0.f;
+                    *reinterpret_cast<float4*>(xw + lane * 4) = v;
+                }
+                __syncwarp();
+                mbar_wait(&S.tfull[acc], aph);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + half * (BN / 2);
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 64; ++ch) {
+                    uint32_t r[32];
+                    TMEM_LD32(taddr + ch * 32, r);
+                    tmem_wait_ld();
+                    const int cb0 = half * (BN / 2) + ch * 32;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float a = __uint_as_float(r[j]);
+                        const float key = IP ? -a : fmaf(-2.f, a, xw[ch * 32 + j]);
+                        const uint32_t ko = f2o(key);
+                        if (cb0 + j < ncols && ko < best_o) {
+                            best_o = ko;
+                            best_i = (uint32_t)(r0 + cb0 + j);
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&S.tempty[acc]);
+            }
+            if (q < p.nq) atomicMin(&p.argmin_out[q], ((unsigned long long)best_o << 32) | best_i);
         }
     } else if (warp >= EPI_WARP0) {
         // ===== epilogue: TMEM -> keys -> candidate buffers =====
@@ -736,14 +792,15 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     }
     const int64_t items = (int64_t)qtiles * nsplit;
     const unsigned grid = (unsigned)std::min<int64_t>(items, sms);
+    pr.argmin_out = nullptr;
     if (sp.ip) {
-        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)tc::SMEM_BYTES));
-        tc::k_enn_scan_tc<true><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+        tc::k_enn_scan_tc<true, 0><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
     } else {
-        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)tc::SMEM_BYTES));
-        tc::k_enn_scan_tc<false><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+        tc::k_enn_scan_tc<false, 0><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
     }
     CK(cudaGetLastError());
     ctx->stats[VS_STAT_LAUNCHES] += 1;
@@ -766,6 +823,70 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     sp.tau_g = tau_g;
     sp.verify = topk_mode;
     *cb = c;
+    return VS_OK;
+}
+
+// First-min nearest column under squared L2 (key ||c||^2 - 2 x.c) for every
+// row of x, on the tensor cores: the k-means assignment step. `cb` holds the
+// columns (centroids) already staged as bf16 [ncols][dp] with their fp32
+// norms; rows are staged here in chunks. out[r] = (orderable key << 32) | col.
+int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, const __nv_bfloat16* cb,
+                   const float* cnorm, int64_t ncols, unsigned long long* out) {
+    using namespace vs_internal;
+    if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cudaStream_t st = ctx->stream;
+    const int dp = (d + 7) / 8 * 8;
+    const int64_t chunk = std::min<int64_t>(n, (int64_t)1 << 22);
+    __nv_bfloat16* xb = nullptr;
+    unsigned* junk = nullptr;
+    CKS(arena_alloc(ctx, (size_t)chunk * dp, &xb));
+    CKS(arena_alloc(ctx, 2, &junk));
+    CK(cudaMemsetAsync(out, 0xff, n * sizeof(unsigned long long), st));
+    CUtensorMap mb;
+    if (!make_map(&mb, cb, ncols, d, dp, tc::BN)) return set_err(VS_ERR_CUDA, "tensor map (columns)");
+    CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tc::SMEM_BYTES));
+    for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t m = std::min(chunk, n - r0);
+        const unsigned blocks = (unsigned)std::min<int64_t>((m * 32 + 255) / 256, 148 * 64);
+        if (dtype == VS_DTYPE_F32)
+            tc::k_stage_rows<float><<<blocks, 256, 0, st>>>((const float*)x + r0 * (int64_t)d, nullptr, m, d, dp,
+                                                            nullptr, xb, nullptr, junk);
+        else
+            tc::k_stage_rows<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)x + r0 * (int64_t)d,
+                                                                    nullptr, m, d, dp, nullptr, xb, nullptr, junk);
+        CK(cudaGetLastError());
+        CUtensorMap ma;
+        if (!make_map(&ma, xb, m, d, dp, tc::BM)) return set_err(VS_ERR_CUDA, "tensor map (rows)");
+        tc::Params pr{};
+        pr.nq = m;
+        pr.d = d;
+        pr.kblocks = (d + tc::BK - 1) / tc::BK;
+        pr.nsel = ncols;
+        pr.qtiles = (int)((m + tc::BM - 1) / tc::BM);
+        pr.nsplit = 1;
+        pr.ntiles = (ncols + tc::BN - 1) / tc::BN;
+        pr.tiles_per_split = pr.ntiles;
+        pr.xn = cnorm;
+        pr.argmin_out = out + r0;
+        const unsigned grid = (unsigned)std::min<int64_t>(pr.qtiles, ctx->sm_count);
+        tc::k_enn_scan_tc<false, 1><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+        CK(cudaGetLastError());
+        ctx->stats[VS_STAT_LAUNCHES] += 2;
+    }
+    return VS_OK;
+}
+
+// stage a float32 matrix to bf16 [n][dp] (no norms)
+int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out) {
+    using namespace vs_internal;
+    const int dp = (d + 7) / 8 * 8;
+    unsigned* junk = nullptr;
+    CKS(arena_alloc(ctx, 2, &junk));
+    const unsigned blocks = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 148 * 64);
+    tc::k_stage_rows<float><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, out, nullptr, junk);
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
     return VS_OK;
 }
 

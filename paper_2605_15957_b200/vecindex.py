@@ -364,10 +364,13 @@ class IvfIndex:
             raise ParameterError(f"nlist must be in [1, {data.count}], got {nlist}")
         ctx = _ctx(device)
         dc = device_column(data, ctx)
+        # the reference's initial rows, drawn exactly as vecindex.py:276-279
+        init = np.ascontiguousarray(np.sort(np.random.default_rng(seed).choice(
+            data.count, size=nlist, replace=False)).astype(np.int64))
         h = C.c_void_p()
-        N.check(N.load().vs_ivf_build(ctx.handle, dc.handle, int(nlist), int(seed) & (2**64 - 1),
-                                      N.METRIC_CODE[metric], int(max_iters), C.byref(h)),
-                "ivf_build")
+        N.check(N.load().vs_ivf_build(ctx.handle, dc.handle, int(nlist), N.ptr(init),
+                                      int(seed) & (2**64 - 1), N.METRIC_CODE[metric], int(max_iters),
+                                      C.byref(h)), "ivf_build")
         div = N.DeviceIvf(ctx, h)
         centroids = np.empty((nlist, data.dim), np.float32)
         sizes = np.empty(nlist, np.int64)
