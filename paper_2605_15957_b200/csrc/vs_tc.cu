@@ -38,10 +38,18 @@ constexpr int BM = 128;                 // queries per tile (UMMA M)
 constexpr int BN = 256;                 // rows per tile (UMMA N)
 constexpr int BK = 64;                  // bf16 elements per stage = 128 B (swizzle atom)
 constexpr int UK = 16;                  // UMMA K for kind::f16
-constexpr int NSTAGE = 4;
 constexpr int A_BYTES = BM * BK * 2;    // 16 KB
-constexpr int B_BYTES = BN * BK * 2;    // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+// single CTA: B tile 256 rows x 64 (32 KB), 4 stages; CTA pair (cta_group::2,
+// M = 256): each CTA stages 128 query rows and 128 data rows (16 + 16 KB), 6 stages
+template <bool PAIR>
+struct Cfg {
+    static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
+    static constexpr int B_BYTES = B_ROWS * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int NSTAGE = PAIR ? 6 : 4;
+    static constexpr int QTILE = PAIR ? 2 * BM : BM;   // queries per work item
+};
+constexpr int MAX_STAGES = 6;
 constexpr int NTHREADS = 384;           // 12 warps
 constexpr int EPI_WARP0 = 4;            // warps 4..11 drain TMEM (2 per lane quadrant)
 constexpr int EPI_THREADS = 256;
@@ -49,13 +57,16 @@ constexpr int TMEM_COLS = 512;          // 2 accumulators x 256 fp32 columns
 
 struct Smem {
     // stage buffers live at the 1024-aligned start of dynamic smem
-    uint64_t full[NSTAGE];
-    uint64_t empty[NSTAGE];
+    uint64_t full[MAX_STAGES];
+    uint64_t empty[MAX_STAGES];
     uint64_t tfull[2];
     uint64_t tempty[2];
     uint32_t tmem_base;
 };
-constexpr size_t SMEM_BYTES = 1024 + (size_t)NSTAGE * STAGE_BYTES + sizeof(Smem);
+template <bool PAIR>
+constexpr size_t smem_bytes() {
+    return 1024 + (size_t)Cfg<PAIR>::NSTAGE * Cfg<PAIR>::STAGE_BYTES + sizeof(Smem);
+}
 
 struct Params {
     int64_t nq;
@@ -107,6 +118,41 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// CTA-pair TMA: the bytes land in this CTA's shared memory, the transaction
+// completes on the leader CTA's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(b) & 0xFEFFFFFFu) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
@@ -171,7 +217,7 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t* r) {
 }
 
 // ---- the kernel --------------------------------------------------------------------------------------
-template <bool IP, int MODE>
+template <bool IP, int MODE, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_enn_scan_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   Params p) {
@@ -180,8 +226,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __shared__ __align__(16) float app_w[8][32];     // per epilogue warp: one lane's chunk keys (appends)
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    constexpr int NSTAGE = Cfg<PAIR>::NSTAGE;
+    constexpr int STAGE_BYTES = Cfg<PAIR>::STAGE_BYTES;
+    constexpr int QTILE = Cfg<PAIR>::QTILE;
     Smem& S = *reinterpret_cast<Smem*>(base + (size_t)NSTAGE * STAGE_BYTES);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // work units: CTAs (single) or CTA pairs; rank 0 of a pair issues the MMAs
+    const uint32_t rank = PAIR ? cluster_rank() : 0u;
+    const int64_t unit = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t nunits = PAIR ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
 
     if (warp == 0 && lane == 0) {
         prefetch_map(&map_a);
@@ -192,17 +245,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&S.tfull[i], 1);
-            mbar_init(&S.tempty[i], EPI_THREADS);
+            mbar_init(&S.tempty[i], PAIR ? 2 * EPI_THREADS : EPI_THREADS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
-                     "n"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                         ::"r"(smem_u32(&S.tmem_base)), "n"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                         ::"r"(smem_u32(&S.tmem_base)), "n"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
 
@@ -213,7 +273,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             long long w_empty = 0;
-            for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            for (int64_t it = unit; it < nitems; it += nunits) {
                 const int qt = (int)(it % p.qtiles);
                 const int64_t s = it / p.qtiles;
                 const int64_t t0 = s * p.tiles_per_split;
@@ -224,9 +284,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         mbar_wait(&S.empty[stage], phase ^ 1);
                         if (p.dbg) w_empty += clock64() - c0;
                         unsigned char* sa = base + (size_t)stage * STAGE_BYTES;
-                        mbar_expect_tx(&S.full[stage], STAGE_BYTES);
-                        tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, qt * BM);
-                        tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, (int)(t * BN));
+                        if (PAIR) {
+                            if (rank == 0) mbar_expect_tx(&S.full[stage], 2 * STAGE_BYTES);
+                            tma_load_2d_pair(sa, &map_a, &S.full[stage], kb * BK, qt * QTILE + (int)rank * BM);
+                            tma_load_2d_pair(sa + A_BYTES, &map_b, &S.full[stage], kb * BK,
+                                             (int)(t * BN) + (int)rank * (BN / 2));
+                        } else {
+                            mbar_expect_tx(&S.full[stage], STAGE_BYTES);
+                            tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, qt * BM);
+                            tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, (int)(t * BN));
+                        }
                         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -234,14 +301,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (p.dbg) atomicAdd(&p.dbg[0], (unsigned long long)w_empty);
         }
     } else if (warp == 1) {
-        // ===== MMA issuer (single thread) =====
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+        // ===== MMA issuer (single thread; rank 0 of a pair) =====
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t tcount = 0;
             long long w_full = 0, w_tempty = 0;
-            for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            for (int64_t it = unit; it < nitems; it += nunits) {
                 const int64_t s = it / p.qtiles;
                 const int64_t t0 = s * p.tiles_per_split;
                 const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
@@ -261,13 +328,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const uint32_t sb = sa + A_BYTES;
 #pragma unroll
                         for (int kk = 0; kk < BK / UK; ++kk) {
-                            mma_bf16(dt, desc_sw128(sa + kk * UK * 2), desc_sw128(sb + kk * UK * 2), idesc,
-                                     (kb | kk) != 0);
+                            if (PAIR)
+                                mma_bf16_pair(dt, desc_sw128(sa + kk * UK * 2), desc_sw128(sb + kk * UK * 2), idesc,
+                                              (kb | kk) != 0);
+                            else
+                                mma_bf16(dt, desc_sw128(sa + kk * UK * 2), desc_sw128(sb + kk * UK * 2), idesc,
+                                         (kb | kk) != 0);
                         }
-                        mma_commit(&S.empty[stage]);
+                        if (PAIR) mma_commit_pair(&S.empty[stage]);
+                        else mma_commit(&S.empty[stage]);
                         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit(&S.tfull[acc]);
+                    if (PAIR) mma_commit_pair(&S.tfull[acc]);
+                    else mma_commit(&S.tfull[acc]);
                 }
             }
             if (p.dbg) {
@@ -284,12 +357,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int quad = warp & 3;
         float* xw = xn_w[warp - EPI_WARP0];
         uint32_t tcount = 0;
-        for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        for (int64_t it = unit; it < nitems; it += nunits) {
             const int qt = (int)(it % p.qtiles);
             const int64_t s = it / p.qtiles;
             const int64_t t0 = s * p.tiles_per_split;
             const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-            const int64_t q = (int64_t)qt * BM + row;
+            const int64_t q = (int64_t)qt * QTILE + (int64_t)rank * BM + row;
             uint32_t best_o = 0xffffffffu, best_i = 0u;
             for (int64_t t = t0; t < t1; ++t, ++tcount) {
                 const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
@@ -326,7 +399,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&S.tempty[acc]);
+                if (PAIR) mbar_arrive_leader(&S.tempty[acc]);
+                else mbar_arrive(&S.tempty[acc]);
             }
             if (q < p.nq) atomicMin(&p.argmin_out[q], ((unsigned long long)best_o << 32) | best_i);
         }
@@ -362,19 +436,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
         unsigned pf_tau = 0xffffffffu;
         {
-            const int64_t it0 = blockIdx.x;
+            const int64_t it0 = unit;
             if (it0 < nitems) {
                 pf = norms4((it0 / p.qtiles) * p.tiles_per_split * BN);
-                const int64_t q0 = (int64_t)(it0 % p.qtiles) * BM + row;
+                const int64_t q0 = (int64_t)(it0 % p.qtiles) * QTILE + (int64_t)rank * BM + row;
                 if (q0 < p.nq) pf_tau = __ldcg(p.tau_g + q0);
             }
         }
-        for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        for (int64_t it = unit; it < nitems; it += nunits) {
             const int qt = (int)(it % p.qtiles);
             const int64_t s = it / p.qtiles;
             const int64_t t0 = s * p.tiles_per_split;
             const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-            const int64_t q = (int64_t)qt * BM + row;
+            const int64_t q = (int64_t)qt * QTILE + (int64_t)rank * BM + row;
             const bool qv = q < p.nq;
             const int64_t sub = s * 2 + half;
             const int64_t cbase = qv ? ((q * p.cb.n_sub + sub) * (int64_t)C) : 0;
@@ -400,12 +474,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 {   // prefetch for the next tile of this CTA's sequence
                     int64_t tn = t + 1, itn = it;
                     if (tn >= t1) {
-                        itn = it + gridDim.x;
+                        itn = it + nunits;
                         tn = (itn / p.qtiles) * p.tiles_per_split;
                     }
                     if (itn < nitems) {
                         pf = norms4(tn * BN);
-                        const int64_t qn = (int64_t)(itn % p.qtiles) * BM + row;
+                        const int64_t qn = (int64_t)(itn % p.qtiles) * QTILE + (int64_t)rank * BM + row;
                         pf_tau = (qn < p.nq) ? __ldcg(p.tau_g + qn) : 0xffffffffu;
                     }
                 }
@@ -512,7 +586,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 if (p.dbg) c_loop += clock64() - cl0;
                 tc_fence_before();
-                mbar_arrive(&S.tempty[acc]);
+                if (PAIR) mbar_arrive_leader(&S.tempty[acc]);
+                else mbar_arrive(&S.tempty[acc]);
             }
             if (qv) {
                 p.cb.cnt[q * p.cb.n_sub + sub] = cnt;
@@ -531,9 +606,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();   // the leader's MMAs also wrote this CTA's TMEM
     tc_fence_after();
     if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
     }
 }
 
@@ -677,6 +756,40 @@ bool make_map(CUtensorMap* map, const void* gaddr, int64_t rows, int d, int dp, 
 }
 }  // namespace
 
+// launch one variant of the phase-A kernel; CTA pairs go out as clusters of 2
+template <bool IP, int MODE, bool PAIR>
+cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& pr, unsigned grid,
+                      cudaStream_t st) {
+    auto kern = tc::k_enn_scan_tc<IP, MODE, PAIR>;
+    const size_t sm = tc::smem_bytes<PAIR>();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    if (PAIR) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+        cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = PAIR ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, ma, mb, pr);
+}
+
+// CTA pairs unless disabled (VS_TC_PAIR=0) or the batch fits one 128-query tile
+bool use_pair(int64_t nq) {
+    static const char* env = getenv("VS_TC_PAIR");
+    if (env) return env[0] == '1';
+    return nq > tc::BM;
+}
+
 bool tc_supported(int d, int dtype, int ip) {
     (void)dtype;
     (void)ip;
@@ -731,9 +844,11 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     }
     // tiling: work item = (query tile, data split); choose the split count
     // so items fill whole waves of SMs
-    const int qtiles = (int)((nq + tc::BM - 1) / tc::BM);
+    const bool pair = use_pair(nq);
+    const int qtile_rows = pair ? 2 * tc::BM : tc::BM;
+    const int qtiles = (int)((nq + qtile_rows - 1) / qtile_rows);
     const int64_t ntiles = (nsel + tc::BN - 1) / tc::BN;
-    const int sms = ctx->sm_count;
+    const int sms = pair ? ctx->sm_count / 2 : ctx->sm_count;   // work units (CTAs or pairs)
     int best_s = 1;
     double best_cost = 1e30;
     const int smin = std::max(1, (int)std::min<int64_t>(ntiles, (2 * sms + qtiles - 1) / qtiles));
@@ -766,7 +881,7 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     CK(cudaMemsetAsync(c.overflow, 0, nq * sizeof(int), st));
 
     CUtensorMap ma, mb;
-    if (!make_map(&ma, qa, nq, d, dp, tc::BM) || !make_map(&mb, xb, nsel, d, dp, tc::BN))
+    if (!make_map(&ma, qa, nq, d, dp, tc::BM) || !make_map(&mb, xb, nsel, d, dp, pair ? tc::BN / 2 : tc::BN))
         return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     tc::Params pr;
     pr.nq = nq;
@@ -791,16 +906,13 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
         CK(cudaMemsetAsync(pr.dbg, 0, 16 * sizeof(unsigned long long), st));
     }
     const int64_t items = (int64_t)qtiles * nsplit;
-    const unsigned grid = (unsigned)std::min<int64_t>(items, sms);
+    const unsigned units = (unsigned)std::min<int64_t>(items, sms);
+    const unsigned grid = pair ? 2 * units : units;
     pr.argmin_out = nullptr;
     if (sp.ip) {
-        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)tc::SMEM_BYTES));
-        tc::k_enn_scan_tc<true, 0><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+        CK((pair ? launch_tc<true, 0, true>(ma, mb, pr, grid, st) : launch_tc<true, 0, false>(ma, mb, pr, grid, st)));
     } else {
-        CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)tc::SMEM_BYTES));
-        tc::k_enn_scan_tc<false, 0><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+        CK((pair ? launch_tc<false, 0, true>(ma, mb, pr, grid, st) : launch_tc<false, 0, false>(ma, mb, pr, grid, st)));
     }
     CK(cudaGetLastError());
     ctx->stats[VS_STAT_LAUNCHES] += 1;
@@ -808,7 +920,7 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
         unsigned long long h[16];
         CK(cudaMemcpyAsync(h, pr.dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        const double ctas = (double)grid, thr = ctas * tc::EPI_THREADS;
+        const double ctas = (double)(pair ? units : grid), thr = (double)grid * tc::EPI_THREADS;
         fprintf(stderr,
                 "[vs_tc] grid=%u nsplit=%d per=%lld C=%lld tiles/cta=%.1f | producer wait-empty %.0f cyc/cta | "
                 "mma wait-full %.0f wait-tempty %.0f cyc/cta | epi wait-tfull %.0f compaction %.0f cyc/thr | "
@@ -842,10 +954,10 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
     CKS(arena_alloc(ctx, (size_t)chunk * dp, &xb));
     CKS(arena_alloc(ctx, 2, &junk));
     CK(cudaMemsetAsync(out, 0xff, n * sizeof(unsigned long long), st));
+    const bool pair = use_pair(n);
     CUtensorMap mb;
-    if (!make_map(&mb, cb, ncols, d, dp, tc::BN)) return set_err(VS_ERR_CUDA, "tensor map (columns)");
-    CK(cudaFuncSetAttribute(tc::k_enn_scan_tc<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)tc::SMEM_BYTES));
+    if (!make_map(&mb, cb, ncols, d, dp, pair ? tc::BN / 2 : tc::BN))
+        return set_err(VS_ERR_CUDA, "tensor map (columns)");
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
         const int64_t m = std::min(chunk, n - r0);
         const unsigned blocks = (unsigned)std::min<int64_t>((m * 32 + 255) / 256, 148 * 64);
@@ -863,14 +975,15 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
         pr.d = d;
         pr.kblocks = (d + tc::BK - 1) / tc::BK;
         pr.nsel = ncols;
-        pr.qtiles = (int)((m + tc::BM - 1) / tc::BM);
+        pr.qtiles = (int)((m + (pair ? 2 * tc::BM : tc::BM) - 1) / (pair ? 2 * tc::BM : tc::BM));
         pr.nsplit = 1;
         pr.ntiles = (ncols + tc::BN - 1) / tc::BN;
         pr.tiles_per_split = pr.ntiles;
         pr.xn = cnorm;
         pr.argmin_out = out + r0;
-        const unsigned grid = (unsigned)std::min<int64_t>(pr.qtiles, ctx->sm_count);
-        tc::k_enn_scan_tc<false, 1><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(ma, mb, pr);
+        const unsigned units = (unsigned)std::min<int64_t>(pr.qtiles, pair ? ctx->sm_count / 2 : ctx->sm_count);
+        CK((pair ? launch_tc<false, 1, true>(ma, mb, pr, 2 * units, st)
+                 : launch_tc<false, 1, false>(ma, mb, pr, units, st)));
         CK(cudaGetLastError());
         ctx->stats[VS_STAT_LAUNCHES] += 2;
     }
