@@ -172,10 +172,11 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
                         (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d));
     bool exhaustive = false;
     {
-        KTimer kt(ctx, job.cls_scan);
         if (use_tc) {
-            CKS(vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive));
+            // times its own GEMM launch under job.cls_scan (staging under VS_K_STAGE)
+            CKS(vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive, job.cls_scan));
         } else {
+            KTimer kt(ctx, job.cls_scan);
             const int64_t qtiles = (job.nq + 127) / 128;
             const int64_t target = (int64_t)ctx->sm_count * 4;  // 2 CTAs/SM x 2 waves
             int64_t n_split = std::max<int64_t>(1, (target + qtiles - 1) / qtiles);

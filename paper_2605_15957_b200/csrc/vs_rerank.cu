@@ -33,7 +33,7 @@ constexpr int WARP_D_MAX = 2048;
 // sort buffers (KMAX x 16 B)
 constexpr size_t UNION_BYTES = 32768;
 __host__ __device__ __forceinline__ size_t union_bytes(int d) {
-    const size_t rows = (size_t)NWARP * (size_t)((d + 3) & ~3) * 4;
+    const size_t rows = (size_t)NWARP * 2 * (size_t)((d + 3) & ~3) * 4;   // two staged rows per warp
     return (d <= WARP_D_MAX && rows > UNION_BYTES) ? rows : UNION_BYTES;
 }
 
@@ -41,8 +41,13 @@ struct Small {
     long long red[NWARP];
     int counter;
     int nleaf;
+    int nnode;
     int leaf_off[MAXLEAF];
     int leaf_n[MAXLEAF];
+    // combine tree of numpy's recursion: value slots 0..nleaf-1 are the leaves
+    // (left to right), slot nleaf + j = slot node_a[j] + slot node_b[j]
+    int node_a[MAXLEAF];
+    int node_b[MAXLEAF];
 };
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
@@ -195,48 +200,49 @@ __device__ void np_leaves(int d, Small& S) {
         st_n[sp] = n2;
     }
     S.nleaf = nl;
-}
-
-// the recursion's combine order applied to precomputed leaf values
-__device__ double np_combine(const double* leafv, int d) {
-    if (d <= 128) return leafv[0];
-    int st_n[16], st_state[16];
-    double st_left[16];
-    int sp = 0, next = 0;
-    st_n[0] = d;
+    // internal nodes in post-order (each combines two earlier slots)
+    int st_n2[16], st_state[16], st_left[16];
+    int sp2 = 0, next_leaf = 0, nn = 0, ret = 0;
+    st_n2[0] = d;
     st_state[0] = 0;
-    double ret = 0.0;
-    while (sp >= 0) {
-        const int m = st_n[sp];
+    if (d <= 128) {
+        S.nnode = 0;
+        return;
+    }
+    while (sp2 >= 0) {
+        const int m = st_n2[sp2];
         if (m <= 128) {
-            ret = leafv[next++];
-            --sp;
+            ret = next_leaf++;
+            --sp2;
             continue;
         }
         int n2 = m / 2;
         n2 -= n2 % 8;
-        if (st_state[sp] == 0) {
-            st_state[sp] = 1;
-            ++sp;
-            st_n[sp] = n2;
-            st_state[sp] = 0;
-        } else if (st_state[sp] == 1) {
-            st_left[sp] = ret;
-            st_state[sp] = 2;
-            ++sp;
-            st_n[sp] = m - n2;
-            st_state[sp] = 0;
+        if (st_state[sp2] == 0) {
+            st_state[sp2] = 1;
+            ++sp2;
+            st_n2[sp2] = n2;
+            st_state[sp2] = 0;
+        } else if (st_state[sp2] == 1) {
+            st_left[sp2] = ret;
+            st_state[sp2] = 2;
+            ++sp2;
+            st_n2[sp2] = m - n2;
+            st_state[sp2] = 0;
         } else {
-            ret = __dadd_rn(st_left[sp], ret);
-            --sp;
+            S.node_a[nn] = st_left[sp2];
+            S.node_b[nn] = ret;
+            ret = nl + nn;
+            ++nn;
+            --sp2;
         }
     }
-    return ret;
+    S.nnode = nn;
 }
 
-template <bool IP>
-__device__ __forceinline__ double term_sm(const float* q, const float* x, int i) {
-    const double a = (double)q[i], b = (double)x[i];
+template <bool IP, typename T>
+__device__ __forceinline__ double term_sm(const float* q, const T* x, int i) {
+    const double a = (double)q[i], b = (double)ld_elem(x + i);
     if (IP) return __dmul_rn(a, b);
     const double t = __dsub_rn(a, b);
     return __dmul_rn(t, t);
@@ -246,8 +252,8 @@ __device__ __forceinline__ double term_sm(const float* q, const float* x, int i)
 // 8-way-unrolled accumulation chains (elements off + j + 8m, in order),
 // then fold each leaf's chains in numpy's order, and lane 0 applies the
 // recursion's combine tree. Bit-identical to np_pairwise.
-template <bool IP>
-__device__ double warp_np_score(const float* q, const float* x, int d, const Small& S, double* cbuf,
+template <bool IP, typename T>
+__device__ double warp_np_score(const float* q, const T* x, int d, const Small& S, double* cbuf,
                                 double* lbuf, int lane) {
     const int nleaf = S.nleaf;
     const int nch = nleaf * 8;
@@ -255,8 +261,8 @@ __device__ double warp_np_score(const float* q, const float* x, int d, const Sma
         const int L = c >> 3, j = c & 7;
         const int off = S.leaf_off[L], n = S.leaf_n[L];
         const int lim = n - (n % 8);
-        double r = term_sm<IP>(q, x, off + j);
-        for (int i = 8 + j; i < lim; i += 8) r = __dadd_rn(r, term_sm<IP>(q, x, off + i));
+        double r = term_sm<IP, T>(q, x, off + j);
+        for (int i = 8 + j; i < lim; i += 8) r = __dadd_rn(r, term_sm<IP, T>(q, x, off + i));
         cbuf[c] = r;
     }
     __syncwarp();
@@ -265,27 +271,38 @@ __device__ double warp_np_score(const float* q, const float* x, int d, const Sma
         double res = __dadd_rn(__dadd_rn(__dadd_rn(cb[0], cb[1]), __dadd_rn(cb[2], cb[3])),
                                __dadd_rn(__dadd_rn(cb[4], cb[5]), __dadd_rn(cb[6], cb[7])));
         const int off = S.leaf_off[L], n = S.leaf_n[L];
-        for (int i = n - (n % 8); i < n; ++i) res = __dadd_rn(res, term_sm<IP>(q, x, off + i));
+        for (int i = n - (n % 8); i < n; ++i) res = __dadd_rn(res, term_sm<IP, T>(q, x, off + i));
         lbuf[L] = res;
     }
     __syncwarp();
+    // lane 0 folds the leaves along numpy's recursion (node list in smem)
     double sc = 0.0;
-    if (lane == 0) sc = np_combine(lbuf, d);
+    if (lane == 0) {
+        const int nn = S.nnode;
+        for (int j = 0; j < nn; ++j) lbuf[nleaf + j] = __dadd_rn(lbuf[S.node_a[j]], lbuf[S.node_b[j]]);
+        sc = nn ? lbuf[nleaf + nn - 1] : lbuf[0];   // the root is the last node
+    }
     sc = __shfl_sync(VS_FULL, sc, 0);
     return sc;
 }
 
-// stage one row (float or bf16) into shared memory as floats, coalesced
+// stage one row into shared memory (same element type), coalesced; 16-byte
+// cp.async chunks when the row size allows, so the copy overlaps compute
 template <typename T>
-__device__ __forceinline__ void stage_row(const T* __restrict__ src, float* dst, int d, int lane) {
-    if (sizeof(T) == 4 && (d % 4) == 0) {
-        const float4* s4 = reinterpret_cast<const float4*>(src);
-        float4* d4 = reinterpret_cast<float4*>(dst);
-        for (int i = lane; i < d / 4; i += 32) d4[i] = __ldg(s4 + i);
+__device__ __forceinline__ void stage_row_async(const T* __restrict__ src, T* dst, int d, int lane) {
+    const int bytes = d * (int)sizeof(T);
+    if ((bytes & 15) == 0) {
+        const char* s8 = reinterpret_cast<const char*>(src);
+        const uint32_t d8 = (uint32_t)__cvta_generic_to_shared(dst);
+        for (int off = lane * 16; off < bytes; off += 32 * 16)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d8 + off), "l"(s8 + off) : "memory");
     } else {
-        for (int i = lane; i < d; i += 32) dst[i] = ld_elem(src + i);
+        for (int i = lane; i < d; i += 32) dst[i] = src[i];
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 }  // namespace
 
 template <typename T, bool IP>
@@ -294,8 +311,8 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     Small& sm = *reinterpret_cast<Small*>(smraw);
     unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));       // union region
     double* cbuf = reinterpret_cast<double*>(u + union_bytes(p.d));          // [NWARP][8*MAXLEAF]
-    double* lbuf = cbuf + NWARP * 8 * MAXLEAF;                               // [NWARP][MAXLEAF]
-    float* qs = reinterpret_cast<float*>(lbuf + NWARP * MAXLEAF);            // [d]
+    double* lbuf = cbuf + NWARP * 8 * MAXLEAF;                               // [NWARP][2*MAXLEAF]
+    float* qs = reinterpret_cast<float*>(lbuf + NWARP * 2 * MAXLEAF);        // [d]
     int* cnts = reinterpret_cast<int*>(qs + ((p.d + 3) & ~3));               // [nsub]
 
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -414,20 +431,44 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     // 3. exact float64 scores (bit-identical to the reference)
     const T* rows = reinterpret_cast<const T*>(p.rows);
     if (warp_path) {
-        float* xw = reinterpret_cast<float*>(u) + (size_t)w * d;
+        // double-buffered: the next survivor row is staged (cp.async-free plain
+        // 128-bit loads issued before scoring) while the current one is scored
+        const int dpad = (d + 7) & ~7;
+        T* xw0 = reinterpret_cast<T*>(u) + (size_t)w * 2 * dpad;
+        T* xw1 = xw0 + dpad;
         double* cb = cbuf + w * 8 * MAXLEAF;
-        double* lb = lbuf + w * MAXLEAF;
-        for (int64_t i = w; i < ns; i += NWARP) {
-            const uint32_t ps = spos[i];
-            const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
-            stage_row<T>(rows + r * (int64_t)d, xw, d, lane);
-            __syncwarp();
-            const double sc = warp_np_score<IP>(qs, xw, d, sm, cb, lb, lane);
-            if (lane == 0) {
-                skey[i] = d2o(IP ? -sc : sc);
-                sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+        double* lb = lbuf + w * 2 * MAXLEAF;
+        int64_t i = w;
+        int64_t r_cur = 0;
+        uint32_t ps_cur = 0;
+        if (i < ns) {
+            ps_cur = spos[i];
+            r_cur = p.row_map ? p.row_map[ps_cur] : (int64_t)ps_cur;
+            stage_row_async<T>(rows + r_cur * (int64_t)d, xw0, d, lane);
+        }
+        for (int buf = 0; i < ns; i += NWARP, buf ^= 1) {
+            T* cur = buf ? xw1 : xw0;
+            T* nxt = buf ? xw0 : xw1;
+            const int64_t inext = i + NWARP;
+            uint32_t ps_n = 0;
+            int64_t r_n = 0;
+            if (inext < ns) {
+                ps_n = spos[inext];
+                r_n = p.row_map ? p.row_map[ps_n] : (int64_t)ps_n;
+                stage_row_async<T>(rows + r_n * (int64_t)d, nxt, d, lane);
+                async_wait_prev();   // the current row has landed, the next is in flight
+            } else {
+                async_wait_all();
             }
             __syncwarp();
+            const double sc = warp_np_score<IP, T>(qs, cur, d, sm, cb, lb, lane);
+            if (lane == 0) {
+                skey[i] = d2o(IP ? -sc : sc);
+                sid[i] = p.id_map ? p.id_map[ps_cur] : r_cur + p.id_offset;
+            }
+            __syncwarp();
+            ps_cur = ps_n;
+            r_cur = r_n;
         }
     } else {
         for (int64_t i = tid; i < ns; i += NT) {
@@ -462,7 +503,7 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
 
 static size_t rerank_smem(int d, int nsub) {
     return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d) + (size_t)NWARP * 8 * MAXLEAF * 8 +
-           (size_t)NWARP * MAXLEAF * 8 + (size_t)((d + 3) & ~3) * 4 + (size_t)nsub * 4 + 16;
+           (size_t)NWARP * 2 * MAXLEAF * 8 + (size_t)((d + 3) & ~3) * 4 + (size_t)nsub * 4 + 16;
 }
 
 template <typename T>

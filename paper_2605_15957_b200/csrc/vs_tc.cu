@@ -801,7 +801,7 @@ bool tc_profitable(int64_t nq, int64_t nsel, int d) {
 }
 
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift, CandBuf* cb,
-                bool* exhaustive) {
+                bool* exhaustive, int timer_class) {
     // first pass: local top-k buffers verified by phase B; re-runs (cshift > 0)
     // keep the full margin band, which is exact by construction
     const int topk_mode = (cshift == 0 && !getenv("VS_TC_MARGIN_MODE")) ? 1 : 0;
@@ -909,6 +909,7 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     const unsigned units = (unsigned)std::min<int64_t>(items, sms);
     const unsigned grid = pair ? 2 * units : units;
     pr.argmin_out = nullptr;
+    KTimer kt_scan(ctx, timer_class);
     if (sp.ip) {
         CK((pair ? launch_tc<true, 0, true>(ma, mb, pr, grid, st) : launch_tc<true, 0, false>(ma, mb, pr, grid, st)));
     } else {

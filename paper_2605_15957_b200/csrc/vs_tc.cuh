@@ -14,7 +14,7 @@ bool tc_profitable(int64_t nq, int64_t nsel, int d);
 // runs phase A on the tensor cores; fills `cb` (allocated by the callee from
 // the context arena) and may rewrite sp.margin with the tensor-core error bound
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift,
-                CandBuf* cb, bool* exhaustive);
+                CandBuf* cb, bool* exhaustive, int timer_class);
 
 // first-min nearest column (squared L2) of every row on the tensor cores
 int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, const __nv_bfloat16* cb,
