@@ -172,6 +172,9 @@ int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t 
                   const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
                   int64_t* out_ids, double* out_dist, int32_t* out_count,
                   int32_t* out_probes, int64_t* out_visited);
+/* list sharding: per-list 0/1 ownership mask of this shard
+ * (nullable = all lists owned). Probes still use every centroid. */
+int vs_ivf_set_owned(vs_ivf* ivf, const uint8_t* list_owned);
 int vs_ivf_free(vs_ivf* ivf);
 
 #ifdef __cplusplus

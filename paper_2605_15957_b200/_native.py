@@ -58,6 +58,7 @@ SIGNATURES = {
     "vs_ivf_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "vs_ivf_search": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp,
                                 _vp, C.POINTER(_i64)]),
+    "vs_ivf_set_owned": (C.c_int, [_vp, _vp]),
     "vs_ivf_free": (C.c_int, [_vp]),
 }
 
@@ -219,6 +220,7 @@ class DeviceIvf:
     def __init__(self, ctx: Context, handle):
         self.ctx = ctx
         self.handle = handle
+        self.owned_key = None
         nlist, d, metric, dtype = _i32(), _i32(), _i32(), _i32()
         n_total = _i64()
         check(load().vs_ivf_info(handle, C.byref(nlist), C.byref(d), C.byref(n_total),

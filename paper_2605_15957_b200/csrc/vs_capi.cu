@@ -706,6 +706,21 @@ int vs_ivf_export(vs_ivf* ivf, float* centroids, int64_t* list_sizes, int64_t* l
     return VS_OK;
 }
 
+int vs_ivf_set_owned(vs_ivf* ivf, const uint8_t* list_owned) {
+    if (!ivf) return set_err(VS_ERR_PARAMETER, "null ivf");
+    DevGuard g(ivf->ctx->device);
+    cudaStream_t s = ivf->ctx->stream;
+    if (!list_owned) {
+        if (ivf->owned) CK(cudaFree(ivf->owned));
+        ivf->owned = nullptr;
+        return VS_OK;
+    }
+    if (!ivf->owned) CK(cudaMalloc(&ivf->owned, ivf->nlist));
+    CK(cudaMemcpyAsync(ivf->owned, list_owned, ivf->nlist, cudaMemcpyDefault, s));
+    CK(cudaStreamSynchronize(s));
+    return VS_OK;
+}
+
 int vs_ivf_free(vs_ivf* v) {
     if (!v) return VS_OK;
     DevGuard g(v->ctx->device);
@@ -745,15 +760,25 @@ struct IvfJob {
 int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift) {
     if (job.nq == 0) return VS_OK;
     const vs_ivf* v = job.ivf;
-    const int64_t target = (int64_t)ctx->sm_count * 8;
-    int n_psplit = (int)std::min<int64_t>(job.nprobe, std::max<int64_t>(1, (target + job.nq - 1) / job.nq));
-    const int n_sub = n_psplit * 8;
-    int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
-    // the largest number of rows one warp can see bounds the buffer need
+    // the largest number of rows one buffer can see bounds the buffer need
     int64_t max_list = 0;
     for (int i = 0; i < v->nlist; ++i) max_list = std::max(max_list, v->h_off[i + 1] - v->h_off[i]);
-    const int64_t per = (job.nprobe + n_psplit - 1) / n_psplit;
-    const int64_t bound = pow2ceil(per * max_list + 64);
+    const int dp = (v->d + 127) / 128 * 128;
+    const bool lmajor = ctx->opt_ivf_kernel != 1 && (v->d % 4) == 0 && v->d <= vs::kIvfLmDMax;
+    int n_sub, n_psplit = 1;
+    int64_t bound;
+    if (lmajor) {
+        // one buffer per (query, probe rank): each sees one list
+        n_sub = job.nprobe;
+        bound = pow2ceil(max_list + 64);
+    } else {
+        const int64_t target = (int64_t)ctx->sm_count * 8;
+        n_psplit = (int)std::min<int64_t>(job.nprobe, std::max<int64_t>(1, (target + job.nq - 1) / job.nq));
+        n_sub = n_psplit * 8;
+        const int64_t per = (job.nprobe + n_psplit - 1) / n_psplit;
+        bound = pow2ceil(per * max_list + 64);
+    }
+    int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
     const bool exhaustive = C >= bound;
     if (exhaustive) C = bound;
     vs::CandBuf cb;
@@ -770,23 +795,79 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         CKS(arena_alloc(ctx, 1, &vis));
         CK(cudaMemsetAsync(vis, 0, sizeof(unsigned long long), ctx->stream));
     }
-    vs::IvfScanParams sp;
-    sp.Q = job.q;
-    sp.nq = job.nq;
-    sp.d = v->d;
-    sp.payload = v->payload;
-    sp.list_off = v->list_off;
-    sp.probes = job.probes;
-    sp.nprobe = job.nprobe;
-    sp.list_owned = v->owned;
-    sp.pbits = job.pbits;
-    sp.margin = margin;
-    sp.ip = v->metric;
-    sp.k = job.k;
-    sp.n_psplit = n_psplit;
-    sp.cb = cb;
-    sp.visited = vis;
-    {
+    if (lmajor) {
+        // group the batch's (query, probe) pairs by list, cut into units
+        const int64_t npairs = job.nq * (int64_t)job.nprobe;
+        vs::IvfGroupArgs g;
+        g.probes = job.probes;
+        g.nq = job.nq;
+        g.nprobe = job.nprobe;
+        g.nlist = v->nlist;
+        g.owned = v->owned;
+        CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_in));
+        CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_out));
+        CKS(arena_alloc(ctx, (size_t)npairs, &g.vals_in));
+        CKS(arena_alloc(ctx, (size_t)npairs, &g.pair_codes));
+        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.cnt));
+        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.qoff));
+        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.ucnt));
+        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.uoff));
+        const int64_t max_units = vs::ivf_max_units(job.nq, job.nprobe, v->nlist);
+        CKS(arena_alloc(ctx, (size_t)max_units, &g.units));
+        g.tmp_bytes = vs::ivf_group_temp_bytes(npairs, v->nlist);
+        char* gtmp = nullptr;
+        CKS(arena_alloc(ctx, g.tmp_bytes, &gtmp));
+        g.tmp = gtmp;
+        int* work = nullptr;
+        CKS(arena_alloc(ctx, 1, &work));
+        CK(cudaMemsetAsync(work, 0, sizeof(int), ctx->stream));
+        CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
+        {
+            KTimer kt(ctx, VS_K_SELECT);
+            CK(vs::launch_ivf_group(g, ctx->stream));
+        }
+        ctx->stats[VS_STAT_LAUNCHES] += 6;
+        vs::IvfLmParams lp;
+        lp.Q = job.q;
+        lp.nq = job.nq;
+        lp.d = v->d;
+        lp.dp = dp;
+        lp.payload = v->payload;
+        lp.list_off = v->list_off;
+        lp.nprobe = job.nprobe;
+        lp.pbits = job.pbits;
+        lp.pair_codes = g.pair_codes;
+        lp.units = g.units;
+        lp.n_units = g.uoff + v->nlist;
+        lp.max_units = max_units;
+        lp.work = work;
+        lp.margin = margin;
+        lp.ip = v->metric;
+        lp.k = job.k;
+        lp.cb = cb;
+        lp.visited = vis;
+        {
+            KTimer kt(ctx, VS_K_IVF_SCAN);
+            if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_lmajor<float>(lp, ctx->sm_count, ctx->stream));
+            else CK(vs::launch_ivf_scan_lmajor<__nv_bfloat16>(lp, ctx->sm_count, ctx->stream));
+        }
+    } else {
+        vs::IvfScanParams sp;
+        sp.Q = job.q;
+        sp.nq = job.nq;
+        sp.d = v->d;
+        sp.payload = v->payload;
+        sp.list_off = v->list_off;
+        sp.probes = job.probes;
+        sp.nprobe = job.nprobe;
+        sp.list_owned = v->owned;
+        sp.pbits = job.pbits;
+        sp.margin = margin;
+        sp.ip = v->metric;
+        sp.k = job.k;
+        sp.n_psplit = n_psplit;
+        sp.cb = cb;
+        sp.visited = vis;
         KTimer kt(ctx, VS_K_IVF_SCAN);
         if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_qmajor<float>(sp, ctx->stream));
         else CK(vs::launch_ivf_scan_qmajor<__nv_bfloat16>(sp, ctx->stream));

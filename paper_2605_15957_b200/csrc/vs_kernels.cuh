@@ -86,6 +86,56 @@ struct IvfScanParams {
 template <typename T>
 cudaError_t launch_ivf_scan_qmajor(const IvfScanParams& p, cudaStream_t s);
 
+// ---- phase A: IVF list scan (list-major) ------------------------------------------------
+// (query, probe) pairs grouped by list; units of <= kIvfLmQT pairs of one list
+constexpr int kIvfLmQT = 16;
+constexpr int kIvfLmDMax = 1024;   // list-major scan: query held in registers
+struct IvfGroupArgs {
+    const int32_t* probes;      // [nq][nprobe]
+    int64_t nq;
+    int nprobe;
+    int nlist;
+    const uint8_t* owned;       // nullable
+    int32_t* keys_in;           // [nq*nprobe]
+    int32_t* keys_out;          // [nq*nprobe]
+    int32_t* vals_in;           // [nq*nprobe]
+    int32_t* pair_codes;        // [nq*nprobe] out: q*nprobe + j, grouped by list
+    int32_t* cnt;               // [nlist+1]
+    int32_t* qoff;              // [nlist+1]
+    int32_t* ucnt;              // [nlist+1]
+    int32_t* uoff;              // [nlist+1] out: uoff[nlist] = number of units
+    int4* units;                // [ivf_max_units] out: (list, first pair, pairs, 0)
+    void* tmp;
+    size_t tmp_bytes;           // >= ivf_group_temp_bytes
+};
+size_t ivf_group_temp_bytes(int64_t npairs, int nlist);
+int64_t ivf_max_units(int64_t nq, int nprobe, int nlist);
+cudaError_t launch_ivf_group(const IvfGroupArgs& g, cudaStream_t s);
+
+struct IvfLmParams {
+    const float* Q;
+    int64_t nq;
+    int d;
+    int dp;                     // d rounded up to 128 (query staging stride)
+    const void* payload;
+    const int64_t* list_off;
+    int nprobe;
+    const uint32_t* pbits;      // nullable
+    const int32_t* pair_codes;
+    const int4* units;
+    const int32_t* n_units;     // device scalar (uoff[nlist])
+    int64_t max_units;
+    int* work;                  // zeroed work counter
+    const float* margin;
+    int ip;
+    int k;
+    CandBuf cb;                 // n_sub = nprobe: one buffer per (query, probe rank)
+    unsigned long long* visited;
+};
+size_t ivf_lmajor_smem(int dp, int dtype_bytes);
+template <typename T>
+cudaError_t launch_ivf_scan_lmajor(const IvfLmParams& p, int sm_count, cudaStream_t s);
+
 // ---- phase B: exact float64 re-rank + tie-rule top-k ------------------------------------
 struct RerankParams {
     const float* Q;

@@ -203,6 +203,11 @@ int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64
                                     std::max(1, (int)std::ceil(std::log2((double)nlist + 1))), st);
     void* sort_tmp = nullptr;
     CK(ctx->arena.alloc(sort_bytes + 256, &sort_tmp));
+    // row staging for the tensor-core assignment, allocated once for all iterations
+    __nv_bfloat16* xb_scratch = nullptr;
+    unsigned* junk = nullptr;
+    CKS(arena_alloc(ctx, (size_t)tc_argmin_chunk(n) * dp, &xb_scratch));
+    CKS(arena_alloc(ctx, 2, &junk));
 
     const float* xf = data->dtype == VS_DTYPE_F32 ? (const float*)data->data : nullptr;
     const __nv_bfloat16* xbf = data->dtype == VS_DTYPE_BF16 ? (const __nv_bfloat16*)data->data : nullptr;
@@ -219,8 +224,8 @@ int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64
         CK(cudaGetLastError());
         CK(cudaMemsetAsync(cmax, 0, sizeof(unsigned), st));
         CK(launch_row_norms<float>(c32, nlist, d, cnorm, cmax, st));
-        CKS(tc_stage_bf16(ctx, c32, nlist, d, cb));
-        CKS(tc_argmin_rows(ctx, data->data, data->dtype, n, d, cb, cnorm, nlist, packed));
+        CKS(tc_stage_bf16(ctx, c32, nlist, d, cb, junk));
+        CKS(tc_argmin_rows(ctx, data->data, data->dtype, n, d, cb, cnorm, nlist, packed, xb_scratch, junk));
         k_unpack<<<grid_for(n), 256, 0, st>>>(packed, data->norms, n, assign, dist);
         CK(cudaGetLastError());
         ctx->stats[VS_STAT_LAUNCHES] += 4;

@@ -943,17 +943,16 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
 // row of x, on the tensor cores: the k-means assignment step. `cb` holds the
 // columns (centroids) already staged as bf16 [ncols][dp] with their fp32
 // norms; rows are staged here in chunks. out[r] = (orderable key << 32) | col.
+int64_t tc_argmin_chunk(int64_t n) { return std::min<int64_t>(n, (int64_t)1 << 22); }
+
 int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, const __nv_bfloat16* cb,
-                   const float* cnorm, int64_t ncols, unsigned long long* out) {
+                   const float* cnorm, int64_t ncols, unsigned long long* out, __nv_bfloat16* xb,
+                   unsigned* junk) {
     using namespace vs_internal;
     if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cudaStream_t st = ctx->stream;
     const int dp = (d + 7) / 8 * 8;
-    const int64_t chunk = std::min<int64_t>(n, (int64_t)1 << 22);
-    __nv_bfloat16* xb = nullptr;
-    unsigned* junk = nullptr;
-    CKS(arena_alloc(ctx, (size_t)chunk * dp, &xb));
-    CKS(arena_alloc(ctx, 2, &junk));
+    const int64_t chunk = tc_argmin_chunk(n);
     CK(cudaMemsetAsync(out, 0xff, n * sizeof(unsigned long long), st));
     const bool pair = use_pair(n);
     CUtensorMap mb;
@@ -992,11 +991,9 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
 }
 
 // stage a float32 matrix to bf16 [n][dp] (no norms)
-int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out) {
+int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out, unsigned* junk) {
     using namespace vs_internal;
     const int dp = (d + 7) / 8 * 8;
-    unsigned* junk = nullptr;
-    CKS(arena_alloc(ctx, 2, &junk));
     const unsigned blocks = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 148 * 64);
     tc::k_stage_rows<float><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, out, nullptr, junk);
     CK(cudaGetLastError());

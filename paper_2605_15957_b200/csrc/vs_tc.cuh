@@ -16,10 +16,14 @@ bool tc_profitable(int64_t nq, int64_t nsel, int d);
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift,
                 CandBuf* cb, bool* exhaustive, int timer_class);
 
-// first-min nearest column (squared L2) of every row on the tensor cores
+// first-min nearest column (squared L2) of every row on the tensor cores.
+// `scratch` = tc_argmin_scratch() bf16 elements + 2 words, allocated once by
+// the caller (the k-means loop calls this every iteration).
+int64_t tc_argmin_chunk(int64_t n);
 int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, const __nv_bfloat16* cb,
-                   const float* cnorm, int64_t ncols, unsigned long long* out);
-int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out);
+                   const float* cnorm, int64_t ncols, unsigned long long* out, __nv_bfloat16* xb,
+                   unsigned* junk);
+int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out, unsigned* junk);
 
 int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows, uint64_t seed,
                   int32_t metric, int32_t max_iters, vs_ivf** out);

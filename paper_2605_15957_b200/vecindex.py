@@ -407,16 +407,27 @@ class IvfIndex:
                         self.centroids, self.partitions, None, base=base)
 
     def device_index(self, ctx: N.Context, list_owned=None) -> N.DeviceIvf:
-        """Device list-contiguous copy of this index (cached per device)."""
-        key = (ctx.device, None if list_owned is None else bytes(np.asarray(list_owned, np.uint8)))
-        div = self._dev.get(key) or (self._dev.get(ctx.device) if list_owned is None else None)
-        if div is not None:
-            return div
+        """Device list-contiguous copy of this index (one per device). With
+        `list_owned` (list sharding) the same copy scans only the
+        owned lists; ownership is applied with vs_ivf_set_owned."""
+        div = self._dev.get(ctx.device)
+        if div is None:
+            div = self._dev[ctx.device] = self._make_device_index(ctx)
+        key = None if list_owned is None else bytes(np.ascontiguousarray(list_owned, np.uint8))
+        if key is not None and len(key) != self.nlist:
+            raise ShapeError(f"list_owned has {len(key)} entries, expected nlist={self.nlist}")
+        if div.owned_key != key:
+            owned = None if key is None else np.frombuffer(key, np.uint8).copy()
+            N.check(N.load().vs_ivf_set_owned(div.handle, N.ptr(owned)), "ivf_set_owned")
+            div.owned_key = key
+        return div
+
+    def _make_device_index(self, ctx: N.Context) -> N.DeviceIvf:
         sizes = np.array([len(p) for p in self.partitions], np.int64)
         ids = np.ascontiguousarray(np.concatenate(self.partitions).astype(np.int64)) \
             if self.partitions else np.empty(0, np.int64)
         cen = np.ascontiguousarray(self.centroids, np.float32)
-        owned = None if list_owned is None else np.ascontiguousarray(list_owned, np.uint8)
+        owned = None
         h = C.c_void_p()
         if self.layout == OWNING and self.payload is not None and not isinstance(self.payload, _LazyPayload):
             pay = np.ascontiguousarray(np.concatenate(self.payload, axis=0), np.float32) \
@@ -432,9 +443,7 @@ class IvfIndex:
             N.check(N.load().vs_ivf_create(ctx.handle, N.ptr(cen), self.nlist, self.dim, N.ptr(sizes),
                                            N.ptr(ids), None, dc.dtype, N.METRIC_CODE[self.metric],
                                            dc.handle, N.ptr(owned), C.byref(h)), "ivf_create")
-        div = N.DeviceIvf(ctx, h)
-        self._dev[key] = div
-        return div
+        return N.DeviceIvf(ctx, h)
 
     def search(self, queries, params: SearchParams, row_filter=None, device=None,
                list_owned=None) -> NeighborTable:

@@ -1,0 +1,123 @@
+"""Both IVF list-scan kernels (query-major and list-major, VS_OPT_IVF_KERNEL
+1 / 2) against the oracle restatement of IvfIndex.search (vecindex.py:230-258,
+filtered extension of SURVEY §8c): identical probes, identical ids,
+bit-identical float64 distances, identical visited counts."""
+
+import numpy as np
+import pytest
+
+import paper_2605_15957_b200 as vs
+from oracle import sqlvs_oracle as O
+from paper_2605_15957_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _index(rng, n, d, nlist, metric="squared_l2", skew=False):
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    centroids = data[rng.choice(n, nlist, replace=False)].copy()
+    if skew:  # one giant list (longer than a 2048-row selection segment)
+        centroids[0] = 0.0
+    assign = np.argmin(O.pairwise_sq_l2_fast(data, centroids), axis=1)
+    parts = [np.flatnonzero(assign == c).astype(np.int64) for c in range(nlist)]
+    payload = [data[p] for p in parts]
+    idx = vs.IvfIndex(nlist, d, n, metric, "owning", centroids, parts, payload)
+    return idx, data, centroids, parts, payload
+
+
+def _check(idx, queries, centroids, parts, payload, nprobe, k, metric, mask, kernel):
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_IVF_KERNEL, kernel)
+    try:
+        nt = idx.search(queries, vs.SearchParams(k=k, nprobe=nprobe), row_filter=mask)
+    finally:
+        ctx.set_option(N.OPT_IVF_KERNEL, 0)
+    ref = O.ivf_search(queries, centroids, parts, lambda c: payload[c], nprobe, k, metric, mask=mask)
+    assert np.array_equal(nt.probes, ref.probes)
+    assert np.array_equal(nt.query_row, ref.query_row)
+    assert np.array_equal(nt.data_row, ref.data_row)
+    assert np.array_equal(nt.distance, ref.distance)
+    assert nt.visited_rows == ref.visited_rows
+    return nt
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+@pytest.mark.parametrize("d,sel", [(64, 0.05), (128, None), (100, 0.3), (384, 0.01), (1024, 0.02)])
+def test_ivf_kernels_vs_oracle(kernel, metric, d, sel):
+    rng = np.random.default_rng(d * 7 + (kernel if sel is None else 3))
+    n, nlist = 12000, 48
+    idx, data, centroids, parts, payload = _index(rng, n, d, nlist, metric)
+    queries = rng.standard_normal((70, d)).astype(np.float32)
+    mask = None if sel is None else rng.random(n) < sel
+    for nprobe, k in ((1, 10), (6, 25), (nlist, 10)):
+        _check(idx, queries, centroids, parts, payload, nprobe, k, metric, mask, kernel)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_ivf_kernels_long_list_and_many_queries_per_list(kernel):
+    # a list longer than one selection segment, and > QT queries per list
+    rng = np.random.default_rng(5)
+    idx, data, centroids, parts, payload = _index(rng, 30000, 64, 8, skew=True)
+    assert max(len(p) for p in parts) > 4096
+    queries = rng.standard_normal((200, 64)).astype(np.float32) * 0.1
+    for mask in (None, rng.random(30000) < 0.5):
+        _check(idx, queries, centroids, parts, payload, 3, 40, "squared_l2", mask, kernel)
+
+
+def test_ivf_kernels_empty_lists_and_empty_filter():
+    rng = np.random.default_rng(9)
+    idx, data, centroids, parts, payload = _index(rng, 3000, 32, 16)
+    queries = rng.standard_normal((30, 32)).astype(np.float32)
+    empty = np.zeros(3000, bool)
+    for kernel in (1, 2):
+        nt = _check(idx, queries, centroids, parts, payload, 4, 5, "squared_l2", empty, kernel)
+        assert nt.data_row.size == 0
+    # a filter that keeps a handful of rows: most queries get short results
+    few = np.zeros(3000, bool)
+    few[rng.choice(3000, 7, replace=False)] = True
+    for kernel in (1, 2):
+        _check(idx, queries, centroids, parts, payload, 16, 5, "squared_l2", few, kernel)
+
+
+def test_ivf_lmajor_bf16_payload_matches_qmajor():
+    """bf16-stored payload (cfg4 storage): both kernels return the same exact
+    top-k over the bf16-rounded rows (the oracle is fed the rounded values)."""
+    import torch
+    rng = np.random.default_rng(21)
+    n, d, nlist = 10000, 96, 32
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    xb = torch.from_numpy(data).to(torch.bfloat16)
+    rounded = xb.float().numpy()
+    col = vs.EmbeddingColumn.from_device(xb.cuda())
+    idx = vs.IvfIndex.build(col, nlist, seed=0)
+    queries = rng.standard_normal((40, d)).astype(np.float32)
+    mask = rng.random(n) < 0.2
+    payload = [rounded[p] for p in idx.partitions]
+    for kernel in (1, 2):
+        _check(idx, queries, idx.centroids, idx.partitions, payload, 5, 12, "squared_l2", mask, kernel)
+
+
+def test_ivf_lmajor_list_sharding_plus_merge():
+    from paper_2605_15957_b200.distributed import lpt_assign
+    rng = np.random.default_rng(13)
+    idx, data, centroids, parts, payload = _index(rng, 9000, 64, 24)
+    q = rng.standard_normal((33, 64)).astype(np.float32)
+    mask = rng.random(9000) < 0.4
+    owner = lpt_assign([len(p) for p in parts], 4)
+    outs = [idx.search_raw(q, 9, 6, row_filter=mask, list_owned=(owner == r).astype(np.uint8))
+            for r in range(4)]
+    ids = np.ascontiguousarray(np.stack([o[0] for o in outs]))
+    dist = np.ascontiguousarray(np.stack([o[1] for o in outs]))
+    cnt = np.ascontiguousarray(np.stack([o[2] for o in outs]))
+    oi, od, oc = np.empty((33, 9), np.int64), np.empty((33, 9)), np.empty(33, np.int32)
+    ctx = N.Context.get()
+    N.check(N.load().vs_topk_merge(ctx.handle, 4, 33, 9, N.ptr(ids), N.ptr(dist), N.ptr(cnt), 9, 0,
+                                   N.ptr(oi), N.ptr(od), N.ptr(oc)))
+    whole = idx.search(q, vs.SearchParams(k=9, nprobe=6), row_filter=mask)
+    m = np.arange(9)[None, :] < oc[:, None]
+    assert np.array_equal(oi[m], whole.data_row)
+    assert np.array_equal(od[m], whole.distance)
+    # ownership reset: the same device copy scans every list again
+    again = idx.search(q, vs.SearchParams(k=9, nprobe=6), row_filter=mask)
+    assert np.array_equal(again.data_row, whole.data_row)
