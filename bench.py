@@ -578,13 +578,17 @@ class IvfWorkload:
         probed lists; also checks our results for those queries bit-exactly."""
         from oracle import sqlvs_oracle as O
         t0 = time.perf_counter()
-        done, res = 0, None
-        while done < len(self.cpu_q) and time.perf_counter() - t0 < args.cpu_budget:
-            res = O.ivf_search(self.cpu_q[done:done + 1], self.index.centroids, self.index.partitions,
-                               lambda c: self.cpu_lists[c], self.nprobe, self.k, mask=self.mask_host)
-            if done == 0:
-                first = res
-            done += 1
+        done, first = 0, None
+        try:
+            while done < len(self.cpu_q) and time.perf_counter() - t0 < args.cpu_budget:
+                res = O.ivf_search(self.cpu_q[done:done + 1], self.index.centroids, self.index.partitions,
+                                   lambda c: self.cpu_lists[c], self.nprobe, self.k, mask=self.mask_host)
+                if done == 0:
+                    first = res
+                done += 1
+        except KeyError as e:   # the oracle probed a list our probes did not: parity failure
+            return {"value": None, "unit": "queries/s", "cores": 1, "kind": "port",
+                    "sample": f"ABORTED: oracle probe {e} not among our probed lists (probe parity failure)"}
         el = time.perf_counter() - t0
         ids, dist, cnt, probes, _ = self.index.search_raw(self.cpu_q[:1], self.k, self.nprobe,
                                                           row_filter=self.bits_host, list_owned=self.owned)

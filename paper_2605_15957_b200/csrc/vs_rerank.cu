@@ -32,13 +32,34 @@ constexpr int WARP_D_MAX = 2048;
 // union of: live candidates (LCAP x 8 B), staged rows (NWARP x d x 4 B),
 // sort buffers (KMAX x 16 B)
 constexpr size_t UNION_BYTES = 32768;
-__host__ __device__ __forceinline__ size_t union_bytes(int d) {
-    const size_t rows = (size_t)NWARP * 2 * (size_t)((d + 3) & ~3) * 4;   // two staged rows per warp
-    return (d <= WARP_D_MAX && rows > UNION_BYTES) ? rows : UNION_BYTES;
+// staged row stride (elements): padded d plus the leaf skews (32 B per leaf;
+// leaves hold >= 64 elements, so at most d / 64 + 1 of them)
+__host__ __device__ __forceinline__ int row_stride(int d) { return ((d + 7) & ~7) + 16 * (d / 64 + 1); }
+__host__ __device__ __forceinline__ int q_stride(int d) { return ((d + 3) & ~3) + 8 * (d / 64 + 1); }
+// number of leaves of numpy's pairwise recursion over n elements (blocks of
+// <= 128 are leaves; larger blocks split at n/2 rounded down to a multiple of 8)
+__host__ __device__ inline int np_nleaf(int n) {
+    if (n <= 128) return 1;
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_nleaf(n2) + np_nleaf(n - n2);
 }
+// register path of the exact scorer: every lane owns two chains of one leaf
+// for the whole row (<= 8 leaves), rows read straight from global memory
+__host__ __device__ inline bool reg_path_ok(int d) { return d >= 8 && d <= 1024 && d % 2 == 0 && np_nleaf(d) <= 8; }
+__host__ __device__ __forceinline__ size_t union_bytes(int d) {
+    const size_t rows = (size_t)NWARP * 2 * (size_t)row_stride(d) * 4;   // two staged rows per warp
+    return (d <= WARP_D_MAX && !reg_path_ok(d) && rows > UNION_BYTES) ? rows : UNION_BYTES;
+}
+
+constexpr int HBINS = 2048;     // radix-select histogram bins (11 bits)
+constexpr int SHQ = 8;          // per-leaf shared-memory skew of the staged query (floats)
 
 struct Small {
     long long red[NWARP];
+    unsigned wtot[NWARP];
+    int sel_bin;
+    unsigned sel_below;
     int counter;
     int nleaf;
     int nnode;
@@ -48,7 +69,63 @@ struct Small {
     // (left to right), slot nleaf + j = slot node_a[j] + slot node_b[j]
     int node_a[MAXLEAF];
     int node_b[MAXLEAF];
+    // leaf index of every 8-element group: the lanes of one warp walk four
+    // consecutive leaves at once, and leaves often start at multiples of 32
+    // words, so leaf L is staged 32 * L bytes after its natural offset to put
+    // the four leaves' lanes on distinct shared-memory banks
+    unsigned char gsk[WARP_D_MAX / 8];
 };
+
+// k-th smallest (1 <= k <= count) orderable key among the keys `foreach`
+// visits: a 3-pass radix select (11 + 11 + 10 bits) over a shared-memory
+// histogram, instead of a 32-step bisection over the keys.
+template <class ForEach>
+__device__ uint32_t block_radix_kth(ForEach foreach, unsigned k, unsigned* hist, Small& sm) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t prefix = 0u, pmask = 0u;
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+        const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+        const int nb = pass == 2 ? 1024 : 2048;
+        for (int i = tid; i < nb; i += NT) hist[i] = 0u;
+        __syncthreads();
+        foreach([&](uint32_t u) {
+            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & (uint32_t)(nb - 1)], 1u);
+        });
+        __syncthreads();
+        const int per = nb / NT;
+        unsigned loc = 0;
+        for (int b = 0; b < per; ++b) loc += hist[tid * per + b];
+        unsigned incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(VS_FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) sm.wtot[w] = incl;
+        __syncthreads();
+        unsigned excl = incl - loc;
+        for (int i = 0; i < w; ++i) excl += sm.wtot[i];
+        if (excl < k && k <= excl + loc) {
+            unsigned c = excl;
+            for (int b = 0; b < per; ++b) {
+                const unsigned h = hist[tid * per + b];
+                if (c + h >= k) {
+                    sm.sel_bin = tid * per + b;
+                    sm.sel_below = c;
+                    break;
+                }
+                c += h;
+            }
+        }
+        __syncthreads();
+        k -= sm.sel_below;
+        prefix |= (uint32_t)sm.sel_bin << shift;
+        pmask |= (uint32_t)(nb - 1) << shift;
+        __syncthreads();
+    }
+    return prefix;
+}
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -200,6 +277,9 @@ __device__ void np_leaves(int d, Small& S) {
         st_n[sp] = n2;
     }
     S.nleaf = nl;
+    for (int L = 0; L < nl && L < MAXLEAF; ++L)
+        for (int g = S.leaf_off[L] / 8; g < (S.leaf_off[L] + S.leaf_n[L] + 7) / 8; ++g)
+            S.gsk[g] = (unsigned char)L;
     // internal nodes in post-order (each combines two earlier slots)
     int st_n2[16], st_state[16], st_left[16];
     int sp2 = 0, next_leaf = 0, nn = 0, ret = 0;
@@ -240,6 +320,10 @@ __device__ void np_leaves(int d, Small& S) {
     S.nnode = nn;
 }
 
+// staged-row skew per class, in elements: 32 bytes (8 banks)
+template <typename T>
+__host__ __device__ constexpr int shx() { return 32 / (int)sizeof(T); }
+
 template <bool IP, typename T>
 __device__ __forceinline__ double term_sm(const float* q, const T* x, int i) {
     const double a = (double)q[i], b = (double)ld_elem(x + i);
@@ -255,14 +339,18 @@ __device__ __forceinline__ double term_sm(const float* q, const T* x, int i) {
 template <bool IP, typename T>
 __device__ double warp_np_score(const float* q, const T* x, int d, const Small& S, double* cbuf,
                                 double* lbuf, int lane) {
+    // q and x are staged skewed: leaf L's elements start SHQ * L floats (q)
+    // and shx<T>() * L elements (x) after their natural offset
     const int nleaf = S.nleaf;
     const int nch = nleaf * 8;
     for (int c = lane; c < nch; c += 32) {
         const int L = c >> 3, j = c & 7;
         const int off = S.leaf_off[L], n = S.leaf_n[L];
+        const float* qL = q + SHQ * L;
+        const T* xL = x + shx<T>() * L;
         const int lim = n - (n % 8);
-        double r = term_sm<IP, T>(q, x, off + j);
-        for (int i = 8 + j; i < lim; i += 8) r = __dadd_rn(r, term_sm<IP, T>(q, x, off + i));
+        double r = term_sm<IP, T>(qL, xL, off + j);
+        for (int i = 8 + j; i < lim; i += 8) r = __dadd_rn(r, term_sm<IP, T>(qL, xL, off + i));
         cbuf[c] = r;
     }
     __syncwarp();
@@ -271,7 +359,9 @@ __device__ double warp_np_score(const float* q, const T* x, int d, const Small& 
         double res = __dadd_rn(__dadd_rn(__dadd_rn(cb[0], cb[1]), __dadd_rn(cb[2], cb[3])),
                                __dadd_rn(__dadd_rn(cb[4], cb[5]), __dadd_rn(cb[6], cb[7])));
         const int off = S.leaf_off[L], n = S.leaf_n[L];
-        for (int i = n - (n % 8); i < n; ++i) res = __dadd_rn(res, term_sm<IP, T>(q, x, off + i));
+        const float* qL = q + SHQ * L;
+        const T* xL = x + shx<T>() * L;
+        for (int i = n - (n % 8); i < n; ++i) res = __dadd_rn(res, term_sm<IP, T>(qL, xL, off + i));
         lbuf[L] = res;
     }
     __syncwarp();
@@ -286,18 +376,84 @@ __device__ double warp_np_score(const float* q, const T* x, int d, const Small& 
     return sc;
 }
 
-// stage one row into shared memory (same element type), coalesced; 16-byte
-// cp.async chunks when the row size allows, so the copy overlaps compute
 template <typename T>
-__device__ __forceinline__ void stage_row_async(const T* __restrict__ src, T* dst, int d, int lane) {
+struct Pair2;
+template <>
+struct Pair2<float> {
+    static __device__ __forceinline__ float2 ld(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+};
+template <>
+struct Pair2<__nv_bfloat16> {
+    static __device__ __forceinline__ float2 ld(const __nv_bfloat16* p) {
+        return __bfloat1622float2(__ldg(reinterpret_cast<const __nv_bfloat162*>(p)));
+    }
+};
+
+template <bool IP>
+__device__ __forceinline__ double term_d(float qf, float xf) {
+    const double a = (double)qf, b = (double)xf;
+    if (IP) return __dmul_rn(a, b);
+    const double t = __dsub_rn(a, b);
+    return __dmul_rn(t, t);
+}
+
+// Exact float64 score of one row held in registers: lane (L, p) = (lane >> 2,
+// lane & 3) owns chains 2p and 2p + 1 of leaf L (elements off + 2p + {0,1} +
+// 8m); the leaf's 8 chains fold with two xor-shuffles in numpy's order
+// ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)); lane p = 0 adds the leaf
+// tail; the combine tree runs on shuffles with slot s held by lane s.
+template <bool IP, typename T>
+__device__ __forceinline__ double warp_np_score_reg(const float2 (&qr)[16], const float2 (&xr)[16], int M,
+                                                    const float* qtail, const T* xtail, int ntail,
+                                                    const Small& S, int lane) {
+    double r0 = 0.0, r1 = 0.0;
+    if (M > 0) {
+        r0 = term_d<IP>(qr[0].x, xr[0].x);
+        r1 = term_d<IP>(qr[0].y, xr[0].y);
+    }
+#pragma unroll
+    for (int m = 1; m < 16; ++m) {
+        if (m < M) {
+            r0 = __dadd_rn(r0, term_d<IP>(qr[m].x, xr[m].x));
+            r1 = __dadd_rn(r1, term_d<IP>(qr[m].y, xr[m].y));
+        }
+    }
+    double v = __dadd_rn(r0, r1);
+    v = __dadd_rn(v, __shfl_xor_sync(VS_FULL, v, 1));
+    v = __dadd_rn(v, __shfl_xor_sync(VS_FULL, v, 2));
+    if ((lane & 3) == 0)
+        for (int i = 0; i < ntail; ++i) v = __dadd_rn(v, term_d<IP>(qtail[i], ld_elem(xtail + i)));
+    const int nleaf = S.nleaf, nn = S.nnode;
+    double slot = __shfl_sync(VS_FULL, v, (lane * 4) & 31);   // lane L < nleaf: leaf L
+    for (int j = 0; j < nn; ++j) {
+        const double a = __shfl_sync(VS_FULL, slot, S.node_a[j]);
+        const double b = __shfl_sync(VS_FULL, slot, S.node_b[j]);
+        const double r = __dadd_rn(a, b);
+        if (lane == nleaf + j) slot = r;
+    }
+    return __shfl_sync(VS_FULL, slot, nn ? nleaf + nn - 1 : 0);
+}
+
+// stage one row into shared memory (same element type) in the skewed leaf
+// layout, coalesced; 16-byte cp.async chunks when the row size allows, so the
+// copy overlaps compute. Leaves split at multiples of 8 elements, so a chunk
+// never straddles two leaves.
+template <typename T>
+__device__ __forceinline__ void stage_row_async(const T* __restrict__ src, T* dst, int d, int lane,
+                                                const unsigned char* gsk) {
     const int bytes = d * (int)sizeof(T);
     if ((bytes & 15) == 0) {
+        constexpr int EPC = 16 / (int)sizeof(T);   // elements per chunk
         const char* s8 = reinterpret_cast<const char*>(src);
         const uint32_t d8 = (uint32_t)__cvta_generic_to_shared(dst);
-        for (int off = lane * 16; off < bytes; off += 32 * 16)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d8 + off), "l"(s8 + off) : "memory");
+        for (int off = lane * 16; off < bytes; off += 32 * 16) {
+            const int e = off / (int)sizeof(T);
+            const int sk = gsk[e / 8] * shx<T>() * (int)sizeof(T);
+            (void)EPC;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d8 + off + sk), "l"(s8 + off) : "memory");
+        }
     } else {
-        for (int i = lane; i < d; i += 32) dst[i] = src[i];
+        for (int i = lane; i < d; i += 32) dst[i + gsk[i / 8] * shx<T>()] = src[i];
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -306,14 +462,15 @@ __device__ __forceinline__ void async_wait_all() { asm volatile("cp.async.wait_g
 }  // namespace
 
 template <typename T, bool IP>
-__global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
+__global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     Small& sm = *reinterpret_cast<Small*>(smraw);
     unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));       // union region
     double* cbuf = reinterpret_cast<double*>(u + union_bytes(p.d));          // [NWARP][8*MAXLEAF]
     double* lbuf = cbuf + NWARP * 8 * MAXLEAF;                               // [NWARP][2*MAXLEAF]
-    float* qs = reinterpret_cast<float*>(lbuf + NWARP * 2 * MAXLEAF);        // [d]
-    int* cnts = reinterpret_cast<int*>(qs + ((p.d + 3) & ~3));               // [nsub]
+    float* qs = reinterpret_cast<float*>(lbuf + NWARP * 2 * MAXLEAF);        // [q_stride] (skewed)
+    int* cnts = reinterpret_cast<int*>(qs + q_stride(p.d));                  // [nsub]
+    unsigned* hist = reinterpret_cast<unsigned*>(cnts + ((p.cb.n_sub + 3) & ~3));   // [HBINS]
 
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const int64_t q = blockIdx.x;
@@ -321,8 +478,12 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     const int d = p.d;
     const bool warp_path = d >= 8 && d <= WARP_D_MAX;
     if (tid == 0 && warp_path) np_leaves(d, sm);
+    __syncthreads();
     const float* qg = p.Q + q * (int64_t)d;
-    for (int i = tid; i < d; i += NT) qs[i] = qg[i];
+    if (warp_path)
+        for (int i = tid; i < d; i += NT) qs[i + SHQ * sm.gsk[i / 8]] = qg[i];
+    else
+        for (int i = tid; i < d; i += NT) qs[i] = qg[i];
     long long tot = 0;
     for (int s = tid; s < nsub; s += NT) {
         const int c = p.cb.cnt[q * nsub + s];
@@ -376,15 +537,12 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
         // 1. k-th smallest approximate key  2. survivors (shared-memory path)
         uint32_t thr_o = 0xffffffffu;
         if (nl > p.k) {
-            uint32_t lo = 0u, hi = pre;
-            while (lo < hi) {
-                const uint32_t mid = lo + ((hi - lo) >> 1);
-                long long c = 0;
-                for (int i = tid; i < nl; i += NT) c += (f2o(lkey[i]) <= mid);
-                c = block_sum_ll(c, sm.red);
-                if (c >= p.k) hi = mid; else lo = mid + 1;
-            }
-            thr_o = f2o(__fadd_ru(o2f(lo), p.margin[q]));
+            const uint32_t kth = block_radix_kth(
+                [&](auto fn) {
+                    for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
+                },
+                (unsigned)p.k, hist, sm);
+            thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
         }
         if (tid == 0) sm.counter = 0;
         __syncthreads();
@@ -400,16 +558,17 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
         // global-memory path (very wide near-tie sets)
         uint32_t thr_o = 0xffffffffu;
         if (tot > p.k) {
-            uint32_t lo = 0u, hi = pre;
-            while (lo < hi) {
-                const uint32_t mid = lo + ((hi - lo) >> 1);
-                long long c = 0;
-                for (int s = w; s < nsub; s += NWARP)
-                    for (int j = lane; j < cnts[s]; j += 32) c += (f2o(ckey[(int64_t)s * C + j]) <= mid);
-                c = block_sum_ll(c, sm.red);
-                if (c >= p.k) hi = mid; else lo = mid + 1;
-            }
-            thr_o = f2o(__fadd_ru(o2f(lo), p.margin[q]));
+            // nl > LCAP >= k live keys (key <= pre): their k-th smallest
+            const uint32_t kth = block_radix_kth(
+                [&](auto fn) {
+                    for (int s = w; s < nsub; s += NWARP)
+                        for (int j = lane; j < cnts[s]; j += 32) {
+                            const uint32_t o = f2o(ckey[(int64_t)s * C + j]);
+                            if (o <= pre) fn(o);
+                        }
+                },
+                (unsigned)p.k, hist, sm);
+            thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
         }
         if (tid == 0) sm.counter = 0;
         __syncthreads();
@@ -430,10 +589,38 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
 
     // 3. exact float64 scores (bit-identical to the reference)
     const T* rows = reinterpret_cast<const T*>(p.rows);
-    if (warp_path) {
+    if (reg_path_ok(d)) {
+        // lane (L, p): chains 2p, 2p + 1 of leaf L; its query pairs in registers
+        const int L = lane >> 2, pp = lane & 3;
+        const bool on = L < sm.nleaf;
+        const int offL = on ? sm.leaf_off[L] : 0, nL = on ? sm.leaf_n[L] : 0;
+        const int M = nL / 8;
+        const int ntail = ((lane & 3) == 0) ? nL - 8 * M : 0;
+        float2 qr[16];
+        const float* qL = qs + SHQ * (on ? L : 0);     // skewed staging of the query
+#pragma unroll
+        for (int m = 0; m < 16; ++m)
+            qr[m] = m < M ? make_float2(qL[offL + 2 * pp + 8 * m], qL[offL + 2 * pp + 8 * m + 1])
+                          : make_float2(0.f, 0.f);
+        const float* qtail = qL + offL + 8 * M;
+        for (int64_t i = w; i < ns; i += NWARP) {
+            const uint32_t ps = spos[i];
+            const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
+            const T* xg = rows + r * (int64_t)d + offL;
+            float2 xr[16];
+#pragma unroll
+            for (int m = 0; m < 16; ++m)
+                xr[m] = m < M ? Pair2<T>::ld(xg + 2 * pp + 8 * m) : make_float2(0.f, 0.f);
+            const double sc = warp_np_score_reg<IP, T>(qr, xr, M, qtail, xg + 8 * M, ntail, sm, lane);
+            if (lane == 0) {
+                skey[i] = d2o(IP ? -sc : sc);
+                sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+            }
+        }
+    } else if (warp_path) {
         // double-buffered: the next survivor row is staged (cp.async-free plain
         // 128-bit loads issued before scoring) while the current one is scored
-        const int dpad = (d + 7) & ~7;
+        const int dpad = row_stride(d);
         T* xw0 = reinterpret_cast<T*>(u) + (size_t)w * 2 * dpad;
         T* xw1 = xw0 + dpad;
         double* cb = cbuf + w * 8 * MAXLEAF;
@@ -444,7 +631,7 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
         if (i < ns) {
             ps_cur = spos[i];
             r_cur = p.row_map ? p.row_map[ps_cur] : (int64_t)ps_cur;
-            stage_row_async<T>(rows + r_cur * (int64_t)d, xw0, d, lane);
+            stage_row_async<T>(rows + r_cur * (int64_t)d, xw0, d, lane, sm.gsk);
         }
         for (int buf = 0; i < ns; i += NWARP, buf ^= 1) {
             T* cur = buf ? xw1 : xw0;
@@ -455,7 +642,7 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
             if (inext < ns) {
                 ps_n = spos[inext];
                 r_n = p.row_map ? p.row_map[ps_n] : (int64_t)ps_n;
-                stage_row_async<T>(rows + r_n * (int64_t)d, nxt, d, lane);
+                stage_row_async<T>(rows + r_n * (int64_t)d, nxt, d, lane, sm.gsk);
                 async_wait_prev();   // the current row has landed, the next is in flight
             } else {
                 async_wait_all();
@@ -486,24 +673,32 @@ __global__ void __launch_bounds__(NT) k_rerank(RerankParams p) {
     // 5. verification of the local-top-k pass: every dropped candidate e had
     //    approx key > tau_g, hence exact key > tau_g - margin/2; the result is
     //    exact iff the k-th exact key + margin/2 < tau_g. Otherwise re-run.
-    if (p.verify && tg != 0xffffffffu && tid == 0) {
-        const int keff = (int)min((int64_t)p.k, ns);
-        const uint64_t* sk = reinterpret_cast<const uint64_t*>(u);  // sorted keys left by the top-k
-        double kth = keff > 0 ? o2d(sk[keff - 1]) : 0.0;             // exact key (-score for IP)
+    if (p.verify && tg != 0xffffffffu && w == 0) {
+        double qq = 0.0;
         if (!IP) {
-            double qq = 0.0;
-            for (int i = 0; i < d; ++i) qq += (double)qs[i] * (double)qs[i];
-            kth -= qq * (1.0 + 1e-12);  // approx keys omit ||q||^2
+            for (int i = lane; i < d; i += 32) {
+                const double a = (double)qg[i];
+                qq = fma(a, a, qq);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(VS_FULL, qq, o);
         }
-        const double bound = (double)o2f(tg) - 0.5 * (double)p.margin[q];
-        const double slack = fabs(bound) * 1e-6 + 1e-12;
-        if (keff < p.k || !(kth < bound - slack)) p.cb.overflow[q] = 1;
+        if (lane == 0) {
+            const int keff = (int)min((int64_t)p.k, ns);
+            const uint64_t* sk = reinterpret_cast<const uint64_t*>(u);  // sorted keys left by the top-k
+            double kth = keff > 0 ? o2d(sk[keff - 1]) : 0.0;             // exact key (-score for IP)
+            if (!IP) kth -= qq * (1.0 + 1e-12);  // approx keys omit ||q||^2
+            const double bound = (double)o2f(tg) - 0.5 * (double)p.margin[q];
+            const double slack = fabs(bound) * 1e-6 + 1e-12;
+            if (keff < p.k || !(kth < bound - slack)) p.cb.overflow[q] = 1;
+        }
     }
 }
 
 static size_t rerank_smem(int d, int nsub) {
     return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d) + (size_t)NWARP * 8 * MAXLEAF * 8 +
-           (size_t)NWARP * 2 * MAXLEAF * 8 + (size_t)((d + 3) & ~3) * 4 + (size_t)nsub * 4 + 16;
+           (size_t)NWARP * 2 * MAXLEAF * 8 + (size_t)q_stride(d) * 4 +
+           (size_t)((nsub + 3) & ~3) * 4 + (size_t)HBINS * 4 + 16;
 }
 
 template <typename T>
