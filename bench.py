@@ -389,7 +389,9 @@ class ExactWorkload:
                                   "tcgen05_bf16" else "fp32 SIMT candidates") + "; f64 exact re-rank"
 
     def extras(self, ctx, N):
-        return {"survivors_per_query": round(ctx.stats()[N.STAT_SURVIVORS] / self.nq, 2)}
+        st = ctx.stats()
+        return {"survivors_per_query": round(st[N.STAT_SURVIVORS] / self.nq, 2),
+                "overflow_requeries_total": int(st[N.STAT_OVERFLOW_QUERIES])}
 
     def cpu_baseline(self, args):
         if self.cfg["id"] == 1:

@@ -137,6 +137,22 @@ template <typename T>
 cudaError_t launch_ivf_scan_lmajor(const IvfLmParams& p, int sm_count, cudaStream_t s);
 
 // ---- phase B: exact float64 re-rank + tie-rule top-k ------------------------------------
+// numpy's pairwise-summation plan for one row length d (<= 2048): leaves left
+// to right, internal nodes in post-order (slot nleaf + j = slot a_j + slot b_j),
+// and the leaf index of every 8-element group
+struct LeafPlan {
+    int nleaf;
+    int nnode;
+    int nlevels;                // depth of the combine tree (nodes of one level are independent)
+    int node_lvl[32];           // 0-based level of every node
+    int leaf_off[32];
+    int leaf_n[32];
+    int node_a[32];
+    int node_b[32];
+    unsigned char gsk[2048 / 8];
+};
+void np_leaves(int d, LeafPlan& plan);
+
 struct RerankParams {
     const float* Q;
     int64_t nq;
@@ -161,6 +177,9 @@ struct RerankParams {
     int32_t* out_ids32;         // [nq][k] (nullable; IVF probes)
     int32_t* out_count;         // [nq] (nullable)
     unsigned long long* n_survivors;
+    LeafPlan plan;              // filled by launch_rerank
+    int ubytes;                 // filled by launch_rerank: shared-memory union size
+    int reg_path;               // filled by launch_rerank: register-resident scorer
 };
 template <typename T>
 cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s);

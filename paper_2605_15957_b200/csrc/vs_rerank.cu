@@ -38,7 +38,7 @@ __host__ __device__ __forceinline__ int row_stride(int d) { return ((d + 7) & ~7
 __host__ __device__ __forceinline__ int q_stride(int d) { return ((d + 3) & ~3) + 8 * (d / 64 + 1); }
 // number of leaves of numpy's pairwise recursion over n elements (blocks of
 // <= 128 are leaves; larger blocks split at n/2 rounded down to a multiple of 8)
-__host__ __device__ inline int np_nleaf(int n) {
+inline int np_nleaf(int n) {
     if (n <= 128) return 1;
     int n2 = n / 2;
     n2 -= n2 % 8;
@@ -46,8 +46,8 @@ __host__ __device__ inline int np_nleaf(int n) {
 }
 // register path of the exact scorer: every lane owns two chains of one leaf
 // for the whole row (<= 8 leaves), rows read straight from global memory
-__host__ __device__ inline bool reg_path_ok(int d) { return d >= 8 && d <= 1024 && d % 2 == 0 && np_nleaf(d) <= 8; }
-__host__ __device__ __forceinline__ size_t union_bytes(int d) {
+inline bool reg_path_ok(int d) { return d >= 8 && d <= 1024 && d % 2 == 0 && np_nleaf(d) <= 8; }
+inline size_t union_bytes(int d) {
     const size_t rows = (size_t)NWARP * 2 * (size_t)row_stride(d) * 4;   // two staged rows per warp
     return (d <= WARP_D_MAX && !reg_path_ok(d) && rows > UNION_BYTES) ? rows : UNION_BYTES;
 }
@@ -55,25 +55,12 @@ __host__ __device__ __forceinline__ size_t union_bytes(int d) {
 constexpr int HBINS = 2048;     // radix-select histogram bins (11 bits)
 constexpr int SHQ = 8;          // per-leaf shared-memory skew of the staged query (floats)
 
-struct Small {
+struct Small : LeafPlan {
     long long red[NWARP];
     unsigned wtot[NWARP];
     int sel_bin;
     unsigned sel_below;
     int counter;
-    int nleaf;
-    int nnode;
-    int leaf_off[MAXLEAF];
-    int leaf_n[MAXLEAF];
-    // combine tree of numpy's recursion: value slots 0..nleaf-1 are the leaves
-    // (left to right), slot nleaf + j = slot node_a[j] + slot node_b[j]
-    int node_a[MAXLEAF];
-    int node_b[MAXLEAF];
-    // leaf index of every 8-element group: the lanes of one warp walk four
-    // consecutive leaves at once, and leaves often start at multiples of 32
-    // words, so leaf L is staged 32 * L bytes after its natural offset to put
-    // the four leaves' lanes on distinct shared-memory banks
-    unsigned char gsk[WARP_D_MAX / 8];
 };
 
 // k-th smallest (1 <= k <= count) orderable key among the keys `foreach`
@@ -250,8 +237,13 @@ __device__ void block_topk_exact(const uint64_t* __restrict__ key, const int64_t
     __syncthreads();
 }
 
-// leaves of numpy's pairwise recursion for a length-d reduction, left to right
-__device__ void np_leaves(int d, Small& S) {
+}  // namespace
+
+// leaves of numpy's pairwise recursion for a length-d reduction, left to right,
+// the combine tree, and the leaf index of every 8-element group (computed on
+// the host once per launch; the kernel copies it into shared memory)
+void np_leaves(int d, LeafPlan& S) {
+    S = LeafPlan{};
     int st_off[16], st_n[16];
     int sp = 0, nl = 0;
     st_off[0] = 0;
@@ -318,7 +310,17 @@ __device__ void np_leaves(int d, Small& S) {
         }
     }
     S.nnode = nn;
+    // levels: a node runs after both operands (leaves are level -1)
+    S.nlevels = 0;
+    for (int j = 0; j < nn; ++j) {
+        const int la = S.node_a[j] >= nl ? S.node_lvl[S.node_a[j] - nl] : -1;
+        const int lb = S.node_b[j] >= nl ? S.node_lvl[S.node_b[j] - nl] : -1;
+        S.node_lvl[j] = (la > lb ? la : lb) + 1;
+        if (S.node_lvl[j] + 1 > S.nlevels) S.nlevels = S.node_lvl[j] + 1;
+    }
 }
+
+namespace {
 
 // staged-row skew per class, in elements: 32 bytes (8 banks)
 template <typename T>
@@ -402,36 +404,69 @@ __device__ __forceinline__ double term_d(float qf, float xf) {
 // 8m); the leaf's 8 chains fold with two xor-shuffles in numpy's order
 // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)); lane p = 0 adds the leaf
 // tail; the combine tree runs on shuffles with slot s held by lane s.
+template <bool IP>
+__device__ __forceinline__ double term_dd(double a, float xf) {
+    const double b = (double)xf;
+    if (IP) return __dmul_rn(a, b);
+    const double t = __dsub_rn(a, b);
+    return __dmul_rn(t, t);
+}
+
+// Exact float64 scores of TWO rows held in registers (independent chains
+// interleaved for ILP; the float64 chains are latency-bound). Lane (L, p) =
+// (lane >> 2, lane & 3) owns chains 2p and 2p + 1 of leaf L (elements
+// off + 2p + {0,1} + 8m, numpy's accumulation order); the leaf's 8 chains fold
+// with two xor-shuffles in numpy's order ((r0 + r1) + (r2 + r3)) + ((r4 + r5) +
+// (r6 + r7)); lane p = 0 adds the leaf tail; the combine tree runs level by
+// level on shuffles (slot s held by lane s; lane nleaf + j computes node j).
+struct TreeLane {
+    int na, nb, lvl, nlevels, root, nleaf;
+};
+
 template <bool IP, typename T>
-__device__ __forceinline__ double warp_np_score_reg(const float2 (&qr)[16], const float2 (&xr)[16], int M,
-                                                    const float* qtail, const T* xtail, int ntail,
-                                                    const Small& S, int lane) {
-    double r0 = 0.0, r1 = 0.0;
+__device__ __forceinline__ void warp_np_score_reg2(const double* qpd, const float2 (&xa)[16], const float2 (&xb)[16],
+                                                   int M, const double* qtail, const T* xta, const T* xtb,
+                                                   int ntail, const TreeLane& tl, int lane, double& oa,
+                                                   double& ob) {
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
     if (M > 0) {
-        r0 = term_d<IP>(qr[0].x, xr[0].x);
-        r1 = term_d<IP>(qr[0].y, xr[0].y);
+        const double2 q = *reinterpret_cast<const double2*>(qpd);
+        a0 = term_dd<IP>(q.x, xa[0].x);
+        a1 = term_dd<IP>(q.y, xa[0].y);
+        b0 = term_dd<IP>(q.x, xb[0].x);
+        b1 = term_dd<IP>(q.y, xb[0].y);
     }
 #pragma unroll
     for (int m = 1; m < 16; ++m) {
         if (m < M) {
-            r0 = __dadd_rn(r0, term_d<IP>(qr[m].x, xr[m].x));
-            r1 = __dadd_rn(r1, term_d<IP>(qr[m].y, xr[m].y));
+            const double2 q = *reinterpret_cast<const double2*>(qpd + 8 * m);
+            a0 = __dadd_rn(a0, term_dd<IP>(q.x, xa[m].x));
+            b0 = __dadd_rn(b0, term_dd<IP>(q.x, xb[m].x));
+            a1 = __dadd_rn(a1, term_dd<IP>(q.y, xa[m].y));
+            b1 = __dadd_rn(b1, term_dd<IP>(q.y, xb[m].y));
         }
     }
-    double v = __dadd_rn(r0, r1);
-    v = __dadd_rn(v, __shfl_xor_sync(VS_FULL, v, 1));
-    v = __dadd_rn(v, __shfl_xor_sync(VS_FULL, v, 2));
-    if ((lane & 3) == 0)
-        for (int i = 0; i < ntail; ++i) v = __dadd_rn(v, term_d<IP>(qtail[i], ld_elem(xtail + i)));
-    const int nleaf = S.nleaf, nn = S.nnode;
-    double slot = __shfl_sync(VS_FULL, v, (lane * 4) & 31);   // lane L < nleaf: leaf L
-    for (int j = 0; j < nn; ++j) {
-        const double a = __shfl_sync(VS_FULL, slot, S.node_a[j]);
-        const double b = __shfl_sync(VS_FULL, slot, S.node_b[j]);
-        const double r = __dadd_rn(a, b);
-        if (lane == nleaf + j) slot = r;
+    double va = __dadd_rn(a0, a1), vb = __dadd_rn(b0, b1);
+    va = __dadd_rn(va, __shfl_xor_sync(VS_FULL, va, 1));
+    vb = __dadd_rn(vb, __shfl_xor_sync(VS_FULL, vb, 1));
+    va = __dadd_rn(va, __shfl_xor_sync(VS_FULL, va, 2));
+    vb = __dadd_rn(vb, __shfl_xor_sync(VS_FULL, vb, 2));
+    for (int i = 0; i < ntail; ++i) {
+        va = __dadd_rn(va, term_dd<IP>(qtail[i], ld_elem(xta + i)));
+        vb = __dadd_rn(vb, term_dd<IP>(qtail[i], ld_elem(xtb + i)));
     }
-    return __shfl_sync(VS_FULL, slot, nn ? nleaf + nn - 1 : 0);
+    double sa = __shfl_sync(VS_FULL, va, (lane * 4) & 31);   // lane L < nleaf: leaf L
+    double sb = __shfl_sync(VS_FULL, vb, (lane * 4) & 31);
+    for (int l = 0; l < tl.nlevels; ++l) {
+        const double pa = __shfl_sync(VS_FULL, sa, tl.na), qa = __shfl_sync(VS_FULL, sa, tl.nb);
+        const double pb = __shfl_sync(VS_FULL, sb, tl.na), qb = __shfl_sync(VS_FULL, sb, tl.nb);
+        if (tl.lvl == l) {
+            sa = __dadd_rn(pa, qa);
+            sb = __dadd_rn(pb, qb);
+        }
+    }
+    oa = __shfl_sync(VS_FULL, sa, tl.root);
+    ob = __shfl_sync(VS_FULL, sb, tl.root);
 }
 
 // stage one row into shared memory (same element type) in the skewed leaf
@@ -461,27 +496,54 @@ __device__ __forceinline__ void async_wait_prev() { asm volatile("cp.async.wait_
 __device__ __forceinline__ void async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 }  // namespace
 
+#ifdef VS_RERANK_PROFILE
+// per-phase cycle totals (thread 0 of every CTA), read by vs_debug_rerank_profile
+__device__ unsigned long long g_rr_prof[8];
+#define RR_MARK(i)                                                        \
+    do {                                                                  \
+        if (threadIdx.x == 0) {                                           \
+            const long long t_ = clock64();                               \
+            atomicAdd(&g_rr_prof[i], (unsigned long long)(t_ - rr_t));    \
+            rr_t = t_;                                                    \
+        }                                                                 \
+    } while (0)
+#else
+#define RR_MARK(i) do {} while (0)
+#endif
+
 template <typename T, bool IP>
 __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
+#ifdef VS_RERANK_PROFILE
+    long long rr_t = clock64();
+#endif
     extern __shared__ __align__(16) unsigned char smraw[];
     Small& sm = *reinterpret_cast<Small*>(smraw);
     unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));       // union region
-    double* cbuf = reinterpret_cast<double*>(u + union_bytes(p.d));          // [NWARP][8*MAXLEAF]
+    double* cbuf = reinterpret_cast<double*>(u + p.ubytes);                  // [NWARP][8*MAXLEAF]
     double* lbuf = cbuf + NWARP * 8 * MAXLEAF;                               // [NWARP][2*MAXLEAF]
     float* qs = reinterpret_cast<float*>(lbuf + NWARP * 2 * MAXLEAF);        // [q_stride] (skewed)
     int* cnts = reinterpret_cast<int*>(qs + q_stride(p.d));                  // [nsub]
     unsigned* hist = reinterpret_cast<unsigned*>(cnts + ((p.cb.n_sub + 3) & ~3));   // [HBINS]
+    double* qd = reinterpret_cast<double*>(hist + HBINS);                    // [q_stride] float64, skewed
 
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const int64_t q = blockIdx.x;
     const int C = p.cb.C, nsub = p.cb.n_sub;
     const int d = p.d;
     const bool warp_path = d >= 8 && d <= WARP_D_MAX;
-    if (tid == 0 && warp_path) np_leaves(d, sm);
+    if (warp_path) {
+        const int* src = reinterpret_cast<const int*>(&p.plan);
+        int* dst = reinterpret_cast<int*>(static_cast<LeafPlan*>(&sm));
+        for (int i = tid; i < (int)(sizeof(LeafPlan) / 4); i += NT) dst[i] = src[i];
+    }
     __syncthreads();
     const float* qg = p.Q + q * (int64_t)d;
     if (warp_path)
-        for (int i = tid; i < d; i += NT) qs[i + SHQ * sm.gsk[i / 8]] = qg[i];
+        for (int i = tid; i < d; i += NT) {
+            const float v = qg[i];
+            qs[i + SHQ * sm.gsk[i / 8]] = v;
+            qd[i + SHQ * sm.gsk[i / 8]] = (double)v;
+        }
     else
         for (int i = tid; i < d; i += NT) qs[i] = qg[i];
     long long tot = 0;
@@ -501,6 +563,7 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     // global one; survivors need key <= K* + margin <= tau_g + margin
     const uint32_t pre = (p.verify && tg != 0xffffffffu) ? f2o(__fadd_ru(o2f(tg), p.margin[q])) : tg;
 
+    RR_MARK(0);
     // 0. live candidates -> shared memory (one warp per buffer, coalesced)
     float* lkey = reinterpret_cast<float*>(u);
     uint32_t* lpos = reinterpret_cast<uint32_t*>(u + LCAP * 4);
@@ -534,6 +597,7 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     __syncthreads();
     int64_t ns = 0;
     if (nl <= LCAP) {
+        RR_MARK(1);
         // 1. k-th smallest approximate key  2. survivors (shared-memory path)
         uint32_t thr_o = 0xffffffffu;
         if (nl > p.k) {
@@ -587,34 +651,70 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
         ns = p.s_cap;
     }
 
+    RR_MARK(2);
     // 3. exact float64 scores (bit-identical to the reference)
     const T* rows = reinterpret_cast<const T*>(p.rows);
-    if (reg_path_ok(d)) {
+    if (p.reg_path) {
         // lane (L, p): chains 2p, 2p + 1 of leaf L; its query pairs in registers
         const int L = lane >> 2, pp = lane & 3;
         const bool on = L < sm.nleaf;
         const int offL = on ? sm.leaf_off[L] : 0, nL = on ? sm.leaf_n[L] : 0;
         const int M = nL / 8;
         const int ntail = ((lane & 3) == 0) ? nL - 8 * M : 0;
-        float2 qr[16];
-        const float* qL = qs + SHQ * (on ? L : 0);     // skewed staging of the query
+        const double* qdL = qd + SHQ * (on ? L : 0);   // skewed float64 staging of the query
+        const double* qpd = qdL + offL + 2 * pp;
+        const double* qtail = qdL + offL + 8 * M;
+        TreeLane tl;
+        {
+            const int sj = lane - sm.nleaf;
+            const bool isnode = sj >= 0 && sj < sm.nnode;
+            tl.na = isnode ? sm.node_a[sj] : lane;
+            tl.nb = isnode ? sm.node_b[sj] : lane;
+            tl.lvl = isnode ? sm.node_lvl[sj] : -1;
+            tl.nlevels = sm.nlevels;
+            tl.nleaf = sm.nleaf;
+            tl.root = sm.nnode ? sm.nleaf + sm.nnode - 1 : 0;
+        }
+        const int row_bytes = d * (int)sizeof(T);
+        auto row_of = [&](int64_t idx, uint32_t& ps) -> int64_t {
+            ps = spos[idx];
+            return p.row_map ? p.row_map[ps] : (int64_t)ps;
+        };
+        auto fetch = [&](float2 (&x)[16], int64_t r) {
+            const T* xg = rows + r * (int64_t)d + offL + 2 * pp;
 #pragma unroll
-        for (int m = 0; m < 16; ++m)
-            qr[m] = m < M ? make_float2(qL[offL + 2 * pp + 8 * m], qL[offL + 2 * pp + 8 * m + 1])
-                          : make_float2(0.f, 0.f);
-        const float* qtail = qL + offL + 8 * M;
-        for (int64_t i = w; i < ns; i += NWARP) {
-            const uint32_t ps = spos[i];
-            const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
-            const T* xg = rows + r * (int64_t)d + offL;
-            float2 xr[16];
-#pragma unroll
-            for (int m = 0; m < 16; ++m)
-                xr[m] = m < M ? Pair2<T>::ld(xg + 2 * pp + 8 * m) : make_float2(0.f, 0.f);
-            const double sc = warp_np_score_reg<IP, T>(qr, xr, M, qtail, xg + 8 * M, ntail, sm, lane);
+            for (int m = 0; m < 16; ++m) x[m] = m < M ? Pair2<T>::ld(xg + 8 * m) : make_float2(0.f, 0.f);
+        };
+        // two rows per iteration (rows i and i + NWARP of this warp)
+        for (int64_t i = w; i < ns; i += 2 * NWARP) {
+            const int64_t i2 = i + NWARP;
+            const bool hasb = i2 < ns;
+            // the next pair -> L2 while this pair is scored
+            for (int h = 0; h < 2; ++h) {
+                const int64_t ip = i + (2 + h) * NWARP;
+                if (ip < ns) {
+                    uint32_t pf;
+                    const char* base = reinterpret_cast<const char*>(rows + row_of(ip, pf) * (int64_t)d);
+                    for (int o = lane * 128; o < row_bytes; o += 32 * 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
+                }
+            }
+            uint32_t psa, psb = 0;
+            const int64_t ra = row_of(i, psa);
+            const int64_t rb = hasb ? row_of(i2, psb) : ra;
+            float2 xa[16], xb[16];
+            fetch(xa, ra);
+            fetch(xb, rb);
+            double sa, sb;
+            warp_np_score_reg2<IP, T>(qpd, xa, xb, M, qtail, rows + ra * (int64_t)d + offL + 8 * M,
+                                      rows + rb * (int64_t)d + offL + 8 * M, ntail, tl, lane, sa, sb);
             if (lane == 0) {
-                skey[i] = d2o(IP ? -sc : sc);
-                sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+                skey[i] = d2o(IP ? -sa : sa);
+                sid[i] = p.id_map ? p.id_map[psa] : ra + p.id_offset;
+                if (hasb) {
+                    skey[i2] = d2o(IP ? -sb : sb);
+                    sid[i2] = p.id_map ? p.id_map[psb] : rb + p.id_offset;
+                }
             }
         }
     } else if (warp_path) {
@@ -668,8 +768,10 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     }
     __syncthreads();
     if (tid == 0 && p.n_survivors) atomicAdd(p.n_survivors, (unsigned long long)ns);
+    RR_MARK(3);
     // 4. exact tie-rule top-k
     block_topk_exact(skey, sid, ns, p.k, sm, u, IP, q, p.out_ids, p.out_dist, p.out_ids32, p.out_count);
+    RR_MARK(4);
     // 5. verification of the local-top-k pass: every dropped candidate e had
     //    approx key > tau_g, hence exact key > tau_g - margin/2; the result is
     //    exact iff the k-th exact key + margin/2 < tau_g. Otherwise re-run.
@@ -698,12 +800,16 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
 static size_t rerank_smem(int d, int nsub) {
     return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d) + (size_t)NWARP * 8 * MAXLEAF * 8 +
            (size_t)NWARP * 2 * MAXLEAF * 8 + (size_t)q_stride(d) * 4 +
-           (size_t)((nsub + 3) & ~3) * 4 + (size_t)HBINS * 4 + 16;
+           (size_t)((nsub + 3) & ~3) * 4 + (size_t)HBINS * 4 + (size_t)q_stride(d) * 8 + 16;
 }
 
 template <typename T>
-cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s) {
-    if (p.nq == 0) return cudaSuccess;
+cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
+    if (p0.nq == 0) return cudaSuccess;
+    RerankParams p = p0;
+    if (p.d >= 8 && p.d <= WARP_D_MAX) np_leaves(p.d, p.plan);
+    p.ubytes = (int)union_bytes(p.d);
+    p.reg_path = reg_path_ok(p.d) ? 1 : 0;
     const size_t smem = rerank_smem(p.d, p.cb.n_sub);
     cudaError_t e;
     if (p.ip) {
@@ -717,6 +823,16 @@ cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s) {
     }
     return cudaGetLastError();
 }
+#ifdef VS_RERANK_PROFILE
+extern "C" int vs_debug_rerank_profile(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_rr_prof, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_rr_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 template cudaError_t launch_rerank<float>(const RerankParams&, cudaStream_t);
 template cudaError_t launch_rerank<__nv_bfloat16>(const RerankParams&, cudaStream_t);
 
