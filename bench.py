@@ -46,6 +46,9 @@ CONFIGS = {
             id=2, n=10_000_000, d=1024, q=10_000, k=100, sel=0.10),
     3: dict(name="cfg3: IVF-Flat nlist=16384 nprobe=32 top-10 over 10M x 1024 fp32, 1% bitmap, 10k queries",
             id=3, n=10_000_000, d=1024, q=10_000, k=10, sel=0.01, nlist=16384, nprobe=32),
+    4: dict(name="cfg4: IVF-Flat bf16 50M x 768, nlist=16384 nprobe=64 top-10, unfiltered, 10k queries, "
+                 "sharded by list", id=4, n=50_000_000, d=768, q=10_000, k=10, sel=None, nlist=16384,
+            nprobe=64, bf16=True, cpu_queries=4),
 }
 
 
@@ -175,6 +178,28 @@ def _device_slice(n, d, lo, hi, dev):
         s, e = max(a, lo), min(b, hi)
         out[s - lo:e - lo] = v[s - a:e - a]
     del synth
+    return out, c
+
+
+def _device_slice_bf16(n, d, lo, hi, dev):
+    """Rows [lo, hi) of the mixture law drawn chunk by chunk straight into
+    bfloat16 (the float32 collection would not fit next to the index)."""
+    import torch
+    chunk = 1 << 20
+    g = torch.Generator(device=dev)
+    g.manual_seed(42)
+    c = torch.randn(64, d, generator=g, device=dev)
+    c /= c.norm(dim=1, keepdim=True)
+    out = torch.empty(hi - lo, d, device=dev, dtype=torch.bfloat16)
+    for ci in range(lo // chunk, (hi + chunk - 1) // chunk):
+        a, b = ci * chunk, min(n, (ci + 1) * chunk)
+        gg = torch.Generator(device=dev)
+        gg.manual_seed(100_000 + ci)
+        asg = torch.randint(0, 64, (b - a,), generator=gg, device=dev)
+        v = c[asg] + 0.55 * torch.randn(b - a, d, generator=gg, device=dev)
+        v /= v.norm(dim=1, keepdim=True)
+        s_, e_ = max(a, lo), min(b, hi)
+        out[s_ - lo:e_ - lo] = v[s_ - a:e_ - a].to(torch.bfloat16)
     return out, c
 
 
@@ -433,15 +458,21 @@ class IvfWorkload:
         self.cfg, self.rank, self.world, self.dev = cfg, rank, world, dev
         self.k, self.nq, self.d, self.nprobe = cfg["k"], cfg["q"], cfg["d"], cfg["nprobe"]
         n, d = cfg["n"], cfg["d"]
+        self.bf16 = bool(cfg.get("bf16"))
+        self.index_dtype = "bf16" if self.bf16 else "f32"
         t0 = time.time()
-        data, centers = _device_slice(n, d, 0, n, dev)
-        g = torch.Generator(device=dev)
-        g.manual_seed(4243)
-        mask = torch.rand(n, generator=g, device=dev) < cfg["sel"]
-        self.bits = pack_bits_torch(mask)
+        data, centers = (_device_slice_bf16 if self.bf16 else _device_slice)(n, d, 0, n, dev)
+        if cfg["sel"] is not None:
+            g = torch.Generator(device=dev)
+            g.manual_seed(4243)
+            mask = torch.rand(n, generator=g, device=dev) < cfg["sel"]
+            self.bits = pack_bits_torch(mask)
+        else:
+            mask, self.bits = None, None
         self.queries = synth.device_queries(centers, self.nq, seed=7)
         torch.cuda.synchronize()
-        log(f"[rank {rank}] generated {n} x {d} in {time.time() - t0:.1f}s")
+        torch.cuda.empty_cache()
+        log(f"[rank {rank}] generated {n} x {d} ({'bf16' if self.bf16 else 'f32'}) in {time.time() - t0:.1f}s")
         t0 = time.time()
         col = vs.EmbeddingColumn.from_device(data)
         self.index = vs.IvfIndex.build(col, cfg["nlist"], seed=0, max_iters=cfg.get("iters", 20))
@@ -455,17 +486,21 @@ class IvfWorkload:
             owner = lpt_assign(sizes, world)
             self.owned = (owner == rank).astype(np.uint8)
         # host copies for the roofline bytes and the CPU reference sample
-        self.mask_host = mask.cpu().numpy()
-        self.ids_host = np.concatenate(self.index.partitions)
-        self.sel_per_list = np.add.reduceat(self.mask_host[self.ids_host].astype(np.int64),
-                                            np.r_[0, np.cumsum(sizes)[:-1]]) if n else sizes * 0
-        self.sel_per_list[sizes == 0] = 0
+        if mask is not None:
+            self.mask_host = mask.cpu().numpy()
+            ids_host = np.concatenate(self.index.partitions)
+            self.sel_per_list = np.add.reduceat(self.mask_host[ids_host].astype(np.int64),
+                                                np.r_[0, np.cumsum(sizes)[:-1]]) if n else sizes * 0
+            self.sel_per_list[sizes == 0] = 0
+        else:
+            self.mask_host = None
+            self.sel_per_list = sizes
         # CPU sample: the first queries' probed lists, gathered before the
         # base collection is released (the owning index keeps its own payload)
-        self.cpu_q = self.queries[:16].cpu().numpy()
+        self.cpu_q = self.queries[:cfg.get("cpu_queries", 16)].cpu().numpy()
         _, _, _, probes, _ = self.index.search_raw(self.cpu_q, self.k, self.nprobe, row_filter=self.bits,
                                                    list_owned=self.owned)
-        self.cpu_lists = {int(c): data[torch.from_numpy(self.index.partitions[int(c)]).to(dev)].cpu().numpy()
+        self.cpu_lists = {int(c): data[torch.from_numpy(self.index.partitions[int(c)]).to(dev)].float().cpu().numpy()
                           for c in np.unique(probes)}
         self.cpu_probes = probes
         del col, data
@@ -475,9 +510,9 @@ class IvfWorkload:
                         torch.empty((nq, k), dtype=torch.float64, device=dev),
                         torch.empty((nq,), dtype=torch.int32, device=dev))
         self.q_host = self.queries.cpu().pin_memory()
-        self.bits_host = self.bits.cpu().pin_memory()
+        self.bits_host = self.bits.cpu().pin_memory() if self.bits is not None else None
         self.out_host = tuple(_pinned_like(t) for t in self.out_dev)
-        self.n_sel_total = int(mask.sum())
+        self.n_sel_total = int(mask.sum()) if mask is not None else n
 
     def _search(self, q, bits, out, want_probes=False):
         return self.index.search_raw(q, self.k, self.nprobe, row_filter=bits, out=out,
@@ -506,7 +541,7 @@ class IvfWorkload:
         assert bool(((dd[:, 1:] >= dd[:, :-1]) | dd[:, 1:].isnan()).all()), "distances not sorted"
 
     def io_bytes(self):
-        h2d = self.q_host.numel() * 4 + self.bits_host.numel() * 4
+        h2d = self.q_host.numel() * 4 + (self.bits_host.numel() * 4 if self.bits_host is not None else 0)
         d2h = sum(t.numel() * t.element_size() for t in self.out_host)
         return h2d, d2h
 
@@ -526,9 +561,8 @@ class IvfWorkload:
             uniq = uniq[self.owned[uniq] == 1]
         s = 4 if self.index_dtype == "f32" else 2
         self.unique_lists = int(uniq.size)
-        return float(np.sum(self.list_sizes[uniq] / 8.0 + self.sel_per_list[uniq] * self.d * s))
-
-    index_dtype = "f32"
+        bitmap = self.list_sizes[uniq] / 8.0 if self.bits is not None else 0.0
+        return float(np.sum(bitmap + self.sel_per_list[uniq] * self.d * s))
 
     def roofline(self, kt, steps, ctx, N):
         peaks = measured_peaks()
@@ -550,6 +584,9 @@ class IvfWorkload:
                 "nlist": c["nlist"], "nprobe": self.nprobe, "selectivity": c["sel"],
                 "n_selected": self.n_sel_total, "unique_probed_lists": getattr(self, "unique_lists", None),
                 "build_s": round(self.build_s, 2),
+                "list_rows": {"mean": round(float(np.mean(self.list_sizes)), 1),
+                              "p99": int(np.percentile(self.list_sizes, 99)),
+                              "max": int(np.max(self.list_sizes))},
                 "parallelism": f"list-shard (LPT) x{self.world} + allgather/merge" if self.world > 1
                 else "single GPU",
                 "l2_flush": "inputs larger than L2 (41 GB payload vs 126 MB L2)"}
@@ -572,7 +609,7 @@ class IvfWorkload:
                 self._search(q, self.bits, out)
             torch.cuda.synchronize()
             lat[f"Q={qn}"] = round((time.perf_counter() - t0) / reps * 1e3, 3)
-        return {"batch_latency_ms": lat}
+        return {"batch_latency_ms": lat, "overflow_requeries_total": int(ctx.stats()[N.STAT_OVERFLOW_QUERIES])}
 
     def cpu_baseline(self, args):
         """The reference IVF search path (oracle port of vecindex.py:230-258,
@@ -603,6 +640,26 @@ class IvfWorkload:
                           f"query-0 bit-exact vs ours: {parity}"}
 
 
+class IvfBf16Workload(IvfWorkload):
+    """Config 4: IVF-Flat over 50M x 768 bf16 embeddings (76.8 GB), built on
+    the GPU over the whole collection with the reference's k-means semantics
+    (the payload copy is the list-contiguous layout; the generated column is
+    released after the build), searched with the list-major tcgen05 scan."""
+
+    def roofline(self, kt, steps, ctx, N):
+        r = super().roofline(kt, steps, ctx, N)
+        r["kernel"] = "ivf_scan (tcgen05 list-major, bf16 payload)"
+        return r
+
+    def config(self):
+        c = super().config()
+        c.update(selectivity=None, l2_flush="inputs larger than L2 (76.8 GB payload vs 126 MB L2)")
+        return c
+
+    def dtype(self):
+        return "bf16 storage; bf16 tcgen05 list scan (fp32 accumulate); f64 exact re-rank"
+
+
 def _traffic(key):
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
@@ -624,7 +681,8 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     H = Harness(world, dev)
-    wl = (IvfWorkload if "nlist" in cfg else ExactWorkload)(args, cfg, rank, world, dev)
+    wl = (IvfBf16Workload if cfg.get("bf16") else IvfWorkload if "nlist" in cfg else ExactWorkload)(
+        args, cfg, rank, world, dev)
     ctx = N.Context.get(local)
 
     log(f"[rank {rank}] warmup {args.warmup}")

@@ -161,6 +161,15 @@ int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
  * final reassignment; lists hold ascending row ids (owning layout). */
 int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows,
                  uint64_t seed, int32_t metric, int32_t max_iters, vs_ivf** out);
+/* Borrow a caller-owned DEVICE list-contiguous payload (must outlive the
+ * index): avoids a second copy of collections that fill most of HBM. */
+int vs_ivf_wrap(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
+                const int64_t* list_sizes, const int64_t* list_ids, void* payload_dev,
+                int32_t dtype, int32_t metric, vs_ivf** out);
+/* Nearest list of every row of a column (squared L2 to the centroids, the
+ * build's assignment step; reference vecindex.py:303-304): for indexes
+ * trained on a sample. out_lists: int32 [n], host or device. */
+int vs_ivf_assign(vs_ctx* ctx, const vs_ivf* ivf, const vs_column* data, int32_t* out_lists);
 int vs_ivf_info(const vs_ivf* ivf, int32_t* nlist, int32_t* d, int64_t* n_total,
                 int32_t* metric, int32_t* dtype);
 /* host copies of the structure (any pointer may be NULL) */

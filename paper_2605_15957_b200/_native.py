@@ -53,6 +53,8 @@ SIGNATURES = {
                                 _vp, _vp, _vp]),
     "vs_ivf_create": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp,
                                 C.POINTER(_vp)]),
+    "vs_ivf_wrap": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, C.POINTER(_vp)]),
+    "vs_ivf_assign": (C.c_int, [_vp, _vp, _vp, _vp]),
     "vs_ivf_build": (C.c_int, [_vp, _vp, _i32, _vp, C.c_uint64, _i32, _i32, C.POINTER(_vp)]),
     "vs_ivf_info": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "vs_ivf_export": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),

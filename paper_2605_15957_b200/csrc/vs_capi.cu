@@ -589,7 +589,7 @@ int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in, const i
 // rows are gathered from `base` into the list-contiguous layout.
 int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, const std::vector<int64_t>& sizes,
              const int64_t* list_ids, const void* list_payload, int32_t dtype, int32_t metric,
-             const vs_column* base, const uint8_t* list_owned, vs_ivf** out) {
+             const vs_column* base, const uint8_t* list_owned, vs_ivf** out, bool borrow_payload) {
     std::vector<int64_t> off(nlist + 1, 0);
     for (int i = 0; i < nlist; ++i) {
         if (sizes[i] < 0) return set_err(VS_ERR_PARAMETER, "negative list size");
@@ -617,7 +617,12 @@ int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, cons
     if ((e = cudaMalloc(&v->cmax, sizeof(unsigned))) != cudaSuccess) return fail(e, "alloc");
     if ((e = cudaMalloc(&v->list_off, (size_t)(nlist + 1) * sizeof(int64_t))) != cudaSuccess) return fail(e, "alloc");
     if ((e = cudaMalloc(&v->list_ids, std::max<size_t>(n_total, 1) * sizeof(int64_t))) != cudaSuccess) return fail(e, "alloc");
-    if ((e = cudaMalloc(&v->payload, std::max<size_t>((size_t)n_total * d * es, 16))) != cudaSuccess) return fail(e, "alloc");
+    if (borrow_payload) {
+        v->payload = const_cast<void*>(list_payload);
+        v->payload_borrowed = true;
+    } else if ((e = cudaMalloc(&v->payload, std::max<size_t>((size_t)n_total * d * es, 16))) != cudaSuccess) {
+        return fail(e, "alloc");
+    }
     if ((e = cudaMalloc(&v->pnorms, std::max<size_t>(n_total, 1) * sizeof(float))) != cudaSuccess) return fail(e, "alloc");
     if ((e = cudaMalloc(&v->pmax, sizeof(unsigned))) != cudaSuccess) return fail(e, "alloc");
     cudaStream_t s = ctx->stream;
@@ -625,7 +630,9 @@ int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, cons
     if ((e = cudaMemcpyAsync(v->list_off, off.data(), (nlist + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s)) != cudaSuccess) return fail(e, "upload");
     if (n_total > 0) {
         if ((e = cudaMemcpyAsync(v->list_ids, list_ids, n_total * sizeof(int64_t), cudaMemcpyDefault, s)) != cudaSuccess) return fail(e, "upload");
-        if (list_payload) {
+        if (borrow_payload) {
+            // borrowed in place
+        } else if (list_payload) {
             if ((e = cudaMemcpyAsync(v->payload, list_payload, (size_t)n_total * d * es, cudaMemcpyDefault, s)) != cudaSuccess) return fail(e, "upload");
         } else {
             if (dtype == VS_DTYPE_F32)
@@ -674,6 +681,26 @@ int vs_ivf_create(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d,
     std::vector<int64_t> sizes(nlist);
     CK(cudaMemcpy(sizes.data(), list_sizes, nlist * sizeof(int64_t), cudaMemcpyDefault));
     return ivf_make(ctx, centroids, nlist, d, sizes, list_ids, list_payload, dtype, metric, base, list_owned, out);
+}
+
+int vs_ivf_wrap(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, const int64_t* list_sizes,
+                const int64_t* list_ids, void* payload_dev, int32_t dtype, int32_t metric, vs_ivf** out) {
+    if (!ctx || !out || !centroids || !list_sizes) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_metric(metric));
+    if (nlist < 1) return set_err(VS_ERR_PARAMETER, "nlist must be >= 1");
+    if (d < 1) return set_err(VS_ERR_SHAPE, "embedding dimension must be >= 1");
+    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
+    cudaPointerAttributes at{};
+    if (!payload_dev || cudaPointerGetAttributes(&at, payload_dev) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        return set_err(VS_ERR_PARAMETER, "vs_ivf_wrap needs a device payload pointer");
+    }
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<int64_t> sizes(nlist);
+    CK(cudaMemcpy(sizes.data(), list_sizes, nlist * sizeof(int64_t), cudaMemcpyDefault));
+    return ivf_make(ctx, centroids, nlist, d, sizes, list_ids, payload_dev, dtype, metric, nullptr, nullptr, out,
+                    true);
 }
 
 int vs_ivf_info(const vs_ivf* ivf, int32_t* nlist, int32_t* d, int64_t* n_total, int32_t* metric,
@@ -730,7 +757,7 @@ int vs_ivf_free(vs_ivf* v) {
     cudaFree(v->cmax);
     cudaFree(v->list_off);
     cudaFree(v->list_ids);
-    cudaFree(v->payload);
+    if (!v->payload_borrowed) cudaFree(v->payload);
     cudaFree(v->pnorms);
     cudaFree(v->pmax);
     if (v->owned) cudaFree(v->owned);
@@ -757,122 +784,203 @@ struct IvfJob {
     unsigned long long* visited;  // nullable (retries do not count)
 };
 
-int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift) {
+// group the batch's (query, probe) pairs by list and cut them into units of
+// <= unit_pairs pairs of one list (list-major scans)
+struct IvfGroups {
+    int32_t* pair_codes = nullptr;
+    int4* units = nullptr;
+    int32_t* uoff = nullptr;
+    int64_t max_units = 0;
+    int64_t npairs = 0;
+};
+int ivf_group(vs_ctx* ctx, const IvfJob& job, int unit_pairs, IvfGroups* out) {
+    const vs_ivf* v = job.ivf;
+    const int64_t npairs = job.nq * (int64_t)job.nprobe;
+    vs::IvfGroupArgs g;
+    g.probes = job.probes;
+    g.nq = job.nq;
+    g.nprobe = job.nprobe;
+    g.nlist = v->nlist;
+    g.owned = v->owned;
+    g.unit_pairs = unit_pairs;
+    CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_in));
+    CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_out));
+    CKS(arena_alloc(ctx, (size_t)npairs, &g.vals_in));
+    CKS(arena_alloc(ctx, (size_t)npairs, &g.pair_codes));
+    CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.cnt));
+    CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.qoff));
+    CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.ucnt));
+    CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.uoff));
+    const int64_t max_units = vs::ivf_max_units(job.nq, job.nprobe, v->nlist, unit_pairs);
+    CKS(arena_alloc(ctx, (size_t)max_units, &g.units));
+    g.tmp_bytes = vs::ivf_group_temp_bytes(npairs, v->nlist);
+    char* gtmp = nullptr;
+    CKS(arena_alloc(ctx, g.tmp_bytes, &gtmp));
+    g.tmp = gtmp;
+    {
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_ivf_group(g, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 6;
+    out->pair_codes = g.pair_codes;
+    out->units = g.units;
+    out->uoff = g.uoff;
+    out->max_units = max_units;
+    out->npairs = npairs;
+    return VS_OK;
+}
+
+enum IvfKernel { IVF_QMAJOR = 1, IVF_LMAJOR = 2, IVF_TC = 3 };
+
+int choose_ivf_kernel(const vs_ctx* ctx, const vs_ivf* v, const IvfJob& job) {
+    const bool tc_ok = v->dtype == VS_DTYPE_BF16 && v->d % 8 == 0 && vs::tc_supported(v->d, v->dtype, v->metric);
+    const bool lm_ok = v->d % 4 == 0 && v->d <= vs::kIvfLmDMax;
+    switch (ctx->opt_ivf_kernel) {
+        case IVF_QMAJOR: return IVF_QMAJOR;
+        case IVF_LMAJOR: return lm_ok ? IVF_LMAJOR : IVF_QMAJOR;
+        case IVF_TC: return tc_ok ? IVF_TC : (lm_ok ? IVF_LMAJOR : IVF_QMAJOR);
+        default: break;
+    }
+    // auto: dense bf16 lists are a GEMM (tensor cores); filtered lists are a
+    // sparse gather (SIMT list-major)
+    if (tc_ok && !job.pbits) return IVF_TC;
+    return lm_ok ? IVF_LMAJOR : IVF_QMAJOR;
+}
+
+int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift, bool allow_force) {
     if (job.nq == 0) return VS_OK;
     const vs_ivf* v = job.ivf;
     // the largest number of rows one buffer can see bounds the buffer need
     int64_t max_list = 0;
     for (int i = 0; i < v->nlist; ++i) max_list = std::max(max_list, v->h_off[i + 1] - v->h_off[i]);
-    const int dp = (v->d + 127) / 128 * 128;
-    const bool lmajor = ctx->opt_ivf_kernel != 1 && (v->d % 4) == 0 && v->d <= vs::kIvfLmDMax;
-    int n_sub, n_psplit = 1;
-    int64_t bound;
-    if (lmajor) {
-        // one buffer per (query, probe rank): each sees one list
-        n_sub = job.nprobe;
-        bound = pow2ceil(max_list + 64);
-    } else {
-        const int64_t target = (int64_t)ctx->sm_count * 8;
-        n_psplit = (int)std::min<int64_t>(job.nprobe, std::max<int64_t>(1, (target + job.nq - 1) / job.nq));
-        n_sub = n_psplit * 8;
-        const int64_t per = (job.nprobe + n_psplit - 1) / n_psplit;
-        bound = pow2ceil(per * max_list + 64);
-    }
-    int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
-    const bool exhaustive = C >= bound;
-    if (exhaustive) C = bound;
-    vs::CandBuf cb;
-    cb.n_sub = n_sub;
-    cb.C = (int)C;
-    const size_t slots = (size_t)job.nq * n_sub * C;
-    CKS(arena_alloc(ctx, slots, &cb.key));
-    CKS(arena_alloc(ctx, slots, &cb.pos));
-    CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
-    CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
-    CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
+    const int kern = choose_ivf_kernel(ctx, v, job);
     unsigned long long* vis = job.visited;
     if (!vis) {
         CKS(arena_alloc(ctx, 1, &vis));
         CK(cudaMemsetAsync(vis, 0, sizeof(unsigned long long), ctx->stream));
     }
-    if (lmajor) {
-        // group the batch's (query, probe) pairs by list, cut into units
-        const int64_t npairs = job.nq * (int64_t)job.nprobe;
-        vs::IvfGroupArgs g;
-        g.probes = job.probes;
-        g.nq = job.nq;
-        g.nprobe = job.nprobe;
-        g.nlist = v->nlist;
-        g.owned = v->owned;
-        CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_in));
-        CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_out));
-        CKS(arena_alloc(ctx, (size_t)npairs, &g.vals_in));
-        CKS(arena_alloc(ctx, (size_t)npairs, &g.pair_codes));
-        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.cnt));
-        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.qoff));
-        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.ucnt));
-        CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.uoff));
-        const int64_t max_units = vs::ivf_max_units(job.nq, job.nprobe, v->nlist);
-        CKS(arena_alloc(ctx, (size_t)max_units, &g.units));
-        g.tmp_bytes = vs::ivf_group_temp_bytes(npairs, v->nlist);
-        char* gtmp = nullptr;
-        CKS(arena_alloc(ctx, g.tmp_bytes, &gtmp));
-        g.tmp = gtmp;
-        int* work = nullptr;
-        CKS(arena_alloc(ctx, 1, &work));
-        CK(cudaMemsetAsync(work, 0, sizeof(int), ctx->stream));
-        CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
-        {
-            KTimer kt(ctx, VS_K_SELECT);
-            CK(vs::launch_ivf_group(g, ctx->stream));
+    vs::CandBuf cb;
+    bool exhaustive = false;
+    const unsigned* tau_g = nullptr;
+    int verify = 0;
+    if (kern == IVF_TC) {
+        IvfGroups gr;
+        CKS(ivf_group(ctx, job, 128, &gr));
+        vs::TcIvfArgs a;
+        a.Q = job.q;
+        a.nq = job.nq;
+        a.d = v->d;
+        a.payload = static_cast<const __nv_bfloat16*>(v->payload);
+        a.n_total = v->n_total;
+        a.pnorms = v->pnorms;
+        a.pmax = v->pmax;
+        a.list_off = v->list_off;
+        a.max_list = max_list;
+        a.pair_codes = gr.pair_codes;
+        a.npairs = gr.npairs;
+        a.units = gr.units;
+        a.n_units = gr.uoff + v->nlist;
+        a.max_units = gr.max_units;
+        a.nprobe = job.nprobe;
+        a.pbits = job.pbits;
+        a.k = job.k;
+        a.ip = v->metric;
+        a.cshift = cshift;
+        a.timer_class = VS_K_IVF_SCAN;
+        vs::TcIvfOut o;
+        CKS(vs::tc_ivf_scan(ctx, a, &o));
+        cb = o.cb;
+        exhaustive = o.exhaustive;
+        margin = o.margin;
+        tau_g = o.tau_g;
+        verify = o.verify;
+        if (job.visited) {
+            int32_t* sel = nullptr;
+            CKS(arena_alloc(ctx, (size_t)v->nlist, &sel));
+            CK(vs::launch_visited_count(job.probes, job.nq, job.nprobe, v->list_off, v->nlist, v->owned, job.pbits,
+                                        sel, vis, ctx->stream));
+            ctx->stats[VS_STAT_LAUNCHES] += 2;
         }
-        ctx->stats[VS_STAT_LAUNCHES] += 6;
-        vs::IvfLmParams lp;
-        lp.Q = job.q;
-        lp.nq = job.nq;
-        lp.d = v->d;
-        lp.dp = dp;
-        lp.payload = v->payload;
-        lp.list_off = v->list_off;
-        lp.nprobe = job.nprobe;
-        lp.pbits = job.pbits;
-        lp.pair_codes = g.pair_codes;
-        lp.units = g.units;
-        lp.n_units = g.uoff + v->nlist;
-        lp.max_units = max_units;
-        lp.work = work;
-        lp.margin = margin;
-        lp.ip = v->metric;
-        lp.k = job.k;
-        lp.cb = cb;
-        lp.visited = vis;
-        {
+    } else {
+        const bool lmajor = kern == IVF_LMAJOR;
+        int n_sub, n_psplit = 1;
+        int64_t bound;
+        if (lmajor) {
+            // one buffer per (query, probe rank): each sees one list
+            n_sub = job.nprobe;
+            bound = pow2ceil(max_list + 64);
+        } else {
+            const int64_t target = (int64_t)ctx->sm_count * 8;
+            n_psplit = (int)std::min<int64_t>(job.nprobe, std::max<int64_t>(1, (target + job.nq - 1) / job.nq));
+            n_sub = n_psplit * 8;
+            const int64_t per = (job.nprobe + n_psplit - 1) / n_psplit;
+            bound = pow2ceil(per * max_list + 64);
+        }
+        int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
+        exhaustive = C >= bound;
+        if (exhaustive) C = bound;
+        cb.n_sub = n_sub;
+        cb.C = (int)C;
+        const size_t slots = (size_t)job.nq * n_sub * C;
+        CKS(arena_alloc(ctx, slots, &cb.key));
+        CKS(arena_alloc(ctx, slots, &cb.pos));
+        CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
+        CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
+        CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
+        if (lmajor) {
+            IvfGroups gr;
+            CKS(ivf_group(ctx, job, vs::kIvfLmQT, &gr));
+            int* work = nullptr;
+            CKS(arena_alloc(ctx, 1, &work));
+            CK(cudaMemsetAsync(work, 0, sizeof(int), ctx->stream));
+            CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
+            vs::IvfLmParams lp;
+            lp.Q = job.q;
+            lp.nq = job.nq;
+            lp.d = v->d;
+            lp.dp = (v->d + 127) / 128 * 128;
+            lp.payload = v->payload;
+            lp.list_off = v->list_off;
+            lp.nprobe = job.nprobe;
+            lp.pbits = job.pbits;
+            lp.pair_codes = gr.pair_codes;
+            lp.units = gr.units;
+            lp.n_units = gr.uoff + v->nlist;
+            lp.max_units = gr.max_units;
+            lp.work = work;
+            lp.margin = margin;
+            lp.ip = v->metric;
+            lp.k = job.k;
+            lp.cb = cb;
+            lp.visited = vis;
             KTimer kt(ctx, VS_K_IVF_SCAN);
             if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_lmajor<float>(lp, ctx->sm_count, ctx->stream));
             else CK(vs::launch_ivf_scan_lmajor<__nv_bfloat16>(lp, ctx->sm_count, ctx->stream));
+        } else {
+            vs::IvfScanParams sp;
+            sp.Q = job.q;
+            sp.nq = job.nq;
+            sp.d = v->d;
+            sp.payload = v->payload;
+            sp.list_off = v->list_off;
+            sp.probes = job.probes;
+            sp.nprobe = job.nprobe;
+            sp.list_owned = v->owned;
+            sp.pbits = job.pbits;
+            sp.margin = margin;
+            sp.ip = v->metric;
+            sp.k = job.k;
+            sp.n_psplit = n_psplit;
+            sp.cb = cb;
+            sp.visited = vis;
+            KTimer kt(ctx, VS_K_IVF_SCAN);
+            if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_qmajor<float>(sp, ctx->stream));
+            else CK(vs::launch_ivf_scan_qmajor<__nv_bfloat16>(sp, ctx->stream));
         }
-    } else {
-        vs::IvfScanParams sp;
-        sp.Q = job.q;
-        sp.nq = job.nq;
-        sp.d = v->d;
-        sp.payload = v->payload;
-        sp.list_off = v->list_off;
-        sp.probes = job.probes;
-        sp.nprobe = job.nprobe;
-        sp.list_owned = v->owned;
-        sp.pbits = job.pbits;
-        sp.margin = margin;
-        sp.ip = v->metric;
-        sp.k = job.k;
-        sp.n_psplit = n_psplit;
-        sp.cb = cb;
-        sp.visited = vis;
-        KTimer kt(ctx, VS_K_IVF_SCAN);
-        if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_qmajor<float>(sp, ctx->stream));
-        else CK(vs::launch_ivf_scan_qmajor<__nv_bfloat16>(sp, ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
     }
-    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    const int n_sub = cb.n_sub;
+    const int64_t C = cb.C;
 
     vs::RerankParams rp;
     rp.Q = job.q;
@@ -882,8 +990,8 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     rp.k = job.k;
     rp.cb = cb;
     rp.margin = margin;
-    rp.tau_g = nullptr;
-    rp.verify = 0;
+    rp.tau_g = tau_g;
+    rp.verify = verify;
     rp.rows = v->payload;
     rp.row_map = nullptr;
     rp.id_map = v->list_ids;
@@ -913,10 +1021,10 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         CK(cudaMemcpyAsync(h.data(), cb.overflow, job.nq * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         for (int64_t i = 0; i < job.nq; ++i)
-            if (h[i] || (cshift == 0 && ctx->opt_force_retry)) which.push_back((int32_t)i);
+            if (h[i] || (allow_force && ctx->opt_force_retry)) which.push_back((int32_t)i);
     }
     if (which.empty()) return VS_OK;
-    if (exhaustive && !(cshift == 0 && ctx->opt_force_retry))
+    if (exhaustive && !(allow_force && ctx->opt_force_retry))
         return set_err(VS_ERR_INTERNAL, "IVF candidate overflow with exhaustive buffers");
     ctx->stats[VS_STAT_OVERFLOW_QUERIES] += (int64_t)which.size();
     const int64_t m = (int64_t)which.size();
@@ -943,7 +1051,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     CKS(arena_alloc(ctx, (size_t)m * job.k, &sub.out_ids));
     CKS(arena_alloc(ctx, (size_t)m * job.k, &sub.out_dist));
     CKS(arena_alloc(ctx, (size_t)m, &sub.out_count));
-    CKS(run_ivf_scan(ctx, sub, d_m, exhaustive ? cshift : cshift + 2));
+    CKS(run_ivf_scan(ctx, sub, d_m, exhaustive ? cshift : cshift + 2, false));
     CKS(scatter_rows(ctx, sub.out_ids, d_idx, m, job.k, job.out_ids));
     CKS(scatter_rows(ctx, sub.out_dist, d_idx, m, job.k, job.out_dist));
     CKS(scatter_rows(ctx, sub.out_count, d_idx, m, 1, job.out_count));
@@ -1031,12 +1139,22 @@ extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* querie
     if (!job.out_ids) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_ids));
     if (!job.out_dist) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_dist));
     if (!job.out_count) CKS(arena_alloc(ctx, (size_t)nq, &job.out_count));
-    CKS(run_ivf_scan(ctx, job, sm, 0));
+    CKS(run_ivf_scan(ctx, job, sm, 0, true));
     unsigned long long h_vis = 0;
     CK(cudaMemcpyAsync(&h_vis, vis, sizeof(h_vis), cudaMemcpyDeviceToHost, ctx->stream));
     CKS(flush_out(ctx, pending));
     if (out_visited) *out_visited = (int64_t)h_vis;
     return VS_OK;
+}
+
+extern "C" int vs_ivf_assign(vs_ctx* ctx, const vs_ivf* ivf, const vs_column* data, int32_t* out_lists) {
+    if (!ctx || !ivf || !data || !out_lists) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (data->d != ivf->d) return set_err(VS_ERR_SHAPE, "column dim %d != index dim %d", data->d, ivf->d);
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    if (data->n == 0) return VS_OK;
+    CKS(ensure_norms(const_cast<vs_column*>(data)));
+    return vs::ivf_assign_gpu(ctx, ivf, data, out_lists);
 }
 
 extern "C" int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows,

@@ -163,6 +163,7 @@ struct vs_ivf {
     float* pnorms = nullptr;
     unsigned* pmax = nullptr;
     uint8_t* owned = nullptr;        // device [nlist] or null
+    bool payload_borrowed = false;   // vs_ivf_wrap: caller-owned device payload
 };
 
 
@@ -243,4 +244,4 @@ inline void resolve_timers(vs_ctx* ctx) {
 
 int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, const std::vector<int64_t>& sizes,
              const int64_t* list_ids, const void* list_payload, int32_t dtype, int32_t metric,
-             const vs_column* base, const uint8_t* list_owned, vs_ivf** out);
+             const vs_column* base, const uint8_t* list_owned, vs_ivf** out, bool borrow_payload = false);

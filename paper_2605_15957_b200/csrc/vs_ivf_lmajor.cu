@@ -310,9 +310,9 @@ __global__ void k_pair_keys(const int32_t* __restrict__ probes, int64_t npairs, 
     }
 }
 
-__global__ void k_unit_counts(const int32_t* __restrict__ cnt, int nlist, int32_t* __restrict__ ucnt) {
+__global__ void k_unit_counts(const int32_t* __restrict__ cnt, int nlist, int qt, int32_t* __restrict__ ucnt) {
     for (int l = blockIdx.x * blockDim.x + threadIdx.x; l <= nlist; l += gridDim.x * blockDim.x)
-        ucnt[l] = l < nlist ? (cnt[l] + QT - 1) / QT : 0;
+        ucnt[l] = l < nlist ? (cnt[l] + qt - 1) / qt : 0;
 }
 
 // units of one list split its pairs evenly (sizes differ by at most one)
@@ -330,6 +330,53 @@ __global__ void k_write_units(const int32_t* __restrict__ cnt, const int32_t* __
     }
 }
 }  // namespace
+
+// visited rows (vecindex.py:253, filtered: the rows left after the filter):
+// selected rows per list (warp per list), then a sum over the owned pairs
+__global__ void k_list_selected(const int64_t* __restrict__ list_off, int nlist, const uint32_t* __restrict__ pbits,
+                                int32_t* __restrict__ sel) {
+    const int lane = threadIdx.x & 31;
+    for (int l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < nlist; l += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = list_off[l], b = list_off[l + 1];
+        int c = 0;
+        if (!pbits) {
+            c = (int)(b - a);
+        } else {
+            for (int64_t r = a + lane * 32; r < b; r += 32 * 32) {
+                const int sh = (int)(r & 31);
+                const uint32_t lo = pbits[r >> 5];
+                const uint32_t hi = sh ? pbits[(r >> 5) + 1] : 0u;
+                uint32_t bits = __funnelshift_r(lo, hi, sh);
+                const int64_t nb = b - r;
+                if (nb < 32) bits &= (1u << nb) - 1u;
+                c += __popc(bits);
+            }
+            c = __reduce_add_sync(VS_FULL, c);
+        }
+        if (lane == 0) sel[l] = c;
+    }
+}
+__global__ void k_visited_pairs(const int32_t* __restrict__ probes, int64_t npairs, const uint8_t* __restrict__ owned,
+                                const int32_t* __restrict__ sel, unsigned long long* __restrict__ visited) {
+    unsigned long long v = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs; i += (int64_t)gridDim.x * blockDim.x) {
+        const int l = probes[i];
+        if (!owned || owned[l]) v += (unsigned long long)sel[l];
+    }
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(VS_FULL, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(visited, v);
+}
+
+cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe, const int64_t* list_off, int nlist,
+                                 const uint8_t* list_owned, const uint32_t* pbits, int32_t* sel_scratch,
+                                 unsigned long long* visited, cudaStream_t s) {
+    const int lb = std::max(1, std::min((nlist * 32 + 255) / 256, 4096));
+    k_list_selected<<<lb, 256, 0, s>>>(list_off, nlist, pbits, sel_scratch);
+    const int64_t np = nq * (int64_t)nprobe;
+    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((np + 255) / 256, 2048));
+    k_visited_pairs<<<pb, 256, 0, s>>>(probes, np, list_owned, sel_scratch, visited);
+    return cudaGetLastError();
+}
 
 size_t ivf_group_temp_bytes(int64_t npairs, int nlist) {
     size_t a = 0, b = 0;
@@ -356,7 +403,7 @@ cudaError_t launch_ivf_group(const IvfGroupArgs& g, cudaStream_t s) {
     tb = g.tmp_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(g.tmp, tb, g.cnt, g.qoff, g.nlist + 1, s)) != cudaSuccess) return e;
     const int lb = std::max(1, std::min((g.nlist + 256) / 256, 1024));
-    k_unit_counts<<<lb, 256, 0, s>>>(g.cnt, g.nlist, g.ucnt);
+    k_unit_counts<<<lb, 256, 0, s>>>(g.cnt, g.nlist, g.unit_pairs, g.ucnt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     tb = g.tmp_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(g.tmp, tb, g.ucnt, g.uoff, g.nlist + 1, s)) != cudaSuccess) return e;
@@ -364,8 +411,8 @@ cudaError_t launch_ivf_group(const IvfGroupArgs& g, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-int64_t ivf_max_units(int64_t nq, int nprobe, int nlist) {
-    return (nq * (int64_t)nprobe + QT - 1) / QT + nlist;
+int64_t ivf_max_units(int64_t nq, int nprobe, int nlist, int unit_pairs) {
+    return (nq * (int64_t)nprobe + unit_pairs - 1) / unit_pairs + nlist;
 }
 
 size_t ivf_lmajor_smem(int dp, int dtype_bytes) {

@@ -107,9 +107,10 @@ struct IvfGroupArgs {
     int4* units;                // [ivf_max_units] out: (list, first pair, pairs, 0)
     void* tmp;
     size_t tmp_bytes;           // >= ivf_group_temp_bytes
+    int unit_pairs;             // max pairs per unit (kIvfLmQT SIMT, 128 tensor cores)
 };
 size_t ivf_group_temp_bytes(int64_t npairs, int nlist);
-int64_t ivf_max_units(int64_t nq, int nprobe, int nlist);
+int64_t ivf_max_units(int64_t nq, int nprobe, int nlist, int unit_pairs);
 cudaError_t launch_ivf_group(const IvfGroupArgs& g, cudaStream_t s);
 
 struct IvfLmParams {
@@ -206,9 +207,8 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_gather_rows(const T* src, const int64_t* ids, int64_t n, int d, T* dst,
                                cudaStream_t s);
-cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe,
-                                 const int64_t* list_off, const uint8_t* list_owned,
-                                 const uint32_t* pbits, unsigned long long* visited,
-                                 cudaStream_t s);
+cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe, const int64_t* list_off, int nlist,
+                                 const uint8_t* list_owned, const uint32_t* pbits, int32_t* sel_scratch,
+                                 unsigned long long* visited, cudaStream_t s);
 
 }  // namespace vs

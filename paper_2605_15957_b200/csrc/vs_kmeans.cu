@@ -304,4 +304,38 @@ int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64
     return ivf_make(ctx, c32, nlist, d, sizes, ids64, nullptr, data->dtype, metric, data, nullptr, out);
 }
 
+// Nearest list (squared L2 to the float32 centroids, first minimum on the
+// tensor cores' bf16 keys, as the build's assignment step) of every row of a
+// column: the "add rows" step for collections too large to build on directly
+// (train on a sample, then assign). out: int32 [n] (device or host).
+int ivf_assign_gpu(vs_ctx* ctx, const vs_ivf* v, const vs_column* col, int32_t* out) {
+    using namespace vs_internal;
+    cudaStream_t st = ctx->stream;
+    const int64_t n = col->n;
+    const int d = v->d;
+    const int dp = (d + 7) / 8 * 8;
+    const int nlist = v->nlist;
+    __nv_bfloat16* cb = nullptr;
+    __nv_bfloat16* xb = nullptr;
+    unsigned* junk = nullptr;
+    unsigned long long* packed = nullptr;
+    int* assign = nullptr;
+    float* dist = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nlist * dp, &cb));
+    CKS(arena_alloc(ctx, (size_t)tc_argmin_chunk(n) * dp, &xb));
+    CKS(arena_alloc(ctx, 2, &junk));
+    CKS(arena_alloc(ctx, (size_t)n, &packed));
+    CKS(arena_alloc(ctx, (size_t)n, &assign));
+    CKS(arena_alloc(ctx, (size_t)n, &dist));
+    CKS(tc_stage_bf16(ctx, v->centroids, nlist, d, cb, junk));
+    CKS(tc_argmin_rows(ctx, col->data, col->dtype, n, d, cb, v->cnorms, nlist, packed, xb, junk));
+    k_unpack<<<grid_for(n), 256, 0, st>>>(packed, col->norms, n, assign, dist);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, assign, (size_t)n * sizeof(int32_t), cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->stats[VS_STAT_LAUNCHES] += 3;
+    return VS_OK;
+}
+
 }  // namespace vs
+

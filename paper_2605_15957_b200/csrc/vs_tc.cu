@@ -50,6 +50,7 @@ struct Cfg {
     static constexpr int QTILE = PAIR ? 2 * BM : BM;   // queries per work item
 };
 constexpr int MAX_STAGES = 6;
+constexpr int PF_BOXES = 16;            // MODE 2: default L2 prefetch distance in B boxes
 constexpr int NTHREADS = 384;           // 12 warps
 constexpr int EPI_WARP0 = 4;            // warps 4..11 drain TMEM (2 per lane quadrant)
 constexpr int EPI_THREADS = 256;
@@ -86,7 +87,54 @@ struct Params {
     unsigned long long* dbg;  // nullable: [8] stall / work counters (VS_TC_DEBUG=1)
     int topk_mode;            // 1: keep the local top-k only (phase B verifies); 0: keep the margin band
     unsigned long long* argmin_out;  // MODE 1: per query row packed (orderable key << 32 | column)
+    // MODE 2 (IVF list-major): A = bf16 queries staged in pair order (pairs
+    // grouped by list), B = the list-contiguous bf16 payload; a work item is
+    // one unit (list, first pair, pairs <= BM), its B tiles cover the list
+    const int4* units;
+    const int* n_units;             // device scalar
+    const int64_t* list_off;        // [nlist + 1]
+    const int32_t* pair_codes;      // q * nprobe + probe rank, grouped by list
+    int nprobe;
+    const uint32_t* pbits;          // nullable: filter bit per payload position
+    int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
 };
+
+// one work item: A tile rows [a_row, a_row + QTILE), B tiles of BN rows from
+// b_row0 (ntile of them), valid B rows < b_end; MODE 2: npairs valid A rows
+struct Item {
+    int64_t a_row;
+    int64_t b_row0;
+    int64_t ntile;
+    int64_t b_end;
+    int64_t s;          // data split (MODE 0/1)
+    int npairs;
+};
+template <int MODE, int QTILE>
+__device__ __forceinline__ Item decode_item(const Params& p, int64_t it) {
+    Item r;
+    if (MODE == 2) {
+        const int4 un = p.units[it];
+        const int64_t off = p.list_off[un.x];
+        const int64_t n = p.list_off[un.x + 1] - off;
+        r.a_row = un.y;
+        r.b_row0 = off;
+        r.ntile = (n + BN - 1) / BN;
+        r.b_end = off + n;
+        r.s = 0;
+        r.npairs = un.z;
+    } else {
+        const int qt = (int)(it % p.qtiles);
+        r.s = it / p.qtiles;
+        const int64_t t0 = r.s * p.tiles_per_split;
+        const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
+        r.a_row = (int64_t)qt * QTILE;
+        r.b_row0 = t0 * BN;
+        r.ntile = t1 - t0;
+        r.b_end = p.nsel;
+        r.npairs = 0;
+    }
+    return r;
+}
 
 // ---- PTX helpers ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -118,6 +166,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// TMA prefetch of one box into L2 (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"((uint64_t)map), "r"(c0),
+                 "r"(c1)
+                 : "memory");
 }
 // CTA-pair TMA: the bytes land in this CTA's shared memory, the transaction
 // completes on the leader CTA's barrier (peer bit cleared)
@@ -265,8 +319,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (PAIR) cluster_sync_all();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
+    unsigned long long t_start = 0;
+    if (p.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-    const int64_t nitems = (int64_t)p.qtiles * p.nsplit;
+    const int64_t nitems = MODE == 2 ? (int64_t)*p.n_units : (int64_t)p.qtiles * p.nsplit;
     if (warp == 0) {
         // ===== TMA producer =====
         if (lane == 0) {
@@ -274,25 +330,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             uint32_t phase = 0;
             long long w_empty = 0;
             for (int64_t it = unit; it < nitems; it += nunits) {
-                const int qt = (int)(it % p.qtiles);
-                const int64_t s = it / p.qtiles;
-                const int64_t t0 = s * p.tiles_per_split;
-                const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-                for (int64_t t = t0; t < t1; ++t) {
+                const Item item = decode_item<MODE, QTILE>(p, it);
+                // MODE 2: the B operand streams from HBM exactly once, so the
+                // smem ring alone keeps too few bytes in flight; a sliding
+                // window of L2 prefetches runs PF boxes ahead of the loads
+                const int64_t nbox = item.ntile * p.kblocks;
+                if (MODE == 2)
+                    for (int64_t pb = 1; pb < p.pf_boxes && pb < nbox; ++pb)
+                        tma_prefetch_2d(&map_b, (int)(pb % p.kblocks) * BK, (int)(item.b_row0 + (pb / p.kblocks) * BN));
+                for (int64_t t = 0; t < item.ntile; ++t) {
+                    const int brow = (int)(item.b_row0 + t * BN);
                     for (int kb = 0; kb < p.kblocks; ++kb) {
+                        if (MODE == 2) {
+                            const int64_t pb = t * p.kblocks + kb + p.pf_boxes;
+                            if (pb < nbox)
+                                tma_prefetch_2d(&map_b, (int)(pb % p.kblocks) * BK,
+                                                (int)(item.b_row0 + (pb / p.kblocks) * BN));
+                        }
                         const long long c0 = p.dbg ? clock64() : 0;
                         mbar_wait(&S.empty[stage], phase ^ 1);
                         if (p.dbg) w_empty += clock64() - c0;
                         unsigned char* sa = base + (size_t)stage * STAGE_BYTES;
                         if (PAIR) {
                             if (rank == 0) mbar_expect_tx(&S.full[stage], 2 * STAGE_BYTES);
-                            tma_load_2d_pair(sa, &map_a, &S.full[stage], kb * BK, qt * QTILE + (int)rank * BM);
+                            tma_load_2d_pair(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row + (int)rank * BM);
                             tma_load_2d_pair(sa + A_BYTES, &map_b, &S.full[stage], kb * BK,
-                                             (int)(t * BN) + (int)rank * (BN / 2));
+                                             brow + (int)rank * (BN / 2));
                         } else {
                             mbar_expect_tx(&S.full[stage], STAGE_BYTES);
-                            tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, qt * BM);
-                            tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, (int)(t * BN));
+                            tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row);
+                            tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow);
                         }
                         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
                     }
@@ -309,10 +376,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             uint32_t tcount = 0;
             long long w_full = 0, w_tempty = 0;
             for (int64_t it = unit; it < nitems; it += nunits) {
-                const int64_t s = it / p.qtiles;
-                const int64_t t0 = s * p.tiles_per_split;
-                const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-                for (int64_t t = t0; t < t1; ++t, ++tcount) {
+                const Item item = decode_item<MODE, QTILE>(p, it);
+                for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
                     const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
                     long long c0 = p.dbg ? clock64() : 0;
                     mbar_wait(&S.tempty[acc], aph ^ 1);
@@ -358,15 +423,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float* xw = xn_w[warp - EPI_WARP0];
         uint32_t tcount = 0;
         for (int64_t it = unit; it < nitems; it += nunits) {
-            const int qt = (int)(it % p.qtiles);
-            const int64_t s = it / p.qtiles;
-            const int64_t t0 = s * p.tiles_per_split;
-            const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-            const int64_t q = (int64_t)qt * QTILE + (int64_t)rank * BM + row;
+            const Item item = decode_item<MODE, QTILE>(p, it);
+            const int64_t q = item.a_row + (int64_t)rank * BM + row;
             uint32_t best_o = 0xffffffffu, best_i = 0u;
-            for (int64_t t = t0; t < t1; ++t, ++tcount) {
+            for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
                 const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
-                const int64_t r0 = t * BN;
+                const int64_t r0 = item.b_row0 + t * BN;
                 const int ncols = (int)min((int64_t)BN, p.nsel - r0);
                 {
                     const int64_t i = r0 + half * (BN / 2) + lane * 4;
@@ -418,19 +480,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         long long w_tfull = 0, c_comp = 0, n_comp = 0, n_app = 0, c_ldw = 0, c_loop = 0;
         // software-pipelined per-tile inputs: the next tile's row norms (4 per
         // lane = the warp's column half) and the next tile's admission bound
-        auto norms4 = [&](int64_t r0n) -> float4 {
+        auto norms4 = [&](int64_t r0n, int64_t bend) -> float4 {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (IP) return v;
             const int64_t i = r0n + half * (BN / 2) + lane * 4;
-            if (i + 3 < p.nsel) {
+            if (i + 3 < bend && MODE != 2) {
                 v = __ldg(reinterpret_cast<const float4*>(p.xn + i));
             } else {
-                v.x = i + 0 < p.nsel ? __ldg(p.xn + i + 0) : 0.f;
-                v.y = i + 1 < p.nsel ? __ldg(p.xn + i + 1) : 0.f;
-                v.z = i + 2 < p.nsel ? __ldg(p.xn + i + 2) : 0.f;
-                v.w = i + 3 < p.nsel ? __ldg(p.xn + i + 3) : 0.f;
+                v.x = i + 0 < bend ? __ldg(p.xn + i + 0) : 0.f;
+                v.y = i + 1 < bend ? __ldg(p.xn + i + 1) : 0.f;
+                v.z = i + 2 < bend ? __ldg(p.xn + i + 2) : 0.f;
+                v.w = i + 3 < bend ? __ldg(p.xn + i + 3) : 0.f;
             }
             return v;
+        };
+        // the query (and its candidate sub-buffer) served by this thread's row
+        // of work item `item`; false for padding rows
+        auto row_query = [&](const Item& item, int64_t& q, int64_t& sub) -> bool {
+            if (MODE == 2) {
+                if (row >= item.npairs) return false;
+                const int code = __ldg(p.pair_codes + item.a_row + row);
+                q = code / p.nprobe;
+                sub = (int64_t)(code % p.nprobe) * 2 + half;
+                return true;
+            }
+            q = item.a_row + (int64_t)rank * BM + row;
+            sub = item.s * 2 + half;
+            return q < p.nq;
         };
         float* xw = xn_w[warp - EPI_WARP0];
         float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -438,19 +514,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         {
             const int64_t it0 = unit;
             if (it0 < nitems) {
-                pf = norms4((it0 / p.qtiles) * p.tiles_per_split * BN);
-                const int64_t q0 = (int64_t)(it0 % p.qtiles) * QTILE + (int64_t)rank * BM + row;
-                if (q0 < p.nq) pf_tau = __ldcg(p.tau_g + q0);
+                const Item i0 = decode_item<MODE, QTILE>(p, it0);
+                pf = norms4(i0.b_row0, i0.b_end);
+                int64_t q0, s0;
+                if (row_query(i0, q0, s0)) pf_tau = __ldcg(p.tau_g + q0);
             }
         }
         for (int64_t it = unit; it < nitems; it += nunits) {
-            const int qt = (int)(it % p.qtiles);
-            const int64_t s = it / p.qtiles;
-            const int64_t t0 = s * p.tiles_per_split;
-            const int64_t t1 = min(p.ntiles, t0 + p.tiles_per_split);
-            const int64_t q = (int64_t)qt * QTILE + (int64_t)rank * BM + row;
-            const bool qv = q < p.nq;
-            const int64_t sub = s * 2 + half;
+            const Item item = decode_item<MODE, QTILE>(p, it);
+            int64_t q = 0, sub = 0;
+            const bool qv = row_query(item, q, sub);
             const int64_t cbase = qv ? ((q * p.cb.n_sub + sub) * (int64_t)C) : 0;
             float* ckey = p.cb.key + cbase;
             uint32_t* cpos = p.cb.pos + cbase;
@@ -464,23 +537,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int lim0 = 2 * p.k + 64;
             int lim = lim0;
             float tau = __int_as_float(0x7f800000);
-            for (int64_t t = t0; t < t1; ++t, ++tcount) {
+            for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
                 const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
-                const int64_t r0 = t * BN;
-                const int ncols = (int)min((int64_t)BN, p.nsel - r0);
+                const int64_t r0 = item.b_row0 + t * BN;
+                const int ncols = (int)min((int64_t)BN, item.b_end - r0);
                 if (!IP) *reinterpret_cast<float4*>(xw + lane * 4) = pf;
                 __syncwarp();
                 if (qv) tau = fminf(tau, o2f(pf_tau));
                 {   // prefetch for the next tile of this CTA's sequence
-                    int64_t tn = t + 1, itn = it;
-                    if (tn >= t1) {
-                        itn = it + nunits;
-                        tn = (itn / p.qtiles) * p.tiles_per_split;
-                    }
-                    if (itn < nitems) {
-                        pf = norms4(tn * BN);
-                        const int64_t qn = (int64_t)(itn % p.qtiles) * QTILE + (int64_t)rank * BM + row;
-                        pf_tau = (qn < p.nq) ? __ldcg(p.tau_g + qn) : 0xffffffffu;
+                    if (t + 1 < item.ntile) {
+                        pf = norms4(r0 + BN, item.b_end);
+                        pf_tau = qv ? __ldcg(p.tau_g + q) : 0xffffffffu;
+                    } else if (it + nunits < nitems) {
+                        const Item in = decode_item<MODE, QTILE>(p, it + nunits);
+                        pf = norms4(in.b_row0, in.b_end);
+                        int64_t qn, sn;
+                        pf_tau = row_query(in, qn, sn) ? __ldcg(p.tau_g + qn) : 0xffffffffu;
                     }
                 }
                 {   // compaction (warp-cooperative, one buffer at a time)
@@ -536,7 +608,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                     }
                     const int nv = ncols - cb0;
-                    const unsigned valid = nv >= 32 ? VS_FULL : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                    unsigned valid = nv >= 32 ? VS_FULL : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+                    if (MODE == 2 && p.pbits && valid) {   // filter bits of payload positions r0+cb0..+31
+                        const int64_t a = r0 + cb0;
+                        const int sh = (int)(a & 31);
+                        const uint32_t lo = __ldg(p.pbits + (a >> 5));
+                        const uint32_t hi = sh ? __ldg(p.pbits + (a >> 5) + 1) : 0u;
+                        valid &= __funnelshift_r(lo, hi, sh);
+                    }
                     float kk[32];
                     unsigned mask = 0;
 #pragma unroll
@@ -599,7 +678,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             atomicAdd(&p.dbg[4], (unsigned long long)c_comp);
             atomicAdd(&p.dbg[5], (unsigned long long)n_comp);
             atomicAdd(&p.dbg[6], (unsigned long long)n_app);
-            if (et == 0) atomicAdd(&p.dbg[7], (unsigned long long)tcount);
+            if (et == 0) {
+                atomicAdd(&p.dbg[7], (unsigned long long)tcount);
+                atomicMax(&p.dbg[12], (unsigned long long)tcount);
+                unsigned long long t_end;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                atomicMax(&p.dbg[10], t_end - t_start);
+                atomicAdd(&p.dbg[11], t_end - t_start);
+            }
             atomicAdd(&p.dbg[8], (unsigned long long)c_ldw);
             atomicAdd(&p.dbg[9], (unsigned long long)c_loop);
         }
@@ -648,6 +734,20 @@ __global__ void k_stage_queries(const float* __restrict__ q, int64_t nq, int d, 
 }
 // selected rows -> contiguous bf16 [nsel][dp] + their fp32 norms (warp per row);
 // max ||x~|| and max ||dx|| over the rows into xmax2[0..1] (float bits, atomicMax)
+// queries in pair order (IVF list-major A operand): row i = bf16(Q[code_i / nprobe])
+__global__ void k_stage_pair_queries(const float* __restrict__ q, const int32_t* __restrict__ codes, int64_t npairs,
+                                     int nprobe, int d, int dp, __nv_bfloat16* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (; w < npairs; w += nw) {
+        const int64_t qi = codes[w] / nprobe;
+        const float* src = q + qi * (int64_t)d;
+        __nv_bfloat16* dst = out + w * (int64_t)dp;
+        for (int c = lane; c < dp; c += 32) dst[c] = __float2bfloat16_rn(c < d ? src[c] : 0.f);
+    }
+}
+
 template <typename T>
 __global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict__ sel, int64_t nsel, int d,
                              int dp, const float* __restrict__ norms, __nv_bfloat16* __restrict__ out,
@@ -1001,4 +1101,122 @@ int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* 
     return VS_OK;
 }
 
+int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
+    using namespace vs_internal;
+    if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if (a.d % 8) return set_err(VS_ERR_PARAMETER, "tensor-core IVF scan needs d %% 8 == 0");
+    cudaStream_t st = ctx->stream;
+    const int d = a.d, dp = (d + 7) / 8 * 8;
+    // margin mode: a buffer (pair, column half) sees one list, and the nearest
+    // list's buffer usually holds the whole top-k, so the local-top-k +
+    // verification scheme of the exhaustive scan would fail its check there;
+    // keeping the band key <= local k-th + margin is exact by construction
+    const int topk_mode = 0;
+    __nv_bfloat16 *qp = nullptr, *qa = nullptr;
+    float* margin = nullptr;
+    float2* qerr = nullptr;
+    unsigned *tau_g = nullptr, *xmax2 = nullptr;
+    CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(a.npairs, 1) * dp, &qp));
+    CKS(arena_alloc(ctx, (size_t)a.nq * dp, &qa));
+    CKS(arena_alloc(ctx, (size_t)a.nq, &margin));
+    CKS(arena_alloc(ctx, (size_t)a.nq, &qerr));
+    CKS(arena_alloc(ctx, (size_t)a.nq, &tau_g));
+    CKS(arena_alloc(ctx, 2, &xmax2));
+    {
+        KTimer kt(ctx, VS_K_STAGE);
+        tc::k_stage_pair_queries<<<(unsigned)std::min<int64_t>((a.npairs * 32 + 255) / 256, 148 * 32), 256, 0, st>>>(
+            a.Q, a.pair_codes, a.npairs, a.nprobe, d, dp, qp);
+        CK(cudaGetLastError());
+        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((a.nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+            a.Q, a.nq, d, dp, qa, qerr);
+        CK(cudaGetLastError());
+        // bf16-stored rows are their own tensor-core operand: ||x~|| = ||x||, dx = 0
+        CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));
+        CK(cudaMemcpyAsync(xmax2, a.pmax, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+        tc::k_tc_margins<<<(unsigned)((a.nq + 255) / 256), 256, 0, st>>>(qerr, a.nq, d, a.pmax, xmax2, a.ip, margin);
+        CK(cudaGetLastError());
+        CK(cudaMemsetAsync(tau_g, 0xff, a.nq * sizeof(unsigned), st));
+        ctx->stats[VS_STAT_LAUNCHES] += 3;
+    }
+    // room for one half-tile of appends (128) beyond the kept band
+    int64_t C = pow2ceil(2 * a.k + 96 + tc::BN / 2) << (ctx->opt_slack + a.cshift);
+    // one buffer per (pair, column half): a column half sees <= 128 rows per tile
+    const int64_t cap = pow2ceil((a.max_list + tc::BN - 1) / tc::BN * (tc::BN / 2) + 64);
+    out->exhaustive = C >= cap;
+    if (C > cap) C = cap;
+    CandBuf c;
+    c.n_sub = 2 * a.nprobe;
+    c.C = (int)C;
+    const size_t slots = (size_t)a.nq * c.n_sub * C;
+    CKS(arena_alloc(ctx, slots, &c.key));
+    CKS(arena_alloc(ctx, slots, &c.pos));
+    CKS(arena_alloc(ctx, (size_t)a.nq * c.n_sub, &c.cnt));
+    CKS(arena_alloc(ctx, (size_t)a.nq, &c.overflow));
+    CK(cudaMemsetAsync(c.overflow, 0, a.nq * sizeof(int), st));
+    CK(cudaMemsetAsync(c.cnt, 0, (size_t)a.nq * c.n_sub * sizeof(int), st));
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, qp, std::max<int64_t>(a.npairs, 1), d, dp, tc::BM) ||
+        !make_map(&mb, a.payload, a.n_total, d, d, tc::BN))
+        return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    tc::Params pr{};
+    pr.nq = a.nq;
+    pr.d = d;
+    pr.kblocks = (d + tc::BK - 1) / tc::BK;
+    pr.nsel = a.n_total;
+    pr.qtiles = 1;
+    pr.nsplit = 1;
+    pr.tiles_per_split = 1;
+    pr.ntiles = 1;
+    pr.xn = a.pnorms;
+    pr.margin = margin;
+    pr.tau_g = tau_g;
+    pr.ip = a.ip;
+    pr.k = a.k;
+    pr.cb = c;
+    pr.dbg = nullptr;
+    pr.topk_mode = topk_mode;
+    pr.argmin_out = nullptr;
+    pr.units = a.units;
+    pr.n_units = a.n_units;
+    pr.list_off = a.list_off;
+    pr.pair_codes = a.pair_codes;
+    pr.nprobe = a.nprobe;
+    pr.pbits = a.pbits;
+    static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
+    pr.pf_boxes = pf_env;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.max_units, ctx->sm_count));
+    static const bool dbg_on = getenv("VS_TC_DEBUG") != nullptr;
+    if (dbg_on) {
+        CKS(arena_alloc(ctx, 16, &pr.dbg));
+        CK(cudaMemsetAsync(pr.dbg, 0, 16 * sizeof(unsigned long long), st));
+    }
+    {
+        KTimer kt(ctx, a.timer_class);
+        if (a.ip) CK((launch_tc<true, 2, false>(ma, mb, pr, grid, st)));
+        else CK((launch_tc<false, 2, false>(ma, mb, pr, grid, st)));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    if (dbg_on) {
+        unsigned long long h[16];
+        int nu = 0;
+        CK(cudaMemcpyAsync(h, pr.dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&nu, a.n_units, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double ctas = grid, thr = (double)grid * tc::EPI_THREADS;
+        fprintf(stderr,
+                "[vs_tc ivf] grid=%u units=%d C=%lld tiles/cta=%.1f | producer wait-empty %.0f cyc/cta | "
+                "mma wait-full %.0f wait-tempty %.0f cyc/cta | epi wait-tfull %.0f compaction %.0f cyc/thr | "
+                "compactions %.0f appends %.0f total | tmem-ld wait %.0f chunk-loop %.0f cyc/thr | "
+                "CTA busy max %.2f ms mean %.2f ms, tiles max %llu\n",
+                grid, nu, (long long)C, h[7] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / thr, h[4] / thr,
+                (double)h[5], (double)h[6], h[8] / thr, h[9] / thr, h[10] / 1e6, h[11] / ctas / 1e6, h[12]);
+    }
+    out->cb = c;
+    out->margin = margin;
+    out->tau_g = tau_g;
+    out->verify = topk_mode;
+    return VS_OK;
+}
+
 }  // namespace vs
+

@@ -25,6 +25,40 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
                    unsigned* junk);
 int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out, unsigned* junk);
 
+// IVF list-major phase A on the tensor cores (bf16 list-contiguous payload):
+// pairs already grouped by list into units of <= 128 pairs
+struct TcIvfArgs {
+    const float* Q;
+    int64_t nq;
+    int d;
+    const __nv_bfloat16* payload;
+    int64_t n_total;
+    const float* pnorms;          // per payload position ||x||^2
+    const unsigned* pmax;         // max ||x||^2 (float bits)
+    const int64_t* list_off;
+    int64_t max_list;
+    const int32_t* pair_codes;
+    int64_t npairs;
+    const int4* units;
+    const int* n_units;
+    int64_t max_units;
+    int nprobe;
+    const uint32_t* pbits;
+    int k;
+    int ip;
+    int cshift;
+    int timer_class;
+};
+struct TcIvfOut {
+    CandBuf cb;
+    float* margin;
+    unsigned* tau_g;
+    int verify;
+    bool exhaustive;
+};
+int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out);
+
+int ivf_assign_gpu(vs_ctx* ctx, const vs_ivf* v, const vs_column* col, int32_t* out);
 int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows, uint64_t seed,
                   int32_t metric, int32_t max_iters, vs_ivf** out);
 

@@ -385,6 +385,59 @@ class IvfIndex:
             idx.base = None
         return idx
 
+    @classmethod
+    def from_device_lists(cls, centroids, list_sizes, list_ids, payload, metric: str = SQUARED_L2,
+                          device=None, count: Optional[int] = None) -> "IvfIndex":
+        """Owning index over a caller-owned CUDA tensor holding the
+        list-contiguous payload ([n_total, dim] float32 or bfloat16, the SVIX
+        owning layout), borrowed without a copy (vs_ivf_wrap): for collections
+        that fill most of HBM. The tensor must outlive the index."""
+        import torch
+        check_metric(metric)
+        if not (N.is_torch(payload) and payload.is_cuda and payload.dim() == 2 and payload.is_contiguous()):
+            raise ParameterError("payload must be a contiguous 2-D CUDA tensor")
+        dt = {torch.float32: N.DTYPE_F32, torch.bfloat16: N.DTYPE_BF16}.get(payload.dtype)
+        if dt is None:
+            raise ParameterError("payload must be float32 or bfloat16")
+        cen = np.ascontiguousarray(centroids, np.float32)
+        nlist, dim = cen.shape
+        sizes = np.ascontiguousarray(list_sizes, np.int64)
+        ids = np.ascontiguousarray(list_ids, np.int64) if not N.is_torch(list_ids) else list_ids.contiguous()
+        if sizes.shape != (nlist,) or int(sizes.sum()) != payload.shape[0] or payload.shape[1] != dim:
+            raise ShapeError("list sizes / payload / centroid shapes disagree")
+        ctx = _ctx(device)
+        h = C.c_void_p()
+        N.check(N.load().vs_ivf_wrap(ctx.handle, N.ptr(cen), int(nlist), int(dim), N.ptr(sizes), N.ptr(ids),
+                                     payload.data_ptr(), dt, N.METRIC_CODE[metric], C.byref(h)), "ivf_wrap")
+        div = N.DeviceIvf(ctx, h)
+        div._keepalive = payload
+        ids_h = ids.cpu().numpy() if N.is_torch(ids) else ids
+        partitions = np.split(ids_h, np.cumsum(sizes)[:-1]) if nlist > 1 else [ids_h]
+        if count is None:   # base rows (a list shard may hold only some of them)
+            count = int(ids_h.max()) + 1 if ids_h.size else 0
+        idx = cls(int(nlist), int(dim), count, metric, OWNING, cen, partitions, None, base=None)
+        idx.payload = _LazyPayload(idx)
+        idx._dev[ctx.device] = div
+        return idx
+
+    def assign(self, data, device=None):
+        """Nearest list of every row of `data` (squared L2 to the centroids,
+        the build's assignment step, vecindex.py:303-304) as int32; a CUDA
+        tensor for device columns, else numpy. For indexes trained on a sample."""
+        ctx = _ctx(device)
+        data = _as_column(data)
+        if data.dim != self.dim:
+            raise ShapeError(f"data dim {data.dim} != index dim {self.dim}")
+        div = self.device_index(ctx)
+        dc = device_column(data, ctx)
+        if data._dev_tensor is not None:
+            import torch
+            out = torch.empty(data.count, dtype=torch.int32, device=data._dev_tensor.device)
+        else:
+            out = np.empty(data.count, np.int32)
+        N.check(N.load().vs_ivf_assign(ctx.handle, div.handle, dc.handle, N.ptr(out)), "ivf_assign")
+        return out
+
     def as_layout(self, layout: str, base=None) -> "IvfIndex":
         """A view of the same build in the other layout; results are identical."""
         if layout == self.layout:

@@ -80,6 +80,44 @@ def test_ivf_kernels_empty_lists_and_empty_filter():
         _check(idx, queries, centroids, parts, payload, 16, 5, "squared_l2", few, kernel)
 
 
+def _bf16_index(rng, n, d, nlist, metric="squared_l2"):
+    import torch
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    xb = torch.from_numpy(data).to(torch.bfloat16)
+    rounded = xb.float().numpy()
+    col = vs.EmbeddingColumn.from_device(xb.cuda())
+    idx = vs.IvfIndex.build(col, nlist, metric=metric, seed=0)
+    payload = [rounded[p] for p in idx.partitions]
+    return idx, payload
+
+
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+@pytest.mark.parametrize("d", [64, 96, 768])
+def test_ivf_tensor_core_scan_vs_oracle(metric, d):
+    """tcgen05 list-major scan (VS_OPT_IVF_KERNEL 3): bf16 payload as the B
+    operand straight from the list-contiguous layout, queries grouped by list
+    as the A operand; exact ids/distances/probes vs the oracle."""
+    rng = np.random.default_rng(d + (metric == "inner_product"))
+    n, nlist = 20000, 24          # ~830 rows per list: several 256-row tiles per list
+    idx, payload = _bf16_index(rng, n, d, nlist, metric)
+    queries = rng.standard_normal((300, d)).astype(np.float32)   # > 128 queries per list -> several units
+    for mask in (None, rng.random(n) < 0.3):
+        for nprobe, k in ((1, 10), (5, 64), (nlist, 10)):
+            _check(idx, queries, idx.centroids, idx.partitions, payload, nprobe, k, metric, mask, 3)
+
+
+def test_ivf_tensor_core_scan_forced_retry():
+    rng = np.random.default_rng(77)
+    idx, payload = _bf16_index(rng, 6000, 64, 12)
+    queries = rng.standard_normal((40, 64)).astype(np.float32)
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_FORCE_RETRY, 1)
+    try:
+        _check(idx, queries, idx.centroids, idx.partitions, payload, 4, 20, "squared_l2", None, 3)
+    finally:
+        ctx.set_option(N.OPT_FORCE_RETRY, 0)
+
+
 def test_ivf_lmajor_bf16_payload_matches_qmajor():
     """bf16-stored payload (cfg4 storage): both kernels return the same exact
     top-k over the bf16-rounded rows (the oracle is fed the rounded values)."""
@@ -94,7 +132,7 @@ def test_ivf_lmajor_bf16_payload_matches_qmajor():
     queries = rng.standard_normal((40, d)).astype(np.float32)
     mask = rng.random(n) < 0.2
     payload = [rounded[p] for p in idx.partitions]
-    for kernel in (1, 2):
+    for kernel in (1, 2, 3):
         _check(idx, queries, idx.centroids, idx.partitions, payload, 5, 12, "squared_l2", mask, kernel)
 
 
