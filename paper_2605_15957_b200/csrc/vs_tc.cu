@@ -50,7 +50,7 @@ struct Cfg {
     static constexpr int QTILE = PAIR ? 2 * BM : BM;   // queries per work item
 };
 constexpr int MAX_STAGES = 6;
-constexpr int PF_BOXES = 16;            // MODE 2: default L2 prefetch distance in B boxes
+constexpr int PF_BOXES = 0;             // MODE 2: L2 prefetch distance in B boxes (0: off, measured best)
 constexpr int NTHREADS = 384;           // 12 warps
 constexpr int EPI_WARP0 = 4;            // warps 4..11 drain TMEM (2 per lane quadrant)
 constexpr int EPI_THREADS = 256;
