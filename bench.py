@@ -49,6 +49,9 @@ CONFIGS = {
     4: dict(name="cfg4: IVF-Flat bf16 50M x 768, nlist=16384 nprobe=64 top-10, unfiltered, 10k queries, "
                  "sharded by list", id=4, n=50_000_000, d=768, q=10_000, k=10, sel=None, nlist=16384,
             nprobe=64, bf16=True, cpu_queries=4),
+    5: dict(name="cfg5 B: exact filtered top-100 over 100M x 768 f32 row-sharded over 8 GPUs; each GPU's "
+                 "12.5M-row shard (38.4 GB) resident in pinned HOST memory and streamed per search",
+            id=5, n=100_000_000, d=768, q=10_000, k=100, sel=0.10, shards=8, host=True),
 }
 
 
@@ -332,11 +335,40 @@ class ExactWorkload:
             self.bits = pack_bits_torch(m)
             self.queries = torch.from_numpy(np.ascontiguousarray(q, np.float32)).to(dev)
             self.lo, self.n_sel, self.n_sel_total = 0, int(mask.sum()), int(mask.sum())
+        elif cfg.get("host"):
+            # this rank's 1/8 shard (ranks 0..7 hold shards 0..7), generated on
+            # the device chunk by chunk and parked in pinned host memory
+            n_sh = cfg["n"] // cfg["shards"]
+            self.lo = (rank % cfg["shards"]) * n_sh
+            t0 = time.time()
+            host = torch.empty((n_sh, cfg["d"]), dtype=torch.float32).pin_memory()
+            chunk = 1 << 20
+            centers = None
+            for a in range(0, n_sh, chunk):
+                b = min(n_sh, a + chunk)
+                part, centers = _device_slice(cfg["n"], cfg["d"], self.lo + a, self.lo + b, dev)
+                host[a:b].copy_(part)
+                del part
+            g = torch.Generator(device=dev)
+            g.manual_seed(4242)
+            mask = torch.rand(cfg["n"], generator=g, device=dev)[self.lo:self.lo + n_sh] < cfg["sel"]
+            self.bits = pack_bits_torch(mask.contiguous())
+            from paper_2605_15957_b200 import synth
+            self.queries = synth.device_queries(centers, self.nq, seed=7)
+            self.n_sel = self.n_sel_total = int(mask.sum())
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            log(f"[rank {rank}] cfg5 shard {n_sh} x {cfg['d']} in pinned host memory ({time.time() - t0:.1f}s)")
+            self.host_data = host
+            self.col = vs.EmbeddingColumn.host_resident(host)
+            self.h2d_peak = _pinned_h2d_gbs(dev)
+            data = None
         else:
             W = build_cfg2(rank, world, cfg)
             data, self.bits, self.queries = W["data"], W["bits"], W["queries"]
             self.lo, self.n_sel, self.n_sel_total = W["lo"], W["n_sel"], W["n_sel_total"]
-        self.col = vs.EmbeddingColumn.from_device(data)
+        if data is not None:
+            self.col = vs.EmbeddingColumn.from_device(data)
         nq, k = self.nq, self.k
         self.out_dev = (torch.empty((nq, k), dtype=torch.int64, device=dev),
                         torch.empty((nq, k), dtype=torch.float64, device=dev),
@@ -382,9 +414,19 @@ class ExactWorkload:
         return self.nq * (self.world if self.replicas else 1)
 
     def scaling(self):
-        return "weak" if self.replicas else "strong"
+        return "weak" if (self.replicas or self.cfg.get("host")) else "strong"
 
     def roofline(self, kt, steps, ctx, N):
+        if self.cfg.get("host"):
+            # streamed variant: the bound is the PCIe transfer of the selected rows
+            byts = float(self.n_sel) * self.d * 4
+            ms = self.last_ms_step
+            achieved = byts / (ms / 1e3) / 1e9
+            return {"bound": "pcie", "kernel": "whole search (selected-row gather over PCIe + tcgen05 scan)",
+                    "achieved": round(achieved, 2), "peak": round(self.h2d_peak, 2), "unit": "GB/s",
+                    "frac": round(achieved / self.h2d_peak, 4),
+                    "peak_source": "measured in this run: pinned host->device copy of 1 GiB",
+                    "algorithmic_bytes_per_step": byts, "traffic": None}
         peaks = measured_peaks()
         scan_ns, scan_n = kt["enn_scan"]
         flops = 2.0 * self.nq * self.n_sel * self.d
@@ -403,9 +445,13 @@ class ExactWorkload:
         c = self.cfg
         par = ("replicas x%d (query batches independent)" % self.world if self.replicas else
                f"row-shard x{self.world} + allgather/merge") if self.world > 1 else "single GPU"
-        return {"workload": c["name"], "n_rows": c["n"], "dim": self.d, "queries": self.nq, "k": self.k,
+        if c.get("host"):
+            par = f"{self.world} of {c['shards']} row shards (one per GPU), host-resident, allgather/merge"
+        n_rows = c["n"] // c["shards"] * self.world if c.get("host") else c["n"]
+        return {"workload": c["name"], "n_rows": n_rows, "dim": self.d, "queries": self.nq, "k": self.k,
                 "selectivity": c["sel"], "n_selected": self.n_sel_total, "parallelism": par,
                 "l2_flush": ("inputs larger than L2 (41 GB collection vs 126 MB L2)" if c["id"] == 2 else
+                             "inputs in host memory (38.4 GB shard), streamed every step" if c["id"] == 5 else
                              "none: 16.5 MB selected working set is L2-resident (latency-bound config)"),
                 "phase_a_kernel": getattr(self, "kernel_name", "?")}
 
@@ -421,9 +467,27 @@ class ExactWorkload:
     def cpu_baseline(self, args):
         if self.cfg["id"] == 1:
             return time_cpu_cfg1(self.host_sample, self.k, args.cpu_budget)
-        qps_cpu, sample, cores = time_cpu_reference(self.cfg, budget_s=args.cpu_budget, processes=1)
+        cfg = dict(self.cfg)
+        if cfg.get("host"):
+            cfg["n"] = cfg["n"] // cfg["shards"]   # the same per-GPU shard the GPU arm searches
+        qps_cpu, sample, cores = time_cpu_reference(cfg, budget_s=args.cpu_budget, processes=1)
         return {"value": round(qps_cpu, 6), "unit": "queries/s", "cores": cores, "kind": "port",
                 "sample": sample}
+
+
+def _pinned_h2d_gbs(dev):
+    import torch
+    a = torch.empty(1 << 28, dtype=torch.float32).pin_memory()
+    b = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+    b.copy_(a, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        b.copy_(a, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return 3 * a.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def time_cpu_cfg1(sample, k, budget_s):
@@ -714,6 +778,7 @@ def run_ours(args, cfg):
     ctx.set_option(N.OPT_TIMING, 0)
 
     units = wl.units_per_step()
+    wl.last_ms_step = ms / args.steps
     qps = units * args.steps / (ms / 1e3)
     qps_e2e = units * args.steps / (ms_e2e / 1e3)
     roof = wl.roofline(kt, args.steps, ctx, N)

@@ -58,7 +58,8 @@ enum vs_option {
     VS_OPT_IVF_KERNEL = 2,   /* 0 auto, 1 query-major scan, 2 list-major scan      */
     VS_OPT_CAND_SLACK = 3,   /* extra candidate-buffer capacity (power-of-2 sized) */
     VS_OPT_FORCE_RETRY = 4,  /* test hook: treat every query as overflowed once    */
-    VS_OPT_TIMING = 5        /* 1: record CUDA events around every kernel class    */
+    VS_OPT_TIMING = 5,       /* 1: record CUDA events around every kernel class    */
+    VS_OPT_STREAM_CHUNK = 6  /* host-resident search: selected rows per chunk (0 auto) */
 };
 
 /* kernel classes reported by vs_ctx_kernel_times (CUDA-event durations on the
@@ -114,6 +115,12 @@ int vs_column_create(vs_ctx* ctx, const void* src, int64_t n, int32_t d,
 /* borrow caller-owned device rows (must outlive the column) */
 int vs_column_wrap(vs_ctx* ctx, void* dev_ptr, int64_t n, int32_t d,
                    int32_t dtype, vs_column** out);
+/* Column over caller-owned HOST memory (pinned, or registered here with
+ * cudaHostRegister): searches stream only the rows the bitmap selects over
+ * PCIe (zero-copy gathers on a few SMs, overlapped with the tensor-core scan of
+ * the previous chunk) and merge the per-chunk top-k. */
+int vs_column_wrap_host(vs_ctx* ctx, void* host_ptr, int64_t n, int32_t d,
+                        int32_t dtype, vs_column** out);
 int vs_column_free(vs_column* col);
 int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype);
 

@@ -24,6 +24,7 @@ VS_ERR_CAP_EXCEEDED, VS_ERR_PLACEMENT, VS_ERR_CUDA, VS_ERR_INTERNAL = 4, 5, 6, 7
 METRIC_CODE = {"squared_l2": 0, "inner_product": 1}
 DTYPE_F32, DTYPE_BF16 = 0, 1
 OPT_ENN_KERNEL, OPT_IVF_KERNEL, OPT_CAND_SLACK, OPT_FORCE_RETRY, OPT_TIMING = 1, 2, 3, 4, 5
+OPT_STREAM_CHUNK = 6
 KERNEL_CLASSES = ("select", "enn_scan", "rerank", "coarse", "ivf_scan", "ivf_rerank", "merge", "stage")
 STAT_LAUNCHES, STAT_OVERFLOW_QUERIES, STAT_SURVIVORS, STAT_LAST_ENN_KERNEL = 0, 1, 2, 3
 
@@ -45,6 +46,7 @@ SIGNATURES = {
     "vs_ctx_kernel_times": (C.c_int, [_vp, _vp, _vp, _i32, _i32]),
     "vs_column_create": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
     "vs_column_wrap": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
+    "vs_column_wrap_host": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
     "vs_column_free": (C.c_int, [_vp]),
     "vs_column_info": (C.c_int, [_vp, _vp, _vp, _vp]),
     "vs_enn_search": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i64,
@@ -198,10 +200,11 @@ class DeviceColumn:
     """Library-owned (or borrowed) device copy of an embedding column."""
 
     def __init__(self, ctx: Context, src, n: int, d: int, dtype: int = DTYPE_F32,
-                 borrow: bool = False, keepalive=None):
+                 borrow: bool = False, keepalive=None, host: bool = False):
         lib = load()
         h = _vp()
-        fn = lib.vs_column_wrap if borrow else lib.vs_column_create
+        fn = lib.vs_column_wrap_host if host else lib.vs_column_wrap if borrow else lib.vs_column_create
+        borrow = borrow or host
         check(fn(ctx.handle, ptr(src) if not isinstance(src, int) else src, int(n), int(d),
                  int(dtype), C.byref(h)), "column")
         self.handle = h

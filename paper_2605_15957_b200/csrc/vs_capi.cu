@@ -111,6 +111,7 @@ struct EnnJob {
     int ip;
     int k;
     int64_t id_offset;
+    const int64_t* id_map = nullptr;   // staged position -> base row (streamed chunks)
     // outputs (device, nullable)
     int64_t* out_ids;
     double* out_dist;
@@ -222,7 +223,7 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     rp.verify = sp.verify;
     rp.rows = job.rows;
     rp.row_map = job.sel;
-    rp.id_map = nullptr;
+    rp.id_map = job.id_map;
     rp.id_offset = job.id_offset;
     const int64_t all_slots = (int64_t)sp.cb.n_sub * sp.cb.C;
     rp.s_cap = (exhaustive || (int64_t)job.nq * all_slots * 20 < (int64_t(1) << 30))
@@ -395,6 +396,7 @@ int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value) {
     switch (key) {
         case VS_OPT_ENN_KERNEL: ctx->opt_enn_kernel = (int)value; break;
         case VS_OPT_IVF_KERNEL: ctx->opt_ivf_kernel = (int)value; break;
+        case VS_OPT_STREAM_CHUNK: ctx->opt_stream_chunk = value; break;
         case VS_OPT_CAND_SLACK: ctx->opt_slack = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8)); break;
         case VS_OPT_FORCE_RETRY: ctx->opt_force_retry = (int)value; break;
         case VS_OPT_TIMING: ctx->opt_timing = (int)value; break;
@@ -472,11 +474,43 @@ int vs_column_wrap(vs_ctx* ctx, void* dev_ptr, int64_t n, int32_t d, int32_t dty
     return VS_OK;
 }
 
+int vs_column_wrap_host(vs_ctx* ctx, void* host_ptr, int64_t n, int32_t d, int32_t dtype, vs_column** out) {
+    if (!ctx || !out || (!host_ptr && n > 0)) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (n < 0 || d < 1) return set_err(VS_ERR_SHAPE, "bad column shape");
+    if (dtype != VS_DTYPE_F32 && dtype != VS_DTYPE_BF16) return set_err(VS_ERR_PARAMETER, "bad dtype");
+    DevGuard g(ctx->device);
+    const size_t bytes = (size_t)n * d * elem_size(dtype);
+    cudaPointerAttributes at{};
+    bool registered = false;
+    if (cudaPointerGetAttributes(&at, host_ptr) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
+        cudaGetLastError();
+        CK(cudaHostRegister(host_ptr, bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+        registered = true;
+    } else if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+        return set_err(VS_ERR_PARAMETER, "vs_column_wrap_host needs host memory");
+    }
+    void* dptr = nullptr;
+    CK(cudaHostGetDevicePointer(&dptr, host_ptr, 0));
+    vs_column* c = new vs_column();
+    c->ctx = ctx;
+    c->data = dptr;
+    c->n = n;
+    c->d = d;
+    c->dtype = dtype;
+    c->owned = false;
+    c->host_resident = true;
+    c->host_registered = registered;
+    c->host_ptr = host_ptr;
+    *out = c;
+    return VS_OK;
+}
+
 int vs_column_free(vs_column* col) {
     if (!col) return VS_OK;
     DevGuard g(col->ctx->device);
     cudaStreamSynchronize(col->ctx->stream);
     if (col->owned && col->data) cudaFree(col->data);
+    if (col->host_registered) cudaHostUnregister(col->host_ptr);
     if (col->norms) cudaFree(col->norms);
     if (col->max_norm_bits) cudaFree(col->max_norm_bits);
     delete col;
@@ -489,6 +523,146 @@ int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype)
     if (d) *d = col->d;
     if (dtype) *dtype = col->dtype;
     return VS_OK;
+}
+
+// device-side merge of nparts [nq][k_in] partial results (no arena reset)
+static int merge_parts(vs_ctx* ctx, int nparts, int64_t nq, int k_in, const int64_t* ids, const double* dist,
+                       const int32_t* counts, int k, int metric, int64_t* out_ids, double* out_dist,
+                       int32_t* out_count) {
+    vs::MergeParams p;
+    p.nparts = nparts;
+    p.nq = nq;
+    p.k_in = k_in;
+    p.k = k;
+    p.ip = metric;
+    p.ids = ids;
+    p.dist = dist;
+    p.counts = counts;
+    const size_t n_in = (size_t)nparts * nq * k_in;
+    CKS(arena_alloc(ctx, n_in, &p.s_key));
+    CKS(arena_alloc(ctx, n_in, &p.s_id));
+    p.out_ids = out_ids;
+    p.out_dist = out_dist;
+    p.out_count = out_count;
+    {
+        KTimer kt(ctx, VS_K_MERGE);
+        CK(vs::launch_merge(p, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    return VS_OK;
+}
+
+// Search of a host-resident column (cfg5 B): only the SELECTED rows cross
+// PCIe (the bitmap is applied before any row byte moves). The selection is cut
+// into chunks; chunk c+1 is gathered by a few SMs over PCIe (zero-copy 16-byte
+// reads, copy stream) while chunk c is searched on the remaining SMs; the
+// per-chunk top-k are merged with the cross-shard merge kernel (same tie rule).
+static int enn_search_streamed(vs_ctx* ctx, vs_column* col, const float* dq, int64_t nq, int d,
+                               const int64_t* sel, int64_t nsel, int k, int metric, int64_t id_offset,
+                               const float* margin, int64_t* out_ids, double* out_dist, int32_t* out_count) {
+    const size_t es = elem_size(col->dtype);
+    const int row_bytes = d * (int)es;
+    if (row_bytes % 16) return set_err(VS_ERR_PARAMETER, "host-resident rows must be 16-byte multiples");
+    int64_t chunk = ctx->opt_stream_chunk > 0 ? ctx->opt_stream_chunk
+                                              : std::max<int64_t>(1, ((int64_t)1 << 30) / row_bytes);   // 1 GiB
+    chunk = std::min(chunk, nsel);
+    const int64_t nchunks = (nsel + chunk - 1) / chunk;
+    if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    // the selection must be a device array the gather can read
+    const int64_t* dsel = sel;
+    int64_t* iota = nullptr;
+    if (!dsel) {
+        std::vector<int64_t> h(nsel);
+        for (int64_t i = 0; i < nsel; ++i) h[i] = i;
+        CKS(arena_alloc(ctx, (size_t)nsel, &iota));
+        CK(cudaMemcpyAsync(iota, h.data(), nsel * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        dsel = iota;
+    }
+    char* buf[2] = {nullptr, nullptr};
+    float* nrm[2] = {nullptr, nullptr};
+    unsigned* junk = nullptr;
+    for (int b = 0; b < std::min<int64_t>(2, nchunks); ++b) {
+        CKS(arena_alloc(ctx, (size_t)chunk * row_bytes, &buf[b]));
+        CKS(arena_alloc(ctx, (size_t)chunk, &nrm[b]));
+    }
+    CKS(arena_alloc(ctx, 1, &junk));
+    int64_t *cids = nullptr;
+    double* cdist = nullptr;
+    int32_t* ccnt = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nchunks * nq * k, &cids));
+    CKS(arena_alloc(ctx, (size_t)nchunks * nq * k, &cdist));
+    CKS(arena_alloc(ctx, (size_t)nchunks * nq, &ccnt));
+    cudaEvent_t ready[2], done[2];
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    }
+    const int reserve = nchunks > 1 ? 8 : 0;     // SMs for the overlapped PCIe gather
+    const int gblocks = nchunks > 1 ? reserve * 4 : ctx->sm_count * 4;
+    auto gather = [&](int64_t c) -> int {
+        const int b = (int)(c & 1);
+        const int64_t c0 = c * chunk, nc = std::min(chunk, nsel - c0);
+        CK(vs::launch_gather_rows_host(col->data, dsel + c0, nc, row_bytes, buf[b], gblocks, ctx->copy_stream));
+        CK(cudaMemsetAsync(junk, 0, sizeof(unsigned), ctx->copy_stream));
+        if (col->dtype == VS_DTYPE_F32)
+            CK(vs::launch_row_norms<float>((const float*)buf[b], nc, d, nrm[b], junk, ctx->copy_stream));
+        else
+            CK(vs::launch_row_norms<__nv_bfloat16>((const __nv_bfloat16*)buf[b], nc, d, nrm[b], junk,
+                                                   ctx->copy_stream));
+        CK(cudaEventRecord(ready[b], ctx->copy_stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 2;
+        return VS_OK;
+    };
+    int rc = VS_OK;
+    ctx->sm_reserve = reserve;
+    CK(cudaEventRecord(done[0], ctx->stream));
+    CK(cudaEventRecord(done[1], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->copy_stream, done[0], 0));   // queries/selection are ready
+    rc = gather(0);
+    for (int64_t c = 0; rc == VS_OK && c < nchunks; ++c) {
+        const int b = (int)(c & 1);
+        if (c + 1 < nchunks) {
+            cudaStreamWaitEvent(ctx->copy_stream, done[(c + 1) & 1], 0);   // buffer reuse
+            if ((rc = gather(c + 1)) != VS_OK) break;
+        }
+        cudaStreamWaitEvent(ctx->stream, ready[b], 0);
+        const int64_t c0 = c * chunk, nc = std::min(chunk, nsel - c0);
+        EnnJob job;
+        job.q = dq;
+        job.nq = nq;
+        job.d = d;
+        job.rows = buf[b];
+        job.dtype = col->dtype;
+        job.sel = nullptr;
+        job.nsel = nc;
+        job.xnorm = nrm[b];
+        job.xmax = col->max_norm_bits;
+        job.ip = metric;
+        job.k = k;
+        job.id_offset = id_offset;
+        job.id_map = dsel + c0;
+        job.out_ids = cids + c * nq * k;
+        job.out_dist = cdist + c * nq * k;
+        job.out_ids32 = nullptr;
+        job.out_count = ccnt + c * nq;
+        if ((rc = run_enn(ctx, job, margin, 0, true)) != VS_OK) break;
+        cudaEventRecord(done[b], ctx->stream);
+    }
+    ctx->sm_reserve = 0;
+    cudaStreamSynchronize(ctx->copy_stream);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(ready[b]);
+        cudaEventDestroy(done[b]);
+    }
+    if (rc != VS_OK) return rc;
+    if (nchunks == 1) {
+        if (out_ids) CK(cudaMemcpyAsync(out_ids, cids, (size_t)nq * k * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (out_dist) CK(cudaMemcpyAsync(out_dist, cdist, (size_t)nq * k * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (out_count) CK(cudaMemcpyAsync(out_count, ccnt, (size_t)nq * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        return VS_OK;
+    }
+    return merge_parts(ctx, (int)nchunks, nq, k, cids, cdist, ccnt, k, metric, out_ids, out_dist, out_count);
 }
 
 int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int64_t nq, int32_t d,
@@ -542,7 +716,12 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
     CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
     job.out_ids32 = nullptr;
-    CKS(run_enn(ctx, job, margin, 0, true));
+    if (col->host_resident) {
+        CKS(enn_search_streamed(ctx, col, dq, nq, d, sel, nsel, k, metric, id_offset, margin, job.out_ids,
+                                job.out_dist, job.out_count));
+    } else {
+        CKS(run_enn(ctx, job, margin, 0, true));
+    }
     CKS(flush_out(ctx, pending));
     return VS_OK;
 }

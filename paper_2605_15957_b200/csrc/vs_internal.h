@@ -126,6 +126,9 @@ struct vs_ctx {
     int opt_slack = 0;
     int opt_force_retry = 0;
     int opt_timing = 0;
+    int64_t opt_stream_chunk = 0;    // host-resident search: selected rows per chunk (0 = auto)
+    int sm_reserve = 0;              // SMs left free by persistent kernels (streamed gathers)
+    cudaStream_t copy_stream = nullptr;   // host-resident search: gathers over PCIe
     // CUDA-event timing of kernel classes (resolved after each call's final sync)
     struct PendingTimer {
         int cls;
@@ -144,6 +147,9 @@ struct vs_column {
     int d = 0;
     int dtype = VS_DTYPE_F32;
     bool owned = false;
+    bool host_resident = false;      // data lives in pinned host memory (streamed per search)
+    bool host_registered = false;    // we cudaHostRegister'ed it (unregister on free)
+    void* host_ptr = nullptr;
     float* norms = nullptr;          // ||x||^2 per row (lazy)
     unsigned* max_norm_bits = nullptr;
     bool norms_ready = false;

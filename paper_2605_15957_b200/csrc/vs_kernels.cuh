@@ -207,6 +207,8 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_gather_rows(const T* src, const int64_t* ids, int64_t n, int d, T* dst,
                                cudaStream_t s);
+cudaError_t launch_gather_rows_host(const void* src, const int64_t* ids, int64_t n, int row_bytes, void* dst,
+                                    int blocks, cudaStream_t s);
 cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe, const int64_t* list_off, int nlist,
                                  const uint8_t* list_owned, const uint32_t* pbits, int32_t* sel_scratch,
                                  unsigned long long* visited, cudaStream_t s);

@@ -710,10 +710,10 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
                                       rows + rb * (int64_t)d + offL + 8 * M, ntail, tl, lane, sa, sb);
             if (lane == 0) {
                 skey[i] = d2o(IP ? -sa : sa);
-                sid[i] = p.id_map ? p.id_map[psa] : ra + p.id_offset;
+                sid[i] = (p.id_map ? p.id_map[psa] : ra) + p.id_offset;
                 if (hasb) {
                     skey[i2] = d2o(IP ? -sb : sb);
-                    sid[i2] = p.id_map ? p.id_map[psb] : rb + p.id_offset;
+                    sid[i2] = (p.id_map ? p.id_map[psb] : rb) + p.id_offset;
                 }
             }
         }
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
             const double sc = warp_np_score<IP, T>(qs, cur, d, sm, cb, lb, lane);
             if (lane == 0) {
                 skey[i] = d2o(IP ? -sc : sc);
-                sid[i] = p.id_map ? p.id_map[ps_cur] : r_cur + p.id_offset;
+                sid[i] = (p.id_map ? p.id_map[ps_cur] : r_cur) + p.id_offset;
             }
             __syncwarp();
             ps_cur = ps_n;
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
             const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
             const double sc = np_pairwise<T, IP>(qs, rows + r * (int64_t)d, d);
             skey[i] = d2o(IP ? -sc : sc);
-            sid[i] = p.id_map ? p.id_map[ps] : r + p.id_offset;
+            sid[i] = (p.id_map ? p.id_map[ps] : r) + p.id_offset;
         }
     }
     __syncthreads();

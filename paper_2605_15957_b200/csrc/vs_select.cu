@@ -253,4 +253,27 @@ template cudaError_t launch_gather_rows<float>(const float*, const int64_t*, int
 template cudaError_t launch_gather_rows<__nv_bfloat16>(const __nv_bfloat16*, const int64_t*, int64_t,
                                                       int, __nv_bfloat16*, cudaStream_t);
 
+// selected rows of a host-resident (pinned, device-mapped) column -> device,
+// 16-byte zero-copy reads over PCIe, warp per row; `blocks` bounds the SMs used
+// so the gather can run beside a persistent tensor-core kernel
+__global__ void k_gather_rows_v16(const uint4* __restrict__ src, const int64_t* __restrict__ ids, int64_t n,
+                                  int row_vecs, uint4* __restrict__ dst) {
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = warp; r < n; r += nwarps) {
+        const uint4* a = src + ids[r] * (int64_t)row_vecs;
+        uint4* b = dst + r * (int64_t)row_vecs;
+        for (int i = lane; i < row_vecs; i += 32) b[i] = a[i];
+    }
+}
+cudaError_t launch_gather_rows_host(const void* src, const int64_t* ids, int64_t n, int row_bytes, void* dst,
+                                    int blocks, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (row_bytes % 16) return cudaErrorInvalidValue;
+    k_gather_rows_v16<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(src), ids, n, row_bytes / 16,
+                                              reinterpret_cast<uint4*>(dst));
+    return cudaGetLastError();
+}
+
 }  // namespace vs

@@ -948,7 +948,8 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     const int qtile_rows = pair ? 2 * tc::BM : tc::BM;
     const int qtiles = (int)((nq + qtile_rows - 1) / qtile_rows);
     const int64_t ntiles = (nsel + tc::BN - 1) / tc::BN;
-    const int sms = pair ? ctx->sm_count / 2 : ctx->sm_count;   // work units (CTAs or pairs)
+    const int sm_avail = std::max(2, ctx->sm_count - ctx->sm_reserve);      // SMs left to this kernel
+    const int sms = pair ? sm_avail / 2 : sm_avail;                         // work units (CTAs or pairs)
     int best_s = 1;
     double best_cost = 1e30;
     const int smin = std::max(1, (int)std::min<int64_t>(ntiles, (2 * sms + qtiles - 1) / qtiles));

@@ -53,10 +53,14 @@ def embedding(dim: int) -> FieldType:
     return FieldType("embedding", dim)
 
 
+def N_is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
 class EmbeddingColumn:
     """Fixed-dimension vectors stored as one contiguous float32 region."""
 
-    __slots__ = ("_values", "dim", "count", "_device", "_dev_tensor", "__weakref__")
+    __slots__ = ("_values", "dim", "count", "_device", "_dev_tensor", "_host_stream", "__weakref__")
 
     def __init__(self, values, dim: int | None = None):
         arr = np.asarray(values, dtype=np.float32)
@@ -81,6 +85,7 @@ class EmbeddingColumn:
         self.count = arr.shape[0]
         self._device = {}
         self._dev_tensor = None
+        self._host_stream = None
 
     @classmethod
     def empty(cls, dim: int) -> "EmbeddingColumn":
@@ -102,10 +107,36 @@ class EmbeddingColumn:
         obj.count = int(tensor.shape[0])
         obj._device = {}
         obj._dev_tensor = tensor.contiguous()
+        obj._host_stream = None
+        return obj
+
+    @classmethod
+    def host_resident(cls, values) -> "EmbeddingColumn":
+        """Keep the vectors in (pinned) HOST memory: searches stream only the
+        rows the row filter selects over PCIe. `values`
+        is a C-contiguous float32/bfloat16 numpy array or CPU torch tensor
+        (pinned memory avoids a registration at first use)."""
+        import torch
+        t = values if N_is_torch(values) else torch.from_numpy(np.ascontiguousarray(values))
+        if t.is_cuda or t.dim() != 2 or not t.is_contiguous():
+            raise ShapeError("host_resident needs a contiguous 2-D host array")
+        if t.dtype not in (torch.float32, torch.bfloat16):
+            raise ShapeError("host-resident embeddings must be float32 or bfloat16")
+        obj = cls.__new__(cls)
+        obj._values = None
+        obj.dim = int(t.shape[1])
+        obj.count = int(t.shape[0])
+        obj._device = {}
+        obj._dev_tensor = None
+        obj._host_stream = t
         return obj
 
     @property
     def values(self) -> np.ndarray:
+        if self._values is None and self._host_stream is not None:
+            v = self._host_stream.float().numpy()
+            v.setflags(write=False)
+            self._values = v
         if self._values is None:
             v = self._dev_tensor.float().cpu().numpy()
             v.setflags(write=False)
@@ -114,7 +145,8 @@ class EmbeddingColumn:
 
     @property
     def storage_dtype(self) -> str:
-        if self._dev_tensor is not None and str(self._dev_tensor.dtype) == "torch.bfloat16":
+        t = self._dev_tensor if self._dev_tensor is not None else self._host_stream
+        if t is not None and str(t.dtype) == "torch.bfloat16":
             return "bfloat16"
         return "float32"
 

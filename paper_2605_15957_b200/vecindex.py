@@ -124,7 +124,11 @@ def device_column(col, ctx: N.Context) -> N.DeviceColumn:
     if isinstance(col, EmbeddingColumn):
         dc = col._device.get(ctx.device)
         if dc is None:
-            if col._dev_tensor is not None:
+            if col._host_stream is not None:
+                t = col._host_stream
+                dt = N.DTYPE_BF16 if col.storage_dtype == "bfloat16" else N.DTYPE_F32
+                dc = N.DeviceColumn(ctx, t.data_ptr(), col.count, col.dim, dt, host=True, keepalive=t)
+            elif col._dev_tensor is not None:
                 t = col._dev_tensor
                 dt = N.DTYPE_BF16 if col.storage_dtype == "bfloat16" else N.DTYPE_F32
                 dc = N.DeviceColumn(ctx, t.data_ptr(), col.count, col.dim, dt, borrow=True, keepalive=t)
