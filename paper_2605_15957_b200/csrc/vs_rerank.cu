@@ -685,26 +685,38 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = m < M ? Pair2<T>::ld(xg + 8 * m) : make_float2(0.f, 0.f);
         };
-        // two rows per iteration (rows i and i + NWARP of this warp)
-        for (int64_t i = w; i < ns; i += 2 * NWARP) {
+        // two rows per iteration (rows i and i + NWARP of this warp). The next
+        // pair's row indices (dependent loads of the survivor list and the
+        // selection) are fetched while this pair's row loads are in flight,
+        // and the next pair's rows are prefetched into L2.
+        auto prefetch_row = [&](int64_t r) {
+            const char* base = reinterpret_cast<const char*>(rows + r * (int64_t)d);
+            for (int o = lane * 128; o < row_bytes; o += 32 * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
+        };
+        int64_t i = w;
+        uint32_t psa = 0, psb = 0;
+        int64_t ra = 0, rb = 0;
+        if (i < ns) {
+            ra = row_of(i, psa);
+            rb = (i + NWARP < ns) ? row_of(i + NWARP, psb) : ra;
+        }
+        for (; i < ns; i += 2 * NWARP) {
             const int64_t i2 = i + NWARP;
             const bool hasb = i2 < ns;
-            // the next pair -> L2 while this pair is scored
-            for (int h = 0; h < 2; ++h) {
-                const int64_t ip = i + (2 + h) * NWARP;
-                if (ip < ns) {
-                    uint32_t pf;
-                    const char* base = reinterpret_cast<const char*>(rows + row_of(ip, pf) * (int64_t)d);
-                    for (int o = lane * 128; o < row_bytes; o += 32 * 128)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
-                }
-            }
-            uint32_t psa, psb = 0;
-            const int64_t ra = row_of(i, psa);
-            const int64_t rb = hasb ? row_of(i2, psb) : ra;
             float2 xa[16], xb[16];
             fetch(xa, ra);
             fetch(xb, rb);
+            // next pair: indices now (overlapping the loads above), rows -> L2
+            const int64_t in = i + 2 * NWARP, in2 = in + NWARP;
+            uint32_t psa_n = 0, psb_n = 0;
+            int64_t ra_n = 0, rb_n = 0;
+            if (in < ns) {
+                ra_n = row_of(in, psa_n);
+                rb_n = (in2 < ns) ? row_of(in2, psb_n) : ra_n;
+                prefetch_row(ra_n);
+                if (in2 < ns) prefetch_row(rb_n);
+            }
             double sa, sb;
             warp_np_score_reg2<IP, T>(qpd, xa, xb, M, qtail, rows + ra * (int64_t)d + offL + 8 * M,
                                       rows + rb * (int64_t)d + offL + 8 * M, ntail, tl, lane, sa, sb);
@@ -716,6 +728,10 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
                     sid[i2] = (p.id_map ? p.id_map[psb] : rb) + p.id_offset;
                 }
             }
+            ra = ra_n;
+            rb = rb_n;
+            psa = psa_n;
+            psb = psb_n;
         }
     } else if (warp_path) {
         // double-buffered: the next survivor row is staged (cp.async-free plain
