@@ -26,12 +26,12 @@ namespace {
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
 constexpr int KMAX = 2048;      // == vs_topk_cap(): sort capacity
-constexpr int LCAP = 4096;      // live candidates staged in shared memory per query
+constexpr int LCAP = 8192;      // live candidates staged in shared memory per query
 constexpr int MAXLEAF = 32;     // numpy pairwise leaves (>= 64 elements each) -> d <= 2048 on the warp path
 constexpr int WARP_D_MAX = 2048;
 // union of: live candidates (LCAP x 8 B), staged rows (NWARP x d x 4 B),
 // sort buffers (KMAX x 16 B)
-constexpr size_t UNION_BYTES = 32768;
+constexpr size_t UNION_BYTES = 65536;
 // staged row stride (elements): padded d plus the leaf skews (32 B per leaf;
 // leaves hold >= 64 elements, so at most d / 64 + 1 of them)
 __host__ __device__ __forceinline__ int row_stride(int d) { return ((d + 7) & ~7) + 16 * (d / 64 + 1); }
@@ -571,24 +571,36 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     __syncthreads();
     for (int s = w; s < nsub; s += NWARP) {
         const int cs = cnts[s];
-        for (int j0 = 0; j0 < cs; j0 += 32) {
-            const int j = j0 + lane;
-            float kk = 0.f;
-            uint32_t pp = 0;
-            bool live = false;
-            if (j < cs) {
-                kk = ckey[(int64_t)s * C + j];
-                live = f2o(kk) <= pre;
-                if (live) pp = cpos[(int64_t)s * C + j];
+        const float* bk = ckey + (int64_t)s * C;
+        const uint32_t* bp = cpos + (int64_t)s * C;
+        for (int j0 = 0; j0 < cs; j0 += 128) {
+            // four independent key loads in flight, then the positions of the live ones
+            float kk[4];
+            uint32_t pp[4];
+            bool live[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int j = j0 + 32 * h + lane;
+                kk[h] = j < cs ? bk[j] : 0.f;
             }
-            const unsigned b = __ballot_sync(VS_FULL, live);
-            int base = 0;
-            if (lane == 0 && b) base = atomicAdd(&sm.counter, __popc(b));
-            base = __shfl_sync(VS_FULL, base, 0);
-            const int slot = base + __popc(b & lanemask_lt());
-            if (live && slot < LCAP) {
-                lkey[slot] = kk;
-                lpos[slot] = pp;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int j = j0 + 32 * h + lane;
+                live[h] = j < cs && f2o(kk[h]) <= pre;
+                pp[h] = live[h] ? bp[j] : 0u;
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const unsigned b = __ballot_sync(VS_FULL, live[h]);
+                if (!b) continue;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
+                base = __shfl_sync(VS_FULL, base, 0);
+                const int slot = base + __popc(b & lanemask_lt());
+                if (live[h] && slot < LCAP) {
+                    lkey[slot] = kk[h];
+                    lpos[slot] = pp[h];
+                }
             }
         }
     }
