@@ -950,6 +950,10 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     const int64_t ntiles = (nsel + tc::BN - 1) / tc::BN;
     const int sm_avail = std::max(2, ctx->sm_count - ctx->sm_reserve);      // SMs left to this kernel
     const int sms = pair ? sm_avail / 2 : sm_avail;                         // work units (CTAs or pairs)
+    // split count: >= 2 waves of work items; among those the smallest makespan
+    // (short splits also keep every candidate buffer below its compaction point)
+    const int64_t C0 = topk_mode ? vs_internal::pow2ceil(2 * sp.k + 96 + tc::BN / 2)
+                                 : vs_internal::pow2ceil(sp.k + 512);
     int best_s = 1;
     double best_cost = 1e30;
     const int smin = std::max(1, (int)std::min<int64_t>(ntiles, (2 * sms + qtiles - 1) / qtiles));
@@ -963,10 +967,12 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
             best_s = s;
         }
     }
+    if (getenv("VS_TC_NSPLIT")) best_s = std::max(1, std::min<int>((int)ntiles, atoi(getenv("VS_TC_NSPLIT"))));
     const int64_t per = (ntiles + best_s - 1) / best_s;
     const int nsplit = (int)((ntiles + per - 1) / per);
-    int64_t C = (topk_mode ? vs_internal::pow2ceil(2 * sp.k + 96) : vs_internal::pow2ceil(sp.k + 512))
-                << (ctx->opt_slack + cshift);
+    // a buffer must hold the kept set plus one half-tile of appends (128)
+    // between compactions, else it compacts on every tile
+    int64_t C = C0 << (ctx->opt_slack + cshift);
     const int64_t rows_per_split = per * tc::BN / 2;  // per column half
     const int64_t cap = vs_internal::pow2ceil(rows_per_split + 64);
     *exhaustive = C >= cap;
