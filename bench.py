@@ -387,7 +387,21 @@ class ExactWorkload:
         gi, gd, gc = all_gather_topk(*self.out_dev)
         return gpu_merge(gi, gd, gc, self.k, "squared_l2")
 
+    def _two_phase(self, q, bits):
+        """Row shards with the two-phase protocol (distributed.two_phase_search):
+        one all-reduce of the shard-local k-th keys, phase B on each shard's
+        candidates under the global bound, all-gather + merge kernel."""
+        from paper_2605_15957_b200.distributed import ShardSearch, TorchComm, two_phase_search
+        if not hasattr(self, "_shard"):
+            self._shard = ShardSearch(self.col)
+            self._comm = TorchComm()
+        return two_phase_search(self._shard, self._comm, q, self.k, "squared_l2", row_filter=bits,
+                                id_offset=self.lo)
+
     def step_device(self):
+        if self.sharded and not self.cfg.get("host"):
+            self.out_dev = self._two_phase(self.queries, self.bits)
+            return
         self._search(self.queries, self.bits, self.out_dev)
         if self.sharded:
             self._exchange()
@@ -396,13 +410,21 @@ class ExactWorkload:
         if not self.sharded:
             self._search(self.q_host, self.bits_host, self.out_host)
             return
+        if not self.cfg.get("host"):
+            # host queries and bitmap in; the global result back to the host
+            q = self.q_host.to(self.dev, non_blocking=True)
+            b = self.bits_host.to(self.dev, non_blocking=True)
+            for h, t in zip(self.out_host, self._two_phase(q, b)):
+                h.copy_(t)
+            return
         self._search(self.q_host, self.bits_host, self.out_dev)
         for h, t in zip(self.out_host, self._exchange()):
             h.copy_(t)
 
     def check(self):
         ids, dd, cc = self.out_dev
-        assert int(cc.min()) == min(self.k, self.n_sel), "short result rows"
+        n_sel = self.n_sel_total if self.sharded else self.n_sel
+        assert int(cc.min()) == min(self.k, n_sel), "short result rows"
         assert bool((dd[:, 1:] >= dd[:, :-1]).all()), "distances not sorted"
 
     def io_bytes(self):
@@ -444,7 +466,8 @@ class ExactWorkload:
     def config(self):
         c = self.cfg
         par = ("replicas x%d (query batches independent)" % self.world if self.replicas else
-               f"row-shard x{self.world} + allgather/merge") if self.world > 1 else "single GPU"
+               f"row-shard x{self.world}: two-phase (all-reduce MIN of shard k-th keys, bounded "
+               f"re-rank) + all-gather/merge kernel") if self.world > 1 else "single GPU"
         if c.get("host"):
             par = f"{self.world} of {c['shards']} row shards (one per GPU), host-resident, allgather/merge"
         n_rows = c["n"] // c["shards"] * self.world if c.get("host") else c["n"]

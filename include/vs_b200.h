@@ -138,6 +138,27 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data,
                   int64_t* out_ids, double* out_dist, int32_t* out_count,
                   int64_t* out_visited);
 
+/* ---- two-phase exact search of one row shard (multi-GPU) -----
+ * begin: selection + phase A (tensor cores) on this shard, and out_keys
+ * [nq][k] = the shard's k smallest approximate keys (ascending, +inf padded).
+ * The caller all-gathers the keys of every shard and takes T = the k-th
+ * smallest of their union (vs_union_kth): the global k-th approximate key.
+ * finish(T): phase B re-ranks only candidates with key <= T + margin, so the
+ * exact float64 work is split across the shards instead of repeated on each;
+ * returns the shard's rows (possibly fewer than k) and out_bound[q]: every
+ * candidate this shard dropped in phase A has exact key (distance; -score
+ * for inner product) above it. After the all-gather + merge, queries whose
+ * merged k-th key is not below the MIN over shards of out_bound are re-run
+ * with vs_enn_search (distributed.py). */
+int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries, int64_t nq,
+                        int32_t d, const uint32_t* bitmap, int64_t nbits, int32_t k,
+                        int32_t metric, float* out_keys, int64_t* out_visited);
+/* [nparts][nq][k] sorted key lists -> out[nq] = k-th smallest of their union */
+int vs_union_kth(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k, const float* keys, float* out);
+int vs_enn_search_finish(vs_ctx* ctx, const float* thresholds, int64_t id_offset,
+                         int64_t* out_ids, double* out_dist, int32_t* out_count,
+                         double* out_bound);
+
 /* ---- cross-shard merge (multi-GPU exchange step) --------------
  * ids/dist: [nparts, nq, k_in], counts: [nparts, nq]; writes the global
  * top-k under the tie rule. Inputs are per-shard outputs of the searches. */

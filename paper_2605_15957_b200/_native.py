@@ -51,6 +51,10 @@ SIGNATURES = {
     "vs_column_info": (C.c_int, [_vp, _vp, _vp, _vp]),
     "vs_enn_search": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i64,
                                 _vp, _vp, _vp, C.POINTER(_i64)]),
+    "vs_enn_search_begin": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _vp,
+                                      C.POINTER(_i64)]),
+    "vs_enn_search_finish": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "vs_union_kth": (C.c_int, [_vp, _i32, _i64, _i32, _vp, _vp]),
     "vs_topk_merge": (C.c_int, [_vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _i32,
                                 _vp, _vp, _vp]),
     "vs_ivf_create": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp,

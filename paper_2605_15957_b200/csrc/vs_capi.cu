@@ -6,11 +6,13 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/vs_b200.h"
@@ -153,10 +155,23 @@ int scatter_rows(vs_ctx* ctx, const T* src, const int32_t* idx, int64_t n, int w
 
 int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force);
 
-// phase A + phase B for the rows [0, nsel) of one job, then re-run overflowed
-// queries with 4x larger candidate buffers (cshift + 2) until none remain.
-int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force) {
-    if (job.nq == 0) return VS_OK;
+// phase A result kept between the two halves of a search
+struct PhaseA {
+    vs::EnnScanParams sp;
+    bool exhaustive = false;
+};
+
+// hooks of the distributed protocol (vs_enn_search_begin/finish): all nullable
+struct PhaseBHooks {
+    const float* ext_thr = nullptr;   // [nq] global upper bound on the k-th approximate key
+    double* out_bound = nullptr;      // [nq] deferred verification bound (key space)
+    float* out_kth = nullptr;         // [nq] k-th approximate key only (no re-rank)
+};
+
+int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bool allow_force,
+                const PhaseBHooks& hk);
+
+int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, PhaseA* st) {
     vs::EnnScanParams sp;
     sp.Q = job.q;
     sp.nq = job.nq;
@@ -206,11 +221,28 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
             else CK(vs::launch_enn_scan_simt<__nv_bfloat16>(sp, ctx->stream));
         }
     }
-    const bool used_tc = use_tc;
-    const vs::CandBuf cb = sp.cb;
-    ctx->stats[VS_STAT_LAST_ENN_KERNEL] = used_tc ? 2 : 1;
+    ctx->stats[VS_STAT_LAST_ENN_KERNEL] = use_tc ? 2 : 1;
     ctx->stats[VS_STAT_LAUNCHES] += 1;
+    st->sp = sp;
+    st->exhaustive = exhaustive;
+    return VS_OK;
+}
 
+// phase A + phase B for the rows [0, nsel) of one job, then re-run overflowed
+// queries with 4x larger candidate buffers (cshift + 2) until none remain.
+int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force) {
+    if (job.nq == 0) return VS_OK;
+    PhaseA st;
+    CKS(enn_phase_a(ctx, job, margin, cshift, &st));
+    return enn_phase_b(ctx, job, st, cshift, allow_force, PhaseBHooks{});
+}
+
+int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bool allow_force,
+                const PhaseBHooks& hk) {
+    const vs::EnnScanParams& sp = st.sp;
+    const bool exhaustive = st.exhaustive;
+    const float* margin = sp.margin;
+    const vs::CandBuf cb = sp.cb;
     vs::RerankParams rp;
     rp.Q = job.q;
     rp.nq = job.nq;
@@ -240,12 +272,16 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     CKS(arena_alloc(ctx, 1, &d_surv));
     CK(cudaMemsetAsync(d_surv, 0, sizeof(unsigned long long), ctx->stream));
     rp.n_survivors = d_surv;
+    rp.ext_thr = hk.ext_thr;
+    rp.out_bound = hk.out_bound;
+    rp.out_kth = hk.out_kth;
     {
         KTimer kt(ctx, job.cls_rerank);
         if (job.dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
         else CK(vs::launch_rerank<__nv_bfloat16>(rp, ctx->stream));
     }
     ctx->stats[VS_STAT_LAUNCHES] += 1;
+    if (hk.out_kth) return VS_OK;   // k-th keys only: phase B proper comes later
 
     unsigned long long h_surv = 0;
     CK(cudaMemcpyAsync(&h_surv, d_surv, sizeof(h_surv), cudaMemcpyDeviceToHost, ctx->stream));
@@ -293,6 +329,16 @@ int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, boo
     CKS(scatter_rows(ctx, sub.out_dist, d_idx, m, k, job.out_dist));
     CKS(scatter_rows(ctx, sub.out_ids32, d_idx, m, k, job.out_ids32));
     CKS(scatter_rows(ctx, sub.out_count, d_idx, m, 1, job.out_count));
+    if (hk.out_bound) {
+        // re-runs keep every candidate in the margin band: their local result is
+        // complete, no bound on the other shards' results
+        double* inf = nullptr;
+        CKS(arena_alloc(ctx, (size_t)m, &inf));
+        std::vector<double> h_inf(m, std::numeric_limits<double>::infinity());
+        CK(cudaMemcpyAsync(inf, h_inf.data(), m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CKS(scatter_rows(ctx, inf, d_idx, m, 1, hk.out_bound));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     return VS_OK;
 }
 
@@ -722,6 +768,164 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     } else {
         CKS(run_enn(ctx, job, margin, 0, true));
     }
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
+// ---- two-phase exact search for row-sharded collections --------------------------
+// begin: phase A on this shard + the shard-local k-th approximate key per
+// query; the caller all-reduces (MIN) those keys into a global bound T; finish:
+// phase B re-ranks only the candidates with key <= min(K*, T) + margin, so the
+// exact work per shard shrinks with the number of shards. out_bound returns,
+// per query, a value below which no dropped candidate of this shard lies
+// (key space: distance, or -score); the merged k-th key must stay below the
+// MIN over shards of out_bound, else the query is re-run (distributed.py).
+}  // extern "C"
+namespace {
+struct PendingEnn {
+    EnnJob job;
+    PhaseA st;
+    bool active = false;
+};
+std::unordered_map<const vs_ctx*, PendingEnn>& pending_map() {
+    static std::unordered_map<const vs_ctx*, PendingEnn> m;
+    return m;
+}
+}  // namespace
+extern "C" {
+
+int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries, int64_t nq, int32_t d,
+                        const uint32_t* bitmap, int64_t nbits, int32_t k, int32_t metric, float* out_kth,
+                        int64_t* out_visited) {
+    if (!ctx || !data) return set_err(VS_ERR_PARAMETER, "null argument");
+    CKS(validate_metric(metric));
+    CKS(validate_k(k));
+    if (d != data->d) return set_err(VS_ERR_SHAPE, "query dim %d != data dim %d", d, data->d);
+    if (nq < 0) return set_err(VS_ERR_PARAMETER, "negative query count");
+    if (data->host_resident) return set_err(VS_ERR_PARAMETER, "two-phase search needs a device-resident shard");
+    if (bitmap && nbits != data->n)
+        return set_err(VS_ERR_SHAPE, "bitmap covers %lld rows, column has %lld", (long long)nbits,
+                       (long long)data->n);
+    DevGuard g(ctx->device);
+    vs_column* col = const_cast<vs_column*>(data);
+    CK(ctx->arena.reset());
+    PendingEnn& pe = pending_map()[ctx];
+    pe.active = false;
+    std::vector<OutBuf> pending;
+    const float* dq = nullptr;
+    CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+    int64_t* sel = nullptr;
+    int64_t nsel = data->n;
+    if (bitmap) {
+        const uint32_t* dbm = nullptr;
+        CKS(stage_in(ctx, bitmap, (size_t)(nbits + 31) / 32, &dbm));
+        CKS(build_selection(ctx, dbm, nbits, &sel, &nsel));
+    }
+    if (out_visited) *out_visited = nq * nsel;
+    EnnJob& job = pe.job;
+    job = EnnJob{};
+    job.q = dq;
+    job.nq = nq;
+    job.d = d;
+    job.rows = col->data;
+    job.dtype = col->dtype;
+    job.sel = sel;
+    job.nsel = nsel;
+    job.ip = metric;
+    job.k = k;
+    job.id_offset = 0;
+    if (nq == 0 || nsel == 0) {   // an empty shard: no candidates, no bound
+        float* dk = nullptr;
+        CKS(stage_out(ctx, out_kth, (size_t)nq * k, &dk, pending));
+        if (dk && nq) {
+            std::vector<float> inf((size_t)nq * k, std::numeric_limits<float>::infinity());
+            CK(cudaMemcpyAsync(dk, inf.data(), inf.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        CKS(flush_out(ctx, pending));
+        pe.active = true;
+        return VS_OK;
+    }
+    CKS(ensure_norms(col));
+    job.xnorm = col->norms;
+    job.xmax = col->max_norm_bits;
+    float* margin = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq, &margin));
+    CK(vs::launch_query_margins(dq, nq, d, col->max_norm_bits, eps_simt(d), metric, margin, nullptr,
+                                ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    CKS(enn_phase_a(ctx, job, margin, 0, &pe.st));
+    float* dk = nullptr;
+    CKS(stage_out(ctx, out_kth, (size_t)nq * k, &dk, pending));
+    if (!dk) CKS(arena_alloc(ctx, (size_t)nq * k, &dk));
+    PhaseBHooks hk;
+    hk.out_kth = dk;
+    CKS(enn_phase_b(ctx, job, pe.st, 0, false, hk));
+    CKS(flush_out(ctx, pending));
+    pe.active = true;
+    return VS_OK;
+}
+
+int vs_union_kth(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k, const float* keys, float* out) {
+    if (!ctx || nparts < 1 || k < 1 || nq < 0) return set_err(VS_ERR_PARAMETER, "bad union-kth shape");
+    if ((int64_t)nparts * k > 16384) return set_err(VS_ERR_PARAMETER, "nparts * k above 16384");
+    if (nq == 0) return VS_OK;
+    DevGuard g(ctx->device);
+    // no arena reset: called between vs_enn_search_begin and _finish on the
+    // same context, whose pending state lives in the arena
+    std::vector<OutBuf> pending;
+    const float* dkeys = nullptr;
+    CKS(stage_in(ctx, keys, (size_t)nparts * nq * k, &dkeys));
+    float* dout = nullptr;
+    CKS(stage_out(ctx, out, (size_t)nq, &dout, pending));
+    CK(vs::launch_union_kth(dkeys, nparts, nq, k, dout, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
+int vs_enn_search_finish(vs_ctx* ctx, const float* thresholds, int64_t id_offset, int64_t* out_ids,
+                         double* out_dist, int32_t* out_count, double* out_bound) {
+    if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
+    auto it = pending_map().find(ctx);
+    if (it == pending_map().end() || !it->second.active)
+        return set_err(VS_ERR_PARAMETER, "vs_enn_search_finish without vs_enn_search_begin");
+    DevGuard g(ctx->device);
+    PendingEnn& pe = it->second;
+    pe.active = false;
+    EnnJob job = pe.job;
+    const int64_t nq = job.nq;
+    const int k = job.k;
+    std::vector<OutBuf> pending;
+    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending));
+    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
+    CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
+    double* dbound = nullptr;
+    CKS(stage_out(ctx, out_bound, (size_t)nq, &dbound, pending));
+    job.out_ids32 = nullptr;
+    job.id_offset = id_offset;
+    if (nq == 0) return VS_OK;
+    if (job.nsel == 0) {   // empty shard: empty rows, no bound
+        if (job.out_ids) CK(cudaMemsetAsync(job.out_ids, 0xff, (size_t)nq * k * sizeof(int64_t), ctx->stream));
+        if (job.out_dist) {
+            std::vector<double> nan((size_t)nq * k, std::numeric_limits<double>::quiet_NaN());
+            CK(cudaMemcpyAsync(job.out_dist, nan.data(), nan.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx->stream));
+        }
+        if (job.out_count) CK(cudaMemsetAsync(job.out_count, 0, (size_t)nq * sizeof(int32_t), ctx->stream));
+        if (dbound) {
+            std::vector<double> inf(nq, std::numeric_limits<double>::infinity());
+            CK(cudaMemcpyAsync(dbound, inf.data(), nq * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        CKS(flush_out(ctx, pending));
+        return VS_OK;
+    }
+    const float* dthr = nullptr;
+    CKS(stage_in(ctx, thresholds, (size_t)nq, &dthr));
+    if (!dbound) CKS(arena_alloc(ctx, (size_t)nq, &dbound));
+    PhaseBHooks hk;
+    hk.ext_thr = dthr;
+    hk.out_bound = dbound;
+    CKS(enn_phase_b(ctx, job, pe.st, 0, true, hk));
     CKS(flush_out(ctx, pending));
     return VS_OK;
 }

@@ -179,11 +179,20 @@ struct RerankParams {
     int32_t* out_count;         // [nq] (nullable)
     unsigned long long* n_survivors;
     LeafPlan plan;              // filled by launch_rerank
+    // distributed protocol (vs_enn_search_begin/finish), all nullable:
+    const float* ext_thr = nullptr;   // [nq] global upper bound on the k-th approximate key
+    double* out_bound = nullptr;      // [nq] deferred verification: dropped candidates have an
+                                      //      exact key (distance, or -score) above this bound
+    float* out_kth = nullptr;         // [nq][k] write this shard's k smallest approximate keys
+                                      //      (ascending, +inf padded) and stop
     int ubytes;                 // filled by launch_rerank: shared-memory union size
     int reg_path;               // filled by launch_rerank: register-resident scorer
 };
 template <typename T>
 cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s);
+
+// [G][nq][k] sorted shard key lists -> [nq] k-th smallest of their union
+cudaError_t launch_union_kth(const float* keys, int G, int64_t nq, int k, float* out, cudaStream_t s);
 
 // ---- cross-shard merge ---------------------------------------------------------------------
 struct MergeParams {

@@ -146,6 +146,49 @@ __device__ __forceinline__ void emit_row(int64_t q, int k, int keff, const uint6
     if (threadIdx.x == 0 && out_count) out_count[q] = keff;
 }
 
+// bitonic sort of P (power of two) orderable keys in shared memory, ascending
+__device__ void bitonic_sort_u32(uint32_t* key, int P) {
+    const int tid = threadIdx.x;
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < P / 2; i += NT) {
+                const int lo_i = 2 * i - (i & (stride - 1));
+                const int hi_i = lo_i + stride;
+                const bool asc = ((lo_i & size) == 0);
+                const uint32_t ka = key[lo_i], kb = key[hi_i];
+                if ((ka > kb) == asc) {
+                    key[lo_i] = kb;
+                    key[hi_i] = ka;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// distributed protocol, phase 1: this shard's k smallest approximate keys,
+// ascending, +inf padded (keys <= kth are gathered into `a` (HBINS slots))
+template <class ForEach>
+__device__ void write_local_topk_keys(ForEach foreach, uint32_t kth, int k, unsigned* a, Small& sm, float* out) {
+    const int tid = threadIdx.x;
+    if (tid == 0) sm.counter = 0;
+    __syncthreads();
+    foreach([&](uint32_t o) {
+        if (o <= kth) {
+            const int slot = atomicAdd(&sm.counter, 1);
+            if (slot < HBINS) a[slot] = o;
+        }
+    });
+    __syncthreads();
+    const int c = min(sm.counter, HBINS);
+    int P = 1;
+    while (P < c) P <<= 1;
+    for (int i = c + tid; i < P; i += NT) a[i] = 0xffffffffu;
+    __syncthreads();
+    bitonic_sort_u32(a, P);
+    for (int i = tid; i < k; i += NT) out[i] = i < c ? o2f(a[i]) : __int_as_float(0x7f800000);
+}
+
 // bitonic sort of P (power of two) (key, id) pairs in shared memory
 __device__ void bitonic_sort(uint64_t* key, int64_t* id, int P) {
     const int tid = threadIdx.x;
@@ -561,7 +604,11 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     const uint32_t tg = p.tau_g ? p.tau_g[q] : 0xffffffffu;
     // verify mode: tau_g is the smallest local k-th key, an upper bound on the
     // global one; survivors need key <= K* + margin <= tau_g + margin
-    const uint32_t pre = (p.verify && tg != 0xffffffffu) ? f2o(__fadd_ru(o2f(tg), p.margin[q])) : tg;
+    uint32_t pre = (p.verify && tg != 0xffffffffu) ? f2o(__fadd_ru(o2f(tg), p.margin[q])) : tg;
+    // distributed protocol: the global bound T on the k-th key (the smallest
+    // shard-local k-th); survivors need key <= min(K*, T) + margin
+    const uint32_t ext_o = p.ext_thr ? f2o(p.ext_thr[q]) : 0xffffffffu;
+    if (p.ext_thr && ext_o != f2o(__int_as_float(0x7f800000))) pre = min(pre, f2o(__fadd_ru(p.ext_thr[q], p.margin[q])));
 
     RR_MARK(0);
     // 0. live candidates -> shared memory (one warp per buffer, coalesced)
@@ -612,14 +659,24 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
         RR_MARK(1);
         // 1. k-th smallest approximate key  2. survivors (shared-memory path)
         uint32_t thr_o = 0xffffffffu;
-        if (nl > p.k) {
-            const uint32_t kth = block_radix_kth(
+        uint32_t kth = 0xffffffffu;
+        if (nl >= p.k && (nl > p.k || p.out_kth)) {
+            kth = block_radix_kth(
                 [&](auto fn) {
                     for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
                 },
                 (unsigned)p.k, hist, sm);
-            thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
         }
+        if (p.out_kth) {   // this shard's k smallest approximate keys (+inf padded)
+            write_local_topk_keys(
+                [&](auto fn) {
+                    for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
+                },
+                kth, p.k, hist, sm, p.out_kth + q * (int64_t)p.k);
+            return;
+        }
+        if (p.ext_thr) kth = min(kth, ext_o);
+        if (kth != 0xffffffffu && (nl > p.k || p.ext_thr)) thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
         if (tid == 0) sm.counter = 0;
         __syncthreads();
         for (int i = tid; i < nl; i += NT) {
@@ -635,7 +692,7 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
         uint32_t thr_o = 0xffffffffu;
         if (tot > p.k) {
             // nl > LCAP >= k live keys (key <= pre): their k-th smallest
-            const uint32_t kth = block_radix_kth(
+            uint32_t kth = block_radix_kth(
                 [&](auto fn) {
                     for (int s = w; s < nsub; s += NWARP)
                         for (int j = lane; j < cnts[s]; j += 32) {
@@ -644,6 +701,19 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
                         }
                 },
                 (unsigned)p.k, hist, sm);
+            if (p.out_kth) {
+                write_local_topk_keys(
+                    [&](auto fn) {
+                        for (int s = w; s < nsub; s += NWARP)
+                            for (int j = lane; j < cnts[s]; j += 32) {
+                                const uint32_t o = f2o(ckey[(int64_t)s * C + j]);
+                                if (o <= pre) fn(o);
+                            }
+                    },
+                    kth, p.k, hist, sm, p.out_kth + q * (int64_t)p.k);
+                return;
+            }
+            if (p.ext_thr) kth = min(kth, ext_o);
             thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
         }
         if (tid == 0) sm.counter = 0;
@@ -803,7 +873,7 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     // 5. verification of the local-top-k pass: every dropped candidate e had
     //    approx key > tau_g, hence exact key > tau_g - margin/2; the result is
     //    exact iff the k-th exact key + margin/2 < tau_g. Otherwise re-run.
-    if (p.verify && tg != 0xffffffffu && w == 0) {
+    if ((p.verify || p.out_bound) && w == 0) {
         double qq = 0.0;
         if (!IP) {
             for (int i = lane; i < d; i += 32) {
@@ -814,15 +884,40 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
             for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(VS_FULL, qq, o);
         }
         if (lane == 0) {
-            const int keff = (int)min((int64_t)p.k, ns);
-            const uint64_t* sk = reinterpret_cast<const uint64_t*>(u);  // sorted keys left by the top-k
-            double kth = keff > 0 ? o2d(sk[keff - 1]) : 0.0;             // exact key (-score for IP)
-            if (!IP) kth -= qq * (1.0 + 1e-12);  // approx keys omit ||q||^2
-            const double bound = (double)o2f(tg) - 0.5 * (double)p.margin[q];
+            const bool has_bound = p.verify && tg != 0xffffffffu;
+            const double bound = has_bound ? (double)o2f(tg) - 0.5 * (double)p.margin[q] : 0.0;
             const double slack = fabs(bound) * 1e-6 + 1e-12;
-            if (keff < p.k || !(kth < bound - slack)) p.cb.overflow[q] = 1;
+            if (p.out_bound) {
+                // deferred (distributed) check, in key space with ||q||^2 restored:
+                // every dropped candidate has exact key > this value
+                p.out_bound[q] = has_bound ? bound - slack + (IP ? 0.0 : qq * (1.0 - 1e-12))
+                                           : __longlong_as_double(0x7ff0000000000000ll);
+            } else if (has_bound) {
+                const int keff = (int)min((int64_t)p.k, ns);
+                const uint64_t* sk = reinterpret_cast<const uint64_t*>(u);  // sorted keys left by the top-k
+                double kth = keff > 0 ? o2d(sk[keff - 1]) : 0.0;             // exact key (-score for IP)
+                if (!IP) kth -= qq * (1.0 + 1e-12);  // approx keys omit ||q||^2
+                if (keff < p.k || !(kth < bound - slack)) p.cb.overflow[q] = 1;
+            }
         }
     }
+}
+
+// k-th smallest of the union of G sorted key lists per query (distributed
+// protocol: the exact global k-th approximate key from every shard's local
+// top-k keys): [G][nq][k] -> [nq]
+__global__ void __launch_bounds__(NT) k_union_kth(const float* __restrict__ keys, int G, int64_t nq, int k,
+                                                  float* __restrict__ out) {
+    extern __shared__ unsigned ukeys[];
+    const int64_t q = blockIdx.x;
+    const int n = G * k;
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += NT)
+        ukeys[i] = i < n ? f2o(keys[((int64_t)(i / k) * nq + q) * k + (i % k)]) : 0xffffffffu;
+    __syncthreads();
+    bitonic_sort_u32(ukeys, P);
+    if (threadIdx.x == 0) out[q] = o2f(ukeys[k - 1]);
 }
 
 static size_t rerank_smem(int d, int nsub) {
@@ -861,6 +956,17 @@ extern "C" int vs_debug_rerank_profile(unsigned long long* out, int reset) {
     return 0;
 }
 #endif
+cudaError_t launch_union_kth(const float* keys, int G, int64_t nq, int k, float* out, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    int P = 1;
+    while (P < G * k) P <<= 1;
+    const size_t smem = (size_t)P * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_union_kth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_union_kth<<<(unsigned)nq, NT, smem, s>>>(keys, G, nq, k, out);
+    return cudaGetLastError();
+}
+
 template cudaError_t launch_rerank<float>(const RerankParams&, cudaStream_t);
 template cudaError_t launch_rerank<__nv_bfloat16>(const RerankParams&, cudaStream_t);
 

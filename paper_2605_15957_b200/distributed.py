@@ -104,3 +104,166 @@ def sharded_search(local_search, k: int, metric: str, merge=None, group=None):
     gi, gd, gc = all_gather_topk(ids, dist, cnt, group)
     merge = merge or gpu_merge
     return merge(gi, gd, gc, k, metric)
+
+
+# ---- two-phase exact search over row shards ----------------------------------------------------
+#
+# Plain row sharding re-ranks every shard's full local top-k (k + margin band
+# survivors per query per shard), so the exact float64 work per GPU does not
+# shrink with the shard count. The two-phase protocol first exchanges each
+# shard's k smallest APPROXIMATE keys per query (k floats); the k-th smallest
+# of their union is exactly the global k-th approximate key K* (every key of
+# the global top-k is in its own shard's top-k), so each shard re-ranks only
+# its candidates with key <= K* + margin: the single-GPU survivor set, split
+# across the shards. Rows a shard dropped in phase A (local top-k mode) have
+# exact key > that shard's bound, which is checked against the merged k-th
+# key; a failing query is re-run with the one-phase search on every shard.
+
+
+class TorchComm:
+    """Collectives of the protocol over torch.distributed (NCCL on GPUs)."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def allreduce_min(self, t):
+        import torch.distributed as dist_
+        dist_.all_reduce(t, op=dist_.ReduceOp.MIN, group=self.group)
+        return t
+
+    def allgather(self, t):
+        import torch
+        import torch.distributed as dist_
+        world = dist_.get_world_size(self.group)
+        t = t.contiguous()
+        if dist_.get_backend(self.group) == "nccl":
+            o = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            dist_.all_gather_into_tensor(o, t, group=self.group)
+            return o
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist_.all_gather(parts, t, group=self.group)
+        return torch.stack(parts)
+
+    def allgather_topk(self, ids, dist, counts):
+        return all_gather_topk(ids, dist, counts, self.group)
+
+
+def _merged_is_exact(md, mc, bound, k: int, metric: str):
+    """Per query: the merged top-k is provably complete (torch, on device)."""
+    import torch
+    inf = torch.full_like(bound, float("inf"))
+    kidx = (mc.clamp(min=1) - 1).long().unsqueeze(1)
+    kth = md.gather(1, kidx).squeeze(1)
+    key = -kth if metric == "inner_product" else kth
+    full = mc >= k
+    ok = torch.where(full, key < bound, bound >= inf)
+    return ok
+
+
+def two_phase_search(shard, comm, queries, k: int, metric: str = "squared_l2", row_filter=None,
+                     id_offset: int = 0, merge=None):
+    """Exact filtered top-k over row shards (one call per rank, collectively).
+
+    `shard` is this rank's ShardSearch (begin / finish / plain); `comm`
+    provides allreduce_min and allgather_topk. Returns (ids, dist, counts) of
+    the global result on every rank (torch tensors on the shard's device)."""
+    import torch
+    merge = merge or gpu_merge
+    keys = shard.begin(queries, k, metric, row_filter)        # [Q, k] shard-local approx keys
+    T = shard.union_kth(comm.allgather(keys))               # [Q] global k-th approx key
+    ids, dist, cnt, bound = shard.finish(T, id_offset)
+    gi, gd, gc = comm.allgather_topk(ids, dist, cnt)
+    mi, md, mc = merge(gi, gd, gc, k, metric)
+    comm.allreduce_min(bound)
+    bad = torch.nonzero(~_merged_is_exact(md, mc, bound, k, metric)).flatten()
+    # every rank holds the same merged result and bounds: the same re-run set
+    if bad.numel():
+        sub_q = queries[bad] if hasattr(queries, "index_select") else queries[bad.cpu().numpy()]
+        ri, rd, rc = shard.plain(sub_q, k, metric, row_filter, id_offset)
+        gi, gd, gc = comm.allgather_topk(ri, rd, rc)
+        si, sd, sc = merge(gi, gd, gc, k, metric)
+        mi[bad], md[bad], mc[bad] = si, sd, sc
+    shard.reruns = int(bad.numel())
+    return mi, md, mc
+
+
+class ShardSearch:
+    """This rank's row shard for two_phase_search (vs_enn_search_begin/finish
+    through ctypes; CUDA torch tensors in and out)."""
+
+    def __init__(self, column, ctx=None):
+        from . import _native as N
+        from .vecindex import _as_column, _ctx, device_column
+        self.col = _as_column(column)
+        self.ctx = ctx or _ctx()
+        self.dc = device_column(self.col, self.ctx)
+        self.N = N
+        self.reruns = 0
+
+    def begin(self, queries, k, metric, row_filter):
+        import ctypes as C
+
+        import torch
+
+        from .vecindex import _query_buffer, _Stream, filter_bitmap
+        N = self.N
+        q, nq, d = _query_buffer(queries)
+        self._q, self._nq, self._k = q, nq, int(k)
+        self._bm = filter_bitmap(row_filter, self.col.count)
+        dev = q.device if N.is_torch(q) and q.is_cuda else torch.device("cuda", self.ctx.device)
+        self._dev = dev
+        keys = torch.empty((nq, self._k), dtype=torch.float32, device=dev)
+        vis = C.c_int64(0)
+        with _Stream(self.ctx, q, self._bm, keys):
+            N.check(N.load().vs_enn_search_begin(
+                self.ctx.handle, self.dc.handle, N.ptr(q), nq, d, N.ptr(self._bm),
+                self.col.count if self._bm is not None else 0, self._k, N.METRIC_CODE[metric],
+                N.ptr(keys), C.byref(vis)), "enn_search_begin")
+        return keys
+
+    def union_kth(self, all_keys):
+        """[G, Q, k] gathered shard keys -> [Q] k-th smallest of the union."""
+        import torch
+
+        from .vecindex import _Stream
+        N = self.N
+        G, nq, k = all_keys.shape
+        out = torch.empty(nq, dtype=torch.float32, device=all_keys.device)
+        with _Stream(self.ctx, all_keys, out):
+            N.check(N.load().vs_union_kth(self.ctx.handle, int(G), int(nq), int(k),
+                                          N.ptr(all_keys.contiguous()), N.ptr(out)), "union_kth")
+        return out
+
+    def finish(self, thresholds, id_offset):
+        import torch
+
+        from .vecindex import _Stream
+        N = self.N
+        nq, k, dev = self._nq, self._k, self._dev
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        dist = torch.empty((nq, k), dtype=torch.float64, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        bound = torch.empty((nq,), dtype=torch.float64, device=dev)
+        with _Stream(self.ctx, thresholds, ids):
+            N.check(N.load().vs_enn_search_finish(
+                self.ctx.handle, N.ptr(thresholds.contiguous()), int(id_offset), N.ptr(ids), N.ptr(dist),
+                N.ptr(cnt), N.ptr(bound)), "enn_search_finish")
+        return ids, dist, cnt, bound
+
+    def plain(self, queries, k, metric, row_filter, id_offset):
+        import torch
+
+        from .vecindex import enn_search_raw
+        nq = queries.shape[0]
+        out = (torch.empty((nq, k), dtype=torch.int64, device=self._dev),
+               torch.empty((nq, k), dtype=torch.float64, device=self._dev),
+               torch.empty((nq,), dtype=torch.int32, device=self._dev))
+        from .errors import EmptyInputError
+        try:
+            enn_search_raw(queries, self.col, k, metric, row_filter=row_filter, id_offset=id_offset,
+                           device=self.ctx, out=out)
+        except EmptyInputError:   # this shard selects no rows: it contributes nothing
+            out[0].fill_(-1)
+            out[1].fill_(float("nan"))
+            out[2].zero_()
+        return out

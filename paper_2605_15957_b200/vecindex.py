@@ -112,6 +112,8 @@ _dev_cols = weakref.WeakKeyDictionary()  # duck-typed (reference) columns -> {de
 
 
 def _ctx(device=None) -> N.Context:
+    if isinstance(device, N.Context):   # an explicit context (several per device are allowed)
+        return device
     return N.Context.get(device)
 
 

@@ -100,3 +100,90 @@ def test_world2_exchange_matches_unsharded():
     m = np.arange(25)[None, :] < cnt[:, None]
     assert np.array_equal(ids[m], ref.data_row)
     assert np.array_equal(dd[m], ref.distance)
+
+
+class _OracleShard:
+    """CPU stand-in for ShardSearch: phase A keys are the exact float64 keys
+    (margin 0), so the protocol's choreography is what is tested here."""
+
+    def __init__(self, data, mask, lo, hi, pessimist=False):
+        self.data, self.mask, self.lo, self.hi, self.pessimist = data, mask, lo, hi, pessimist
+        self.reruns = 0
+
+    def _scores(self, q):
+        rows = self.lo + np.flatnonzero(self.mask[self.lo:self.hi])
+        return rows, (O.pairwise(q, self.data[rows]) if rows.size else np.zeros((len(q), 0)))
+
+    def begin(self, q, k, metric, row_filter):
+        self.q, self.k = q, k
+        rows, s = self._scores(q)
+        keys = np.full((len(q), k), np.inf, np.float32)
+        if rows.size:
+            srt = np.sort(s, axis=1)[:, :k].astype(np.float32)
+            keys[:, :srt.shape[1]] = srt
+        return torch.from_numpy(keys)
+
+    def union_kth(self, all_keys):
+        G, nq, k = all_keys.shape
+        u = all_keys.permute(1, 0, 2).reshape(nq, G * k)
+        return torch.sort(u, dim=1).values[:, k - 1]
+
+    def finish(self, thr, id_offset):
+        rows, s = self._scores(self.q)
+        nq, k = len(self.q), self.k
+        ids = torch.full((nq, k), -1, dtype=torch.int64)
+        dd = torch.full((nq, k), float("nan"), dtype=torch.float64)
+        cnt = torch.zeros(nq, dtype=torch.int32)
+        for i in range(nq):
+            keep = s[i] <= float(thr[i]) * (1 + 1e-6) + 1e-6
+            if keep.any():
+                top = O.select_top(s[i][keep], rows[keep], min(k, int(keep.sum())), "squared_l2")
+                r_ = rows[keep][top]
+                ids[i, :len(r_)] = torch.from_numpy(r_)
+                dd[i, :len(r_)] = torch.from_numpy(s[i][keep][top])
+                cnt[i] = len(r_)
+        bound = torch.full((nq,), -1e30 if self.pessimist else float("inf"), dtype=torch.float64)
+        return ids, dd, cnt, bound
+
+    def plain(self, q, k, metric, row_filter, id_offset):
+        rows = self.lo + np.flatnonzero(self.mask[self.lo:self.hi])
+        res = O.enn_search(np.asarray(q), self.data[rows], k, row_ids=rows)
+        return _padded(res, len(q), k)
+
+
+def _worker_two_phase(rank, world, port, out):
+    from paper_2605_15957_b200.distributed import TorchComm, two_phase_search
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(1)
+    data = rng.standard_normal((2400, 16)).astype(np.float32)
+    q = rng.standard_normal((9, 16)).astype(np.float32)
+    mask = rng.random(2400) < 0.5
+    lo, hi = row_shard(2400, rank, world)
+    for pess in (False, True):
+        shard = _OracleShard(data, mask, lo, hi, pessimist=pess)
+        mi, md, mc = two_phase_search(shard, TorchComm(), torch.from_numpy(q), 20, "squared_l2",
+                                      id_offset=lo, merge=_oracle_merge)
+        if rank == 0:
+            out[f"tp{int(pess)}"] = (mi.numpy(), md.numpy(), mc.numpy(), shard.reruns)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_world3_two_phase_protocol_matches_unsharded():
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker_two_phase, args=(3, port, out), nprocs=3, join=True)
+        res = dict(out)
+    rng = np.random.default_rng(1)
+    data = rng.standard_normal((2400, 16)).astype(np.float32)
+    q = rng.standard_normal((9, 16)).astype(np.float32)
+    mask = rng.random(2400) < 0.5
+    ref = O.enn_filtered(q, data, mask, 20)
+    for key, reruns in (("tp0", 0), ("tp1", 9)):
+        ids, dd, cnt, rr = res[key]
+        m = np.arange(20)[None, :] < cnt[:, None]
+        assert np.array_equal(ids[m], ref.data_row)
+        assert np.array_equal(dd[m], ref.distance)
+        assert rr == reruns

@@ -1,0 +1,132 @@
+"""Two-phase exact search over row shards (distributed.two_phase_search,
+vs_enn_search_begin/finish): G shards emulated on one GPU by G library
+contexts driven from G threads with in-process collectives. The merged result
+must equal the unsharded search bit for bit (ids, float64 distances), which
+itself equals the reference composition."""
+
+import threading
+from functools import partial
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_15957_b200 as vs
+from oracle import sqlvs_oracle as O
+from paper_2605_15957_b200 import _native as N
+from paper_2605_15957_b200.distributed import ShardSearch, gpu_merge, row_shard, two_phase_search
+
+pytestmark = pytest.mark.gpu
+
+
+class ThreadComm:
+    """allreduce(MIN) / all-gather between threads of one process."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+    def rank(self, r):
+        comm = self
+
+        class _R:
+            def allreduce_min(self, t):
+                comm.slots[r] = t.clone()
+                comm.barrier.wait()
+                m = torch.stack(comm.slots).min(0).values
+                comm.barrier.wait()
+                t.copy_(m)
+                return t
+
+            def allgather(self, t):
+                comm.slots[r] = t
+                comm.barrier.wait()
+                out = torch.stack(list(comm.slots))
+                comm.barrier.wait()
+                return out
+
+            def allgather_topk(self, ids, dist, cnt):
+                comm.slots[r] = (ids, dist, cnt)
+                comm.barrier.wait()
+                out = tuple(torch.stack([s[j] for s in comm.slots]) for j in range(3))
+                comm.barrier.wait()
+                return out
+
+        return _R()
+
+
+def _run(world, data, q, mask, k, metric, shard_cls=ShardSearch):
+    n = data.shape[0]
+    xd = torch.from_numpy(data).cuda()
+    qd = torch.from_numpy(q).cuda()
+    comm = ThreadComm(world)
+    results, shards, errors = [None] * world, [None] * world, []
+
+    def rank(r):
+        try:
+            lo, hi = row_shard(n, r, world)
+            ctx = N.Context(0)
+            shard = shard_cls(vs.EmbeddingColumn.from_device(xd[lo:hi].contiguous()), ctx)
+            shards[r] = shard
+            results[r] = two_phase_search(shard, comm.rank(r), qd, k, metric,
+                                          row_filter=None if mask is None else mask[lo:hi],
+                                          id_offset=lo, merge=partial(gpu_merge, device=ctx))
+            torch.cuda.synchronize()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+            comm.barrier.abort()
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errors:
+        raise errors[0]
+    return results, shards
+
+
+def _flat(res):
+    ids, dist, cnt = (t.cpu().numpy() for t in res)
+    m = np.arange(ids.shape[1])[None, :] < cnt[:, None]
+    return ids[m], dist[m], cnt
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+def test_two_phase_equals_unsharded(world, metric):
+    rng = np.random.default_rng(world * 10 + (metric == "inner_product"))
+    n, d, k = 40000, 128, 50
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((300, d)).astype(np.float32)   # >= 256: tensor-core phase A
+    mask = rng.random(n) < 0.4
+    results, shards = _run(world, data, q, mask, k, metric)
+    whole = vs.enn_search(q, data, vs.SearchParams(k=k), metric=metric, row_filter=mask)
+    for r in range(world):
+        ids, dist, _ = _flat(results[r])
+        assert np.array_equal(ids, whole.data_row)
+        assert np.array_equal(dist, whole.distance)
+
+
+def test_two_phase_rerun_path_and_empty_shard():
+    rng = np.random.default_rng(5)
+    n, d, k = 20000, 64, 30
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((280, d)).astype(np.float32)
+    mask = rng.random(n) < 0.5
+    mask[: n // 3] = False                   # shard 0 of 3 selects nothing
+
+    class Pessimist(ShardSearch):            # bounds below every key: every query re-runs
+        def finish(self, thresholds, id_offset):
+            ids, dist, cnt, bound = super().finish(thresholds, id_offset)
+            return ids, dist, cnt, torch.full_like(bound, -1e30)
+
+    for cls in (ShardSearch, Pessimist):
+        results, shards = _run(3, data, q, mask, k, "squared_l2", cls)
+        ref = O.enn_filtered(q, data, mask, k)
+        ids, dist, _ = _flat(results[1])
+        assert np.array_equal(ids, ref.data_row)
+        assert np.array_equal(dist, ref.distance)
+        if cls is Pessimist:
+            assert shards[0].reruns == q.shape[0]
