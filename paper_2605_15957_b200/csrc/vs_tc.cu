@@ -97,6 +97,8 @@ struct Params {
     int nprobe;
     const uint32_t* pbits;          // nullable: filter bit per payload position
     int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
+    int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
+                                    // appends per thread instead of cooperatively
 };
 
 // one work item: A tile rows [a_row, a_row + QTILE), B tiles of BN rows from
@@ -630,7 +632,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // staging their 32 keys in shared memory; the warp then writes
                     // only the admitted (key, position) pairs, in column order
                     unsigned am = __ballot_sync(VS_FULL, mask != 0);
-                    if (am) {
+                    if (__popc(am) >= p.direct_lanes) {
+                        // dense admissions (short splits): every lane appends its
+                        // own keys directly (predicated, static register indices)
+                        if (p.dbg) n_app += __popc(mask);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if ((mask >> j) & 1u) {
+                                ckey[cnt] = kk[j];
+                                cpos[cnt] = (uint32_t)(r0 + cb0 + j);
+                                ++cnt;
+                            }
+                        }
+                    } else if (am) {
                         float* st = app_w[warp - EPI_WARP0];
                         if (p.dbg) n_app += __popc(mask);
                         while (am) {
@@ -1016,6 +1030,10 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     const unsigned units = (unsigned)std::min<int64_t>(items, sms);
     const unsigned grid = pair ? 2 * units : units;
     pr.argmin_out = nullptr;
+    // short splits append densely (the per-split fill is a larger share):
+    // per-thread appends there, warp-cooperative ones for long splits (measured)
+    static const int direct_env = getenv("VS_TC_DIRECT") ? atoi(getenv("VS_TC_DIRECT")) : 0;
+    pr.direct_lanes = direct_env ? direct_env : ((per >= 8 && per < 128) ? 16 : 33);
     KTimer kt_scan(ctx, timer_class);
     if (sp.ip) {
         CK((pair ? launch_tc<true, 0, true>(ma, mb, pr, grid, st) : launch_tc<true, 0, false>(ma, mb, pr, grid, st)));

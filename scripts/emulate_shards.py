@@ -59,6 +59,13 @@ def main():
             t_begin.append(timed(lambda: sh.begin(q, k, "squared_l2", sb)))
             kths.append(sh.begin(q, k, "squared_l2", sb).clone())
         T = shards[0][0].union_kth(torch.stack(kths))
+        sh0, ctx0, _, sb0, _ = shards[0]
+        ctx0.set_option(N.OPT_TIMING, 1)
+        ctx0.kernel_times(reset=True)
+        sh0.begin(q, k, "squared_l2", sb0)
+        torch.cuda.synchronize()
+        kt_begin = {c: round(v[0] / 1e6, 3) for c, v in ctx0.kernel_times(reset=True).items() if v[1]}
+        ctx0.set_option(N.OPT_TIMING, 0)
         t_finish, surv = [], []
         for (sh, ctx, col, sb, lo) in shards:
             tot = 0.0
@@ -86,7 +93,8 @@ def main():
                           "finish_ms_max": round(max(t_finish), 3),
                           "two_phase_ms_per_rank": round(max(b + f for b, f in zip(t_begin, t_finish)), 3),
                           "one_phase_ms_per_rank": round(max(t_plain), 3),
-                          "survivors_per_query_per_shard": [round(s, 1) for s in surv]}), flush=True)
+                          "survivors_per_query_per_shard": [round(s, 1) for s in surv],
+                          "begin_kernel_ms_shard0": kt_begin}), flush=True)
         del shards, kths
         torch.cuda.empty_cache()
 
