@@ -484,8 +484,37 @@ class ExactWorkload:
 
     def extras(self, ctx, N):
         st = ctx.stats()
-        return {"survivors_per_query": round(st[N.STAT_SURVIVORS] / self.nq, 2),
-                "overflow_requeries_total": int(st[N.STAT_OVERFLOW_QUERIES])}
+        ex = {"survivors_per_query": round(st[N.STAT_SURVIVORS] / self.nq, 2),
+              "overflow_requeries_total": int(st[N.STAT_OVERFLOW_QUERIES])}
+        if self.cfg["id"] == 1:
+            ex["gpu_filter_ms"] = self._gpu_filter_ms()
+        return ex
+
+    def _gpu_filter_ms(self):
+        """Config 1's relational filter built on the GPU from the raw columns:
+        isin(rv_partkey, part[p_size <= 5].p_partkey) as a packed bitmap
+        (predicate.compare + predicate.isin; checked against the host mask)."""
+        import torch
+
+        from paper_2605_15957_b200 import predicate as P
+        from paper_2605_15957_b200 import synth
+        spec = synth.Spec(sf=0.1, d_r=384, d_i=384, seed=42)
+        pk = torch.from_numpy(synth.review_partkeys(spec)[:self.cfg["n"]].astype(np.int64)).to(self.dev)
+        psize = torch.from_numpy(synth.part_sizes(spec).astype(np.int64)).to(self.dev)
+        pkeys = torch.arange(1, psize.numel() + 1, dtype=torch.int64, device=self.dev)
+
+        def run():
+            small = pkeys[torch.from_numpy(synth.unpack_bitmap(
+                P.compare(psize, "<=", 5).cpu().numpy().view(np.uint32), psize.numel())).to(self.dev)]
+            return P.isin(pk, small)
+        bits = run()
+        assert torch.equal(bits, self.bits), "GPU filter differs from the reference mask"
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(20):
+            run()
+        torch.cuda.synchronize()
+        return round((time.perf_counter() - t0) / 20 * 1e3, 3)
 
     def cpu_baseline(self, args):
         if self.cfg["id"] == 1:

@@ -214,6 +214,22 @@ int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t 
 int vs_ivf_set_owned(vs_ivf* ivf, const uint8_t* list_owned);
 int vs_ivf_free(vs_ivf* ivf);
 
+/* ---- relational filters -> packed row bitmaps (the step before the search) -
+ * Output words are the row_filter format above. valid_bits (nullable) is the
+ * column's validity bitmap: null rows never match.
+ *   vs_bitmap_compare: values[i] <op> value, vtype 0 int32 / 1 int64 /
+ *     2 float32 / 3 float64, op 0 < / 1 <= / 2 == / 3 != / 4 >= / 5 >, with
+ *     numpy's rules (eval_predicate, expr.py:568-576; NaN only satisfies !=);
+ *   vs_bitmap_isin: keys[i] occurs in set (semi join, relops.py:88-113);
+ *   vs_bitmap_combine: a & b (0), a | b (1), a & ~b (2) over nwords words. */
+enum vs_value_type { VS_VALUE_I32 = 0, VS_VALUE_I64 = 1, VS_VALUE_F32 = 2, VS_VALUE_F64 = 3 };
+int vs_bitmap_compare(vs_ctx* ctx, const void* values, int32_t vtype, int64_t n, int32_t op,
+                      double value, const uint32_t* valid_bits, uint32_t* out_bits);
+int vs_bitmap_isin(vs_ctx* ctx, const int64_t* keys, int64_t n, const uint32_t* valid_bits,
+                   const int64_t* set, int64_t nset, uint32_t* out_bits);
+int vs_bitmap_combine(vs_ctx* ctx, const uint32_t* a, const uint32_t* b, int64_t nwords,
+                      int32_t op, uint32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

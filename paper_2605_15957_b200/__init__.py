@@ -12,6 +12,7 @@ from .table import EmbeddingColumn, FieldType, Schema, Table, embedding  # noqa:
 from .vecindex import (INNER_PRODUCT, NON_OWNING, OWNING, SQUARED_L2, FlatIndex,  # noqa: F401
                        IvfIndex, NeighborTable, SearchParams, enn_search, load_index, save_index)
 from .vecsearch import VsStats, oversample_postfilter, vector_search_operator  # noqa: F401
+from . import predicate  # noqa: F401,E402
 
 __all__ = [
     "SearchParams", "NeighborTable", "enn_search", "FlatIndex", "IvfIndex", "save_index",

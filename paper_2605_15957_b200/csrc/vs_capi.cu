@@ -930,6 +930,81 @@ int vs_enn_search_finish(vs_ctx* ctx, const float* thresholds, int64_t id_offset
     return VS_OK;
 }
 
+// ---- relational filters -> packed row bitmaps ----------------------------------
+static size_t value_size(int vtype) { return vtype == 0 || vtype == 2 ? 4 : 8; }
+
+int vs_bitmap_compare(vs_ctx* ctx, const void* values, int32_t vtype, int64_t n, int32_t op, double value,
+                      const uint32_t* valid_bits, uint32_t* out_bits) {
+    if (!ctx || (!values && n > 0) || !out_bits) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (vtype < 0 || vtype > 3) return set_err(VS_ERR_PARAMETER, "unknown value type %d", vtype);
+    if (op < 0 || op > 5) return set_err(VS_ERR_PARAMETER, "unknown comparison %d", op);
+    if (n < 0) return set_err(VS_ERR_PARAMETER, "negative row count");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    const char* dv = nullptr;
+    CKS(stage_in(ctx, static_cast<const char*>(values), (size_t)n * value_size(vtype), &dv));
+    const uint32_t* dvalid = nullptr;
+    CKS(stage_in(ctx, valid_bits, (size_t)(n + 31) / 32, &dvalid));
+    uint32_t* dout = nullptr;
+    CKS(stage_out(ctx, out_bits, (size_t)(n + 31) / 32, &dout, pending));
+    {
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_bitmap_compare(dv, vtype, n, op, value, dvalid, dout, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
+int vs_bitmap_isin(vs_ctx* ctx, const int64_t* keys, int64_t n, const uint32_t* valid_bits, const int64_t* set,
+                   int64_t nset, uint32_t* out_bits) {
+    if (!ctx || (!keys && n > 0) || (!set && nset > 0) || !out_bits) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (n < 0 || nset < 0) return set_err(VS_ERR_PARAMETER, "negative size");
+    if (nset >= (int64_t(1) << 31)) return set_err(VS_ERR_PARAMETER, "set too large");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    const int64_t* dk = nullptr;
+    const int64_t* ds = nullptr;
+    const uint32_t* dvalid = nullptr;
+    CKS(stage_in(ctx, keys, (size_t)n, &dk));
+    CKS(stage_in(ctx, set, (size_t)nset, &ds));
+    CKS(stage_in(ctx, valid_bits, (size_t)(n + 31) / 32, &dvalid));
+    int64_t* sorted = nullptr;
+    CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(nset, 1), &sorted));
+    const size_t tb = vs::bitmap_isin_temp_bytes(nset);
+    char* tmp = nullptr;
+    CKS(arena_alloc(ctx, tb, &tmp));
+    uint32_t* dout = nullptr;
+    CKS(stage_out(ctx, out_bits, (size_t)(n + 31) / 32, &dout, pending));
+    {
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_bitmap_isin(dk, n, dvalid, ds, nset, sorted, tmp, tb, dout, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 2;
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
+int vs_bitmap_combine(vs_ctx* ctx, const uint32_t* a, const uint32_t* b, int64_t nwords, int32_t op,
+                      uint32_t* out) {
+    if (!ctx || ((!a || !b || !out) && nwords > 0)) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (op < 0 || op > 2) return set_err(VS_ERR_PARAMETER, "unknown bitmap op %d", op);
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    const uint32_t *da = nullptr, *db = nullptr;
+    CKS(stage_in(ctx, a, (size_t)nwords, &da));
+    CKS(stage_in(ctx, b, (size_t)nwords, &db));
+    uint32_t* dout = nullptr;
+    CKS(stage_out(ctx, out, (size_t)nwords, &dout, pending));
+    CK(vs::launch_bitmap_combine(da, db, nwords, op, dout, ctx->stream));
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    CKS(flush_out(ctx, pending));
+    return VS_OK;
+}
+
 int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in, const int64_t* ids,
                   const double* dist, const int32_t* counts, int32_t k, int32_t metric,
                   int64_t* out_ids, double* out_dist, int32_t* out_count) {

@@ -222,4 +222,16 @@ cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe, 
                                  const uint8_t* list_owned, const uint32_t* pbits, int32_t* sel_scratch,
                                  unsigned long long* visited, cudaStream_t s);
 
+// ---- relational filters -> packed bitmaps (vs_predicate.cu) ------------------------------
+// vtype: 0 int32, 1 int64, 2 float32, 3 float64; op: 0 <, 1 <=, 2 ==, 3 !=, 4 >=, 5 >
+cudaError_t launch_bitmap_compare(const void* values, int vtype, int64_t n, int op, double value,
+                                  const uint32_t* valid, uint32_t* out, cudaStream_t s);
+size_t bitmap_isin_temp_bytes(int64_t nset);
+cudaError_t launch_bitmap_isin(const int64_t* keys, int64_t n, const uint32_t* valid, const int64_t* set,
+                               int64_t nset, int64_t* sorted_set, void* tmp, size_t tmp_bytes, uint32_t* out,
+                               cudaStream_t s);
+// op: 0 and, 1 or, 2 and-not
+cudaError_t launch_bitmap_combine(const uint32_t* a, const uint32_t* b, int64_t nwords, int op, uint32_t* out,
+                                  cudaStream_t s);
+
 }  // namespace vs
