@@ -33,9 +33,12 @@
 namespace vs {
 
 namespace tc {
+#ifndef VS_TC_BN
+#define VS_TC_BN 256
+#endif
 
 constexpr int BM = 128;                 // queries per tile (UMMA M)
-constexpr int BN = 256;                 // rows per tile (UMMA N)
+constexpr int BN = VS_TC_BN;            // rows per tile (UMMA N)
 constexpr int BK = 64;                  // bf16 elements per stage = 128 B (swizzle atom)
 constexpr int UK = 16;                  // UMMA K for kind::f16
 constexpr int A_BYTES = BM * BK * 2;    // 16 KB
@@ -46,22 +49,23 @@ struct Cfg {
     static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
     static constexpr int B_BYTES = B_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int NSTAGE = PAIR ? 6 : 4;
+    static constexpr int NSTAGE = 196608 / STAGE_BYTES;   // the ring fills 192 KB of shared memory
     static constexpr int QTILE = PAIR ? 2 * BM : BM;   // queries per work item
 };
-constexpr int MAX_STAGES = 6;
+constexpr int MAX_STAGES = 8;
 constexpr int PF_BOXES = 0;             // MODE 2: L2 prefetch distance in B boxes (0: off, measured best)
 constexpr int NTHREADS = 384;           // 12 warps
 constexpr int EPI_WARP0 = 4;            // warps 4..11 drain TMEM (2 per lane quadrant)
 constexpr int EPI_THREADS = 256;
-constexpr int TMEM_COLS = 512;          // 2 accumulators x 256 fp32 columns
+constexpr int TMEM_COLS = 512;          // NACC accumulators x BN fp32 columns
+constexpr int NACC = TMEM_COLS / BN;    // TMEM accumulator ring depth
 
 struct Smem {
     // stage buffers live at the 1024-aligned start of dynamic smem
     uint64_t full[MAX_STAGES];
     uint64_t empty[MAX_STAGES];
-    uint64_t tfull[2];
-    uint64_t tempty[2];
+    uint64_t tfull[NACC];
+    uint64_t tempty[NACC];
     uint32_t tmem_base;
 };
 template <bool PAIR>
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&S.full[i], 1);
             mbar_init(&S.empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NACC; ++i) {
             mbar_init(&S.tfull[i], 1);
             mbar_init(&S.tempty[i], PAIR ? 2 * EPI_THREADS : EPI_THREADS);
         }
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int64_t it = unit; it < nitems; it += nunits) {
                 const Item item = decode_item<MODE, QTILE>(p, it);
                 for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
-                    const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
+                    const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                     long long c0 = p.dbg ? clock64() : 0;
                     mbar_wait(&S.tempty[acc], aph ^ 1);
                     if (p.dbg) w_tempty += clock64() - c0;
@@ -429,10 +433,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int64_t q = item.a_row + (int64_t)rank * BM + row;
             uint32_t best_o = 0xffffffffu, best_i = 0u;
             for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
-                const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
+                const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                 const int64_t r0 = item.b_row0 + t * BN;
                 const int ncols = (int)min((int64_t)BN, p.nsel - r0);
-                {
+                if (lane * 4 < BN / 2) {
                     const int64_t i = r0 + half * (BN / 2) + lane * 4;
                     float4 v;
                     v.x = i + 0 < p.nsel ? __ldg(p.xn + i + 0) : 0.f;
@@ -540,10 +544,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int lim = lim0;
             float tau = __int_as_float(0x7f800000);
             for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
-                const uint32_t acc = tcount & 1, aph = (tcount >> 1) & 1;
+                const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                 const int64_t r0 = item.b_row0 + t * BN;
                 const int ncols = (int)min((int64_t)BN, item.b_end - r0);
-                if (!IP) *reinterpret_cast<float4*>(xw + lane * 4) = pf;
+                if (!IP && lane * 4 < BN / 2) *reinterpret_cast<float4*>(xw + lane * 4) = pf;
                 __syncwarp();
                 if (qv) tau = fminf(tau, o2f(pf_tau));
                 {   // prefetch for the next tile of this CTA's sequence
