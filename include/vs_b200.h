@@ -212,6 +212,15 @@ int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t 
 /* list sharding: per-list 0/1 ownership mask of this shard
  * (nullable = all lists owned). Probes still use every centroid. */
 int vs_ivf_set_owned(vs_ivf* ivf, const uint8_t* list_owned);
+/* coarse quantizer only: [nq][nprobe] probed lists (the probes of vs_ivf_search) */
+int vs_ivf_probe(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                 int32_t nprobe, int32_t* out_probes);
+/* IVF search with given probes (e.g. computed by other ranks for their query
+ * slices and all-gathered): skips the coarse quantizer */
+int vs_ivf_search_probed(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                         const uint32_t* bitmap, int64_t nbits, int32_t nprobe,
+                         const int32_t* probes, int32_t k, int64_t* out_ids, double* out_dist,
+                         int32_t* out_count, int64_t* out_visited);
 int vs_ivf_free(vs_ivf* ivf);
 
 /* ---- relational filters -> packed row bitmaps (the step before the search) -

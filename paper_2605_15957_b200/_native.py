@@ -70,6 +70,9 @@ SIGNATURES = {
     "vs_ivf_search": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp,
                                 _vp, C.POINTER(_i64)]),
     "vs_ivf_set_owned": (C.c_int, [_vp, _vp]),
+    "vs_ivf_probe": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "vs_ivf_search_probed": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp,
+                                       C.POINTER(_i64)]),
     "vs_ivf_free": (C.c_int, [_vp]),
 }
 

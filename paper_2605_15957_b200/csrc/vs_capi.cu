@@ -1518,10 +1518,13 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
 
 }  // namespace
 
-extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
-                             const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
-                             int64_t* out_ids, double* out_dist, int32_t* out_count, int32_t* out_probes,
-                             int64_t* out_visited) {
+// IVF search; probes_in (nullable, [nq][nprobe]) skips the coarse quantizer
+// (multi-GPU: each rank probes a slice of the queries, the probes are
+// all-gathered); probe_only stops after the coarse quantizer.
+static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                           const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
+                           int64_t* out_ids, double* out_dist, int32_t* out_count, int32_t* out_probes,
+                           int64_t* out_visited, const int32_t* probes_in, bool probe_only) {
     if (!ctx || !ivf) return set_err(VS_ERR_PARAMETER, "null argument");
     CKS(validate_k(k));
     if (nprobe < 1) return set_err(VS_ERR_PARAMETER, "nprobe must be >= 1");
@@ -1542,6 +1545,11 @@ extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* querie
     CKS(arena_alloc(ctx, (size_t)nq, &cm));
     CK(vs::launch_query_margins(dq, nq, d, ivf->cmax, eps_simt(d), 0, cm, nullptr, ctx->stream));
     int32_t* probes = nullptr;
+    if (probes_in) {
+        const int32_t* dp = nullptr;
+        CKS(stage_in(ctx, probes_in, (size_t)nq * nprobe, &dp));
+        probes = const_cast<int32_t*>(dp);
+    } else {
     CKS(stage_out(ctx, out_probes, (size_t)nq * nprobe, &probes, pending));
     if (!probes) CKS(arena_alloc(ctx, (size_t)nq * nprobe, &probes));
     EnnJob cj;
@@ -1564,6 +1572,11 @@ extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* querie
     cj.cls_scan = VS_K_COARSE;
     cj.cls_rerank = VS_K_COARSE;
     CKS(run_enn(ctx, cj, cm, 0, false));
+    }
+    if (probe_only) {
+        CKS(flush_out(ctx, pending));
+        return VS_OK;
+    }
     // permuted bitmap over payload positions
     uint32_t* pbits = nullptr;
     if (bitmap) {
@@ -1625,4 +1638,28 @@ extern "C" int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, c
     CK(ctx->arena.reset());
     CKS(ensure_norms(const_cast<vs_column*>(data)));
     return vs::ivf_build_gpu(ctx, data, nlist, init_rows, seed, metric, max_iters, out);
+}
+
+extern "C" int vs_ivf_search(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                             const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
+                             int64_t* out_ids, double* out_dist, int32_t* out_count, int32_t* out_probes,
+                             int64_t* out_visited) {
+    return ivf_search_impl(ctx, ivf, queries, nq, bitmap, nbits, nprobe, k, out_ids, out_dist, out_count,
+                           out_probes, out_visited, nullptr, false);
+}
+
+extern "C" int vs_ivf_probe(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq, int32_t nprobe,
+                            int32_t* out_probes) {
+    if (!out_probes) return set_err(VS_ERR_PARAMETER, "null out_probes");
+    return ivf_search_impl(ctx, ivf, queries, nq, nullptr, 0, nprobe, 1, nullptr, nullptr, nullptr, out_probes,
+                           nullptr, nullptr, true);
+}
+
+extern "C" int vs_ivf_search_probed(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, int64_t nq,
+                                    const uint32_t* bitmap, int64_t nbits, int32_t nprobe,
+                                    const int32_t* probes, int32_t k, int64_t* out_ids, double* out_dist,
+                                    int32_t* out_count, int64_t* out_visited) {
+    if (!probes && nq > 0) return set_err(VS_ERR_PARAMETER, "null probes");
+    return ivf_search_impl(ctx, ivf, queries, nq, bitmap, nbits, nprobe, k, out_ids, out_dist, out_count,
+                           nullptr, out_visited, probes, false);
 }

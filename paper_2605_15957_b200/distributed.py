@@ -126,6 +126,14 @@ class TorchComm:
     def __init__(self, group=None):
         self.group = group
 
+    def size(self):
+        import torch.distributed as dist_
+        return dist_.get_world_size(self.group) if dist_.is_initialized() else 1
+
+    def rank(self):
+        import torch.distributed as dist_
+        return dist_.get_rank(self.group) if dist_.is_initialized() else 0
+
     def allreduce_min(self, t):
         import torch.distributed as dist_
         dist_.all_reduce(t, op=dist_.ReduceOp.MIN, group=self.group)
@@ -267,3 +275,42 @@ class ShardSearch:
             out[1].fill_(float("nan"))
             out[2].zero_()
         return out
+
+
+# ---- IVF over list shards --------------------------------------------------------------------
+
+
+def ivf_sharded_search(index, queries, k: int, nprobe: int, row_filter=None, list_owned=None, comm=None,
+                       merge=None, device=None):
+    """IVF search with lists sharded across ranks (LPT `list_owned`).
+
+    The coarse quantizer is split by QUERIES instead of replicated: rank r
+    probes its slice of the batch, the [Q, nprobe] probes are all-gathered
+    (every rank then holds the probes of the reference's coarse step), each
+    rank scans the probed lists it owns, and the per-rank top-k are
+    all-gathered and merged (tie rule). Returns (ids, dist, counts) on every
+    rank."""
+    import torch
+    comm = comm or TorchComm()
+    merge = merge or gpu_merge
+    world, rank = comm.size(), comm.rank()
+    nq = queries.shape[0]
+    per = (nq + world - 1) // world
+    lo, hi = min(nq, rank * per), min(nq, (rank + 1) * per)
+    mine = index.probe(queries[lo:hi], nprobe, device=device) if hi > lo else None
+    pad = torch.full((per, nprobe), -1, dtype=torch.int32, device=queries.device)
+    if mine is not None:
+        pad[: hi - lo] = mine if N_is_torch(mine) else torch.from_numpy(mine).to(queries.device)
+    probes = comm.allgather(pad).reshape(world * per, nprobe)[:nq].contiguous()
+    dev = queries.device
+    out = (torch.empty((nq, k), dtype=torch.int64, device=dev),
+           torch.empty((nq, k), dtype=torch.float64, device=dev),
+           torch.empty((nq,), dtype=torch.int32, device=dev))
+    index.search_raw(queries, k, nprobe, row_filter=row_filter, device=device, list_owned=list_owned,
+                     out=out, probes_in=probes)
+    gi, gd, gc = comm.allgather_topk(*out)
+    return merge(gi, gd, gc, k, index.metric)
+
+
+def N_is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")

@@ -528,7 +528,9 @@ class IvfIndex:
         return NeighborTable.from_padded(ids, dist, cnt, self.metric, visited, probes)
 
     def search_raw(self, queries, k, nprobe, row_filter=None, device=None, list_owned=None,
-                   out=None, want_probes=True):
+                   out=None, want_probes=True, probes_in=None):
+        """Padded device-layout search. `probes_in` ([nq, nprobe] int32, host
+        or device) skips the coarse quantizer (multi-GPU query-sliced probing)."""
         ctx = _ctx(device)
         div = self.device_index(ctx, list_owned)
         q, nq, d = _query_buffer(queries)
@@ -536,14 +538,40 @@ class IvfIndex:
             raise ShapeError(f"query dim {d} != index dim {self.dim}")
         bm = filter_bitmap(row_filter, self.count)
         ids, dist, cnt = out if out is not None else _outputs(nq, k)
-        probes = np.empty((nq, nprobe), np.int32) if want_probes else None
         visited = C.c_int64(0)
+        if probes_in is not None:
+            with _Stream(ctx, q, bm, ids, probes_in):
+                N.check(N.load().vs_ivf_search_probed(
+                    ctx.handle, div.handle, N.ptr(q), nq, N.ptr(bm), self.count if bm is not None else 0,
+                    int(nprobe), N.ptr(probes_in), int(k), N.ptr(ids), N.ptr(dist), N.ptr(cnt),
+                    C.byref(visited)), "ivf_search_probed")
+            return ids, dist, cnt, probes_in, visited.value
+        probes = np.empty((nq, nprobe), np.int32) if want_probes else None
         with _Stream(ctx, q, bm, ids):
             N.check(N.load().vs_ivf_search(ctx.handle, div.handle, N.ptr(q), nq, N.ptr(bm),
                                            self.count if bm is not None else 0, int(nprobe), int(k),
                                            N.ptr(ids), N.ptr(dist), N.ptr(cnt), N.ptr(probes),
                                            C.byref(visited)), "ivf_search")
         return ids, dist, cnt, probes, visited.value
+
+    def probe(self, queries, nprobe, device=None, out=None):
+        """Coarse quantizer only: [nq, nprobe] int32 probed lists (exact
+        tie-rule top-nprobe centroids, vecindex.py:238-243)."""
+        ctx = _ctx(device)
+        div = self.device_index(ctx)
+        q, nq, d = _query_buffer(queries)
+        if d != self.dim:
+            raise ShapeError(f"query dim {d} != index dim {self.dim}")
+        if out is None:
+            if N.is_torch(q) and q.is_cuda:
+                import torch
+                out = torch.empty((nq, nprobe), dtype=torch.int32, device=q.device)
+            else:
+                out = np.empty((nq, nprobe), np.int32)
+        with _Stream(ctx, q, out):
+            N.check(N.load().vs_ivf_probe(ctx.handle, div.handle, N.ptr(q), nq, int(nprobe), N.ptr(out)),
+                    "ivf_probe")
+        return out
 
     def structure_nbytes(self) -> int:
         return self.centroids.nbytes

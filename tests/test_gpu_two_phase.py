@@ -31,6 +31,12 @@ class ThreadComm:
         comm = self
 
         class _R:
+            def size(self):
+                return comm.world
+
+            def rank(self):
+                return r
+
             def allreduce_min(self, t):
                 comm.slots[r] = t.clone()
                 comm.barrier.wait()
@@ -130,3 +136,48 @@ def test_two_phase_rerun_path_and_empty_shard():
         assert np.array_equal(dist, ref.distance)
         if cls is Pessimist:
             assert shards[0].reruns == q.shape[0]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ivf_list_sharded_query_sliced_probing(world):
+    """IVF with LPT list shards: each rank probes a slice of the queries, the
+    probes are all-gathered, each rank scans its own lists, merge == one GPU."""
+    from paper_2605_15957_b200.distributed import ivf_sharded_search, lpt_assign
+    rng = np.random.default_rng(40 + world)
+    n, d, nlist = 30000, 64, 40
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    cen = data[rng.choice(n, nlist, replace=False)].copy()
+    assign = np.argmin(O.pairwise_sq_l2_fast(data, cen), axis=1)
+    parts = [np.flatnonzero(assign == c).astype(np.int64) for c in range(nlist)]
+    payload = [data[p] for p in parts]
+    q = rng.standard_normal((101, d)).astype(np.float32)
+    mask = rng.random(n) < 0.6
+    owner = lpt_assign([len(p) for p in parts], world)
+    qd = torch.from_numpy(q).cuda()
+    comm = ThreadComm(world)
+    results, errors = [None] * world, []
+
+    def rank(r):
+        try:
+            ctx = N.Context(0)
+            idx = vs.IvfIndex(nlist, d, n, "squared_l2", "owning", cen, parts, payload)
+            results[r] = ivf_sharded_search(idx, qd, 15, 7, row_filter=mask,
+                                            list_owned=(owner == r).astype(np.uint8), comm=comm.rank(r),
+                                            merge=partial(gpu_merge, device=ctx), device=ctx)
+            torch.cuda.synchronize()
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            comm.barrier.abort()
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errors:
+        raise errors[0]
+    ref = O.ivf_search(q, cen, parts, lambda c: payload[c], 7, 15, mask=mask)
+    for r in range(world):
+        ids, dist, _ = _flat(results[r])
+        assert np.array_equal(ids, ref.data_row)
+        assert np.array_equal(dist, ref.distance)
