@@ -26,7 +26,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 
 def _hdr_digest() -> str:
     h = hashlib.sha256()
-    for p in sorted(list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "vs_b200.h"]):
+    # every .cu too: vs_tc128.cu includes vs_tc.cu (one tile width per object)
+    for p in sorted(list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list(CSRC.glob("vs_tc.cu")) +
+                    [ROOT / "include" / "vs_b200.h"]):
         h.update(p.read_bytes())
     return h.hexdigest()[:16]
 

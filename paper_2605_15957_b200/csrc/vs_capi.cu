@@ -114,6 +114,7 @@ struct EnnJob {
     int k;
     int64_t id_offset;
     const int64_t* id_map = nullptr;   // staged position -> base row (streamed chunks)
+    bool narrow = false;               // 128-row tensor-core tiles (IVF coarse quantizer)
     // outputs (device, nullable)
     int64_t* out_ids;
     double* out_dist;
@@ -190,7 +191,10 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
     {
         if (use_tc) {
             // times its own GEMM launch under job.cls_scan (staging under VS_K_STAGE)
-            CKS(vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive, job.cls_scan));
+            if (job.narrow)
+                CKS(vs::bn128::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive, job.cls_scan));
+            else
+                CKS(vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive, job.cls_scan));
         } else {
             KTimer kt(ctx, job.cls_scan);
             const int64_t qtiles = (job.nq + 127) / 128;
@@ -1571,6 +1575,7 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     cj.out_count = nullptr;
     cj.cls_scan = VS_K_COARSE;
     cj.cls_rerank = VS_K_COARSE;
+    cj.narrow = !getenv("VS_COARSE_WIDE");
     CKS(run_enn(ctx, cj, cm, 0, false));
     }
     if (probe_only) {

@@ -30,12 +30,20 @@
 #include "vs_kernels.cuh"
 #include "vs_tc.cuh"
 
-namespace vs {
-
-namespace tc {
+// Compiled twice: this file with 256-row tiles (the default entry points,
+// inline namespace bn256) and vs_tc128.cu with 128-row tiles and four TMEM
+// accumulators (namespace bn128: the IVF coarse quantizer, where short splits
+// make the epilogue the bottleneck; measured faster there, slower on config 2).
 #ifndef VS_TC_BN
 #define VS_TC_BN 256
+#define VS_TC_NS bn256
+#define VS_TC_INLINE inline
 #endif
+
+namespace vs {
+VS_TC_INLINE namespace VS_TC_NS {
+
+namespace tc {
 
 constexpr int BM = 128;                 // queries per tile (UMMA M)
 constexpr int BN = VS_TC_BN;            // rows per tile (UMMA N)
@@ -924,6 +932,9 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     // keep the full margin band, which is exact by construction
     const int topk_mode = (cshift == 0 && !getenv("VS_TC_MARGIN_MODE")) ? 1 : 0;
     using namespace vs_internal;
+    // this translation unit's copy of the driver entry point (the file is
+    // compiled once per tile width)
+    if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cudaStream_t st = ctx->stream;
     const int d = sp.d;
     const int dp = (d + 7) / 8 * 8;
@@ -1247,5 +1258,5 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     return VS_OK;
 }
 
+}  // namespace VS_TC_NS
 }  // namespace vs
-

@@ -6,6 +6,17 @@
 #include "vs_kernels.cuh"
 
 namespace vs {
+#ifndef VS_TC_INLINE
+#define VS_TC_INLINE_DECL inline
+#else
+#define VS_TC_INLINE_DECL VS_TC_INLINE
+#endif
+// the 128-row-tile build of the phase-A GEMM (vs_tc128.cu)
+namespace bn128 {
+int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift,
+                CandBuf* cb, bool* exhaustive, int timer_class);
+}
+inline namespace bn256 {
 
 // whether the tensor-core phase A handles this shape / dtype / metric
 bool tc_supported(int d, int dtype, int ip);
@@ -58,6 +69,9 @@ struct TcIvfOut {
 };
 int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out);
 
+}  // namespace bn256
+
+// GPU IVF build / assignment (vs_kmeans.cu)
 int ivf_assign_gpu(vs_ctx* ctx, const vs_ivf* v, const vs_column* col, int32_t* out);
 int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows, uint64_t seed,
                   int32_t metric, int32_t max_iters, vs_ivf** out);
