@@ -191,7 +191,8 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
     {
         if (use_tc) {
             // times its own GEMM launch under job.cls_scan (staging under VS_K_STAGE)
-            if (job.narrow)
+            static const int narrow_env = getenv("VS_TC_NARROW") ? atoi(getenv("VS_TC_NARROW")) : -1;
+            if (narrow_env == 1 || (narrow_env != 0 && job.narrow))
                 CKS(vs::bn128::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive, job.cls_scan));
             else
                 CKS(vs::tc_enn_scan(ctx, sp, job.dtype, job.xmax, cshift, &sp.cb, &exhaustive, job.cls_scan));
