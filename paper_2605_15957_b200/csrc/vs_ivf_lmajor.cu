@@ -32,7 +32,7 @@
 namespace vs {
 
 namespace {
-constexpr int NT = 256;
+constexpr int NT = 128;
 constexpr int NW = NT / 32;
 constexpr int QT = kIvfLmQT;   // queries per unit (two per warp)
 constexpr int RS = 8;          // staged rows per chunk
@@ -128,7 +128,7 @@ struct UnitSmem {
 }  // namespace
 
 template <typename T, bool IP>
-__global__ void __launch_bounds__(NT, 2) k_ivf_scan_lmajor(IvfLmParams p) {
+__global__ void __launch_bounds__(NT, 4) k_ivf_scan_lmajor(IvfLmParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
     UnitSmem& S = *reinterpret_cast<UnitSmem*>(smraw);
     T* xs = reinterpret_cast<T*>(smraw + ((sizeof(UnitSmem) + 127) & ~size_t(127)));  // [RS][dp]

@@ -88,7 +88,7 @@ cudaError_t launch_ivf_scan_qmajor(const IvfScanParams& p, cudaStream_t s);
 
 // ---- phase A: IVF list scan (list-major) ------------------------------------------------
 // (query, probe) pairs grouped by list; units of <= kIvfLmQT pairs of one list
-constexpr int kIvfLmQT = 16;
+constexpr int kIvfLmQT = 8;
 constexpr int kIvfLmDMax = 1024;   // list-major scan: query held in registers
 struct IvfGroupArgs {
     const int32_t* probes;      // [nq][nprobe]
