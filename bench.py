@@ -810,6 +810,8 @@ def run_ours(args, cfg):
     wl = (IvfBf16Workload if cfg.get("bf16") else IvfWorkload if "nlist" in cfg else ExactWorkload)(
         args, cfg, rank, world, dev)
     ctx = N.Context.get(local)
+    if args.cand_slack:
+        ctx.set_option(N.OPT_CAND_SLACK, args.cand_slack)
 
     log(f"[rank {rank}] warmup {args.warmup}")
     for _ in range(args.warmup):
@@ -917,6 +919,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--cand-slack", type=int, default=0, help="VS_OPT_CAND_SLACK (candidate buffer x2^s)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -17,7 +17,7 @@ import numpy as np
 from . import errors as E
 
 LIB_NAME = "libvsb200.so"
-LIB_PATH = Path(os.environ.get("VSB200_LIB_OVERRIDE") or Path(__file__).resolve().parent / LIB_NAME)
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 VS_OK, VS_ERR_SHAPE, VS_ERR_EMPTY_INPUT, VS_ERR_PARAMETER = 0, 1, 2, 3
 VS_ERR_CAP_EXCEEDED, VS_ERR_PLACEMENT, VS_ERR_CUDA, VS_ERR_INTERNAL = 4, 5, 6, 7

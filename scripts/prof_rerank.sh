@@ -8,5 +8,5 @@ NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -linein
 for f in paper_2605_15957_b200/csrc/*.cu; do $NV -c $f -o /tmp/vsprof/$(basename $f).o & done; wait
 $NV -shared -o /tmp/vsprof/libvsb200_prof.so /tmp/vsprof/*.o -lcuda
 shift
-VSB200_LIB_OVERRIDE=/tmp/vsprof/libvsb200_prof.so python scripts/prof_rerank.py "${@:-2}" > $OUT/phases.txt 2>&1
+VS_B200_LIB=/tmp/vsprof/libvsb200_prof.so python scripts/prof_rerank.py "${@:-2}" > $OUT/phases.txt 2>&1
 cat $OUT/phases.txt

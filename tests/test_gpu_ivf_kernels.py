@@ -5,6 +5,7 @@ bit-identical float64 distances, identical visited counts."""
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2605_15957_b200 as vs
 from oracle import sqlvs_oracle as O
@@ -159,3 +160,32 @@ def test_ivf_lmajor_list_sharding_plus_merge():
     # ownership reset: the same device copy scans every list again
     again = idx.search(q, vs.SearchParams(k=9, nprobe=6), row_filter=mask)
     assert np.array_equal(again.data_row, whole.data_row)
+
+
+def test_sample_trained_index_assign_and_borrowed_payload():
+    """Train on a sample (vs_ivf_build), assign every row (vs_ivf_assign,
+    vecindex.py:303-304), build the list-contiguous payload in a caller-owned
+    device buffer and borrow it (vs_ivf_wrap): searches equal the oracle on
+    that structure (the tensor-core and list-major scans alike)."""
+    rng = np.random.default_rng(31)
+    n, d, nlist = 24000, 96, 20
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    xd = torch.from_numpy(data).cuda()
+    trained = vs.IvfIndex.build(vs.EmbeddingColumn.from_device(xd[:4000].contiguous()), nlist, seed=3)
+    lists = trained.assign(vs.EmbeddingColumn.from_device(xd))
+    assert lists.dtype == torch.int32 and lists.shape == (n,)
+    ref_assign = np.argmin(O.pairwise(data, trained.centroids), axis=1)
+    agree = float((lists.cpu().numpy() == ref_assign).mean())
+    assert agree > 0.99          # bf16 tensor-core keys: near-ties may differ
+    order = torch.sort(lists, stable=True).indices
+    sizes = torch.bincount(lists, minlength=nlist).cpu().numpy().astype(np.int64)
+    payload = xd[order].to(torch.bfloat16).contiguous()
+    idx = vs.IvfIndex.from_device_lists(trained.centroids, sizes, order.cpu().numpy(), payload, count=n)
+    parts = np.split(order.cpu().numpy(), np.cumsum(sizes)[:-1])
+    rounded = payload.float().cpu().numpy()
+    offs = np.r_[0, np.cumsum(sizes)]
+    q = rng.standard_normal((50, d)).astype(np.float32)
+    mask = rng.random(n) < 0.5
+    for kernel in (2, 3):
+        _check(idx, q, trained.centroids, parts, [rounded[offs[c]:offs[c + 1]] for c in range(nlist)],
+               4, 12, "squared_l2", mask, kernel)
