@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <functional>
 #include <limits>
 #include <cmath>
 #include <cstdarg>
@@ -448,6 +449,7 @@ int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value) {
         case VS_OPT_ENN_KERNEL: ctx->opt_enn_kernel = (int)value; break;
         case VS_OPT_IVF_KERNEL: ctx->opt_ivf_kernel = (int)value; break;
         case VS_OPT_STREAM_CHUNK: ctx->opt_stream_chunk = value; break;
+        case VS_OPT_IVF_CHUNK_ROWS: ctx->opt_ivf_chunk_rows = value; break;
         case VS_OPT_CAND_SLACK: ctx->opt_slack = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8)); break;
         case VS_OPT_FORCE_RETRY: ctx->opt_force_retry = (int)value; break;
         case VS_OPT_TIMING: ctx->opt_timing = (int)value; break;
@@ -1256,7 +1258,8 @@ struct IvfGroups {
     int64_t max_units = 0;
     int64_t npairs = 0;
 };
-int ivf_group(vs_ctx* ctx, const IvfJob& job, int unit_pairs, IvfGroups* out) {
+int ivf_group(vs_ctx* ctx, const IvfJob& job, int unit_pairs, IvfGroups* out, const int32_t* chunks = nullptr,
+              int max_chunks = 1) {
     const vs_ivf* v = job.ivf;
     const int64_t npairs = job.nq * (int64_t)job.nprobe;
     vs::IvfGroupArgs g;
@@ -1266,6 +1269,7 @@ int ivf_group(vs_ctx* ctx, const IvfJob& job, int unit_pairs, IvfGroups* out) {
     g.nlist = v->nlist;
     g.owned = v->owned;
     g.unit_pairs = unit_pairs;
+    g.chunks = chunks;
     CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_in));
     CKS(arena_alloc(ctx, (size_t)npairs, &g.keys_out));
     CKS(arena_alloc(ctx, (size_t)npairs, &g.vals_in));
@@ -1274,7 +1278,7 @@ int ivf_group(vs_ctx* ctx, const IvfJob& job, int unit_pairs, IvfGroups* out) {
     CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.qoff));
     CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.ucnt));
     CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &g.uoff));
-    const int64_t max_units = vs::ivf_max_units(job.nq, job.nprobe, v->nlist, unit_pairs);
+    const int64_t max_units = vs::ivf_max_units(job.nq, job.nprobe, v->nlist, unit_pairs) * max_chunks;
     CKS(arena_alloc(ctx, (size_t)max_units, &g.units));
     g.tmp_bytes = vs::ivf_group_temp_bytes(npairs, v->nlist);
     char* gtmp = nullptr;
@@ -1327,8 +1331,24 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     const unsigned* tau_g = nullptr;
     int verify = 0;
     if (kern == IVF_TC) {
+        // lists longer than kChunkRows are cut into row chunks, each its own
+        // work unit with its own candidate buffers (flat per-query ranges), so
+        // one long list cannot hold a CTA for many times the mean work
+        const int64_t kChunkRows = ctx->opt_ivf_chunk_rows > 0 ? ctx->opt_ivf_chunk_rows : 512 * 256;
+        std::vector<int32_t> h_ch(v->nlist);
+        int max_ch = 1;
+        for (int i = 0; i < v->nlist; ++i) {
+            const int64_t nl = v->h_off[i + 1] - v->h_off[i];
+            h_ch[i] = (int32_t)std::max<int64_t>(1, (nl + kChunkRows - 1) / kChunkRows);
+            max_ch = std::max(max_ch, (int)h_ch[i]);
+        }
+        int32_t* d_ch = nullptr;
+        if (max_ch > 1) {
+            CKS(arena_alloc(ctx, (size_t)v->nlist, &d_ch));
+            CK(cudaMemcpyAsync(d_ch, h_ch.data(), v->nlist * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        }
         IvfGroups gr;
-        CKS(ivf_group(ctx, job, 128, &gr));
+        CKS(ivf_group(ctx, job, 128, &gr, d_ch, max_ch));
         vs::TcIvfArgs a;
         a.Q = job.q;
         a.nq = job.nq;
@@ -1350,6 +1370,29 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         a.ip = v->metric;
         a.cshift = cshift;
         a.timer_class = VS_K_IVF_SCAN;
+        if (max_ch > 1) {
+            int64_t *sub_off = nullptr, *pair_base = nullptr;
+            char* tmp = nullptr;
+            const size_t tb = vs::ivf_pair_subs_temp_bytes(job.nq);
+            CKS(arena_alloc(ctx, (size_t)job.nq + 1, &sub_off));
+            CKS(arena_alloc(ctx, (size_t)job.nq * job.nprobe, &pair_base));
+            CKS(arena_alloc(ctx, tb, &tmp));
+            CK(vs::launch_ivf_pair_subs(job.probes, job.nq, job.nprobe, d_ch, sub_off, pair_base, tmp, tb,
+                                        ctx->stream));
+            int64_t total = 0;
+            CK(cudaMemcpyAsync(&total, sub_off + job.nq, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            std::vector<int32_t> srt(h_ch);
+            std::sort(srt.begin(), srt.end(), std::greater<int32_t>());
+            int64_t bound = 0;
+            for (int j = 0; j < job.nprobe && j < (int)srt.size(); ++j) bound += 2 * (int64_t)srt[j];
+            a.chunk_rows = kChunkRows;
+            a.pair_base = pair_base;
+            a.sub_off = sub_off;
+            a.total_subs = total;
+            a.max_subs = (int)bound;
+            ctx->stats[VS_STAT_LAUNCHES] += 3;
+        }
         vs::TcIvfOut o;
         CKS(vs::tc_ivf_scan(ctx, a, &o));
         cb = o.cb;

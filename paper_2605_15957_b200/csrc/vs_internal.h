@@ -127,6 +127,7 @@ struct vs_ctx {
     int opt_force_retry = 0;
     int opt_timing = 0;
     int64_t opt_stream_chunk = 0;    // host-resident search: selected rows per chunk (0 = auto)
+    int64_t opt_ivf_chunk_rows = 0;  // tensor-core IVF scan: rows per list chunk (0 = 131072)
     int sm_reserve = 0;              // SMs left free by persistent kernels (streamed gathers)
     cudaStream_t copy_stream = nullptr;   // host-resident search: gathers over PCIe
     // CUDA-event timing of kernel classes (resolved after each call's final sync)

@@ -310,21 +310,46 @@ __global__ void k_pair_keys(const int32_t* __restrict__ probes, int64_t npairs, 
     }
 }
 
-__global__ void k_unit_counts(const int32_t* __restrict__ cnt, int nlist, int qt, int32_t* __restrict__ ucnt) {
+__global__ void k_unit_counts(const int32_t* __restrict__ cnt, int nlist, int qt, const int32_t* __restrict__ chunks,
+                              int32_t* __restrict__ ucnt) {
     for (int l = blockIdx.x * blockDim.x + threadIdx.x; l <= nlist; l += gridDim.x * blockDim.x)
-        ucnt[l] = l < nlist ? (cnt[l] + qt - 1) / qt : 0;
+        ucnt[l] = l < nlist ? (cnt[l] + qt - 1) / qt * (chunks ? chunks[l] : 1) : 0;
 }
 
-// units of one list split its pairs evenly (sizes differ by at most one)
+// per query: its flat buffer count 2 * sum_j chunks(probe j); per pair: its base
+__global__ void k_pair_subs(const int32_t* __restrict__ probes, int64_t nq, int nprobe,
+                            const int32_t* __restrict__ chunks, int64_t* __restrict__ qsubs,
+                            int64_t* __restrict__ pair_base) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        int64_t acc = 0;
+        for (int j = 0; j < nprobe; ++j) {
+            pair_base[q * nprobe + j] = acc;   // relative; made absolute below
+            acc += 2 * (int64_t)chunks[probes[q * nprobe + j]];
+        }
+        qsubs[q] = acc;
+    }
+}
+__global__ void k_pair_subs_abs(const int64_t* __restrict__ sub_off, int64_t nq, int nprobe,
+                                int64_t* __restrict__ pair_base) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq * nprobe;
+         i += (int64_t)gridDim.x * blockDim.x)
+        pair_base[i] += sub_off[i / nprobe];
+}
+
+// units of one list split its pairs evenly (sizes differ by at most one), times
+// its row chunks
 __global__ void k_write_units(const int32_t* __restrict__ cnt, const int32_t* __restrict__ qoff,
-                              const int32_t* __restrict__ uoff, int nlist, int4* __restrict__ units) {
+                              const int32_t* __restrict__ uoff, int nlist, const int32_t* __restrict__ chunks,
+                              int4* __restrict__ units) {
     for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlist; l += gridDim.x * blockDim.x) {
         const int n = cnt[l];
-        const int nu = uoff[l + 1] - uoff[l];
+        const int ch = chunks ? chunks[l] : 1;
+        const int nu = (uoff[l + 1] - uoff[l]) / ch;   // pair groups
         int b = qoff[l];
+        int u = uoff[l];
         for (int j = 0; j < nu; ++j) {
             const int m = n / nu + (j < n % nu ? 1 : 0);
-            units[uoff[l] + j] = make_int4(l, b, m, 0);
+            for (int c = 0; c < ch; ++c) units[u++] = make_int4(l, b, m, c);
             b += m;
         }
     }
@@ -403,11 +428,34 @@ cudaError_t launch_ivf_group(const IvfGroupArgs& g, cudaStream_t s) {
     tb = g.tmp_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(g.tmp, tb, g.cnt, g.qoff, g.nlist + 1, s)) != cudaSuccess) return e;
     const int lb = std::max(1, std::min((g.nlist + 256) / 256, 1024));
-    k_unit_counts<<<lb, 256, 0, s>>>(g.cnt, g.nlist, g.unit_pairs, g.ucnt);
+    k_unit_counts<<<lb, 256, 0, s>>>(g.cnt, g.nlist, g.unit_pairs, g.chunks, g.ucnt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     tb = g.tmp_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(g.tmp, tb, g.ucnt, g.uoff, g.nlist + 1, s)) != cudaSuccess) return e;
-    k_write_units<<<lb, 256, 0, s>>>(g.cnt, g.qoff, g.uoff, g.nlist, g.units);
+    k_write_units<<<lb, 256, 0, s>>>(g.cnt, g.qoff, g.uoff, g.nlist, g.chunks, g.units);
+    return cudaGetLastError();
+}
+
+size_t ivf_pair_subs_temp_bytes(int64_t nq) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nq + 1));
+    return b + 256 + (size_t)(nq + 1) * sizeof(int64_t);
+}
+
+cudaError_t launch_ivf_pair_subs(const int32_t* probes, int64_t nq, int nprobe, const int32_t* chunks,
+                                 int64_t* sub_off, int64_t* pair_base, void* tmp, size_t tmp_bytes,
+                                 cudaStream_t s) {
+    cudaError_t e;
+    int64_t* qsubs = reinterpret_cast<int64_t*>(tmp);
+    void* scan_tmp = reinterpret_cast<char*>(tmp) + ((size_t)(nq + 1) * sizeof(int64_t) + 255) / 256 * 256;
+    size_t tb = tmp_bytes - ((size_t)(nq + 1) * sizeof(int64_t) + 255) / 256 * 256;
+    if ((e = cudaMemsetAsync(qsubs + nq, 0, sizeof(int64_t), s)) != cudaSuccess) return e;
+    const int b = (int)std::max<int64_t>(1, std::min<int64_t>((nq + 255) / 256, 1024));
+    k_pair_subs<<<b, 256, 0, s>>>(probes, nq, nprobe, chunks, qsubs, pair_base);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cub::DeviceScan::ExclusiveSum(scan_tmp, tb, qsubs, sub_off, (int)(nq + 1), s)) != cudaSuccess) return e;
+    const int b2 = (int)std::max<int64_t>(1, std::min<int64_t>((nq * nprobe + 255) / 256, 4096));
+    k_pair_subs_abs<<<b2, 256, 0, s>>>(sub_off, nq, nprobe, pair_base);
     return cudaGetLastError();
 }
 

@@ -15,8 +15,9 @@ struct CandBuf {
     uint32_t* pos;     // [nq][n_sub][C]
     int* cnt;          // [nq][n_sub]
     int* overflow;     // [nq]
-    int n_sub;
+    int n_sub;         // subs per query (with sub_off: the maximum over queries)
     int C;
+    const int64_t* sub_off = nullptr;   // [nq+1] variable subs per query (flat buffers), nullable
 };
 
 // ---- bitmap -> ascending selection vector -------------------------------------------
@@ -108,7 +109,15 @@ struct IvfGroupArgs {
     void* tmp;
     size_t tmp_bytes;           // >= ivf_group_temp_bytes
     int unit_pairs;             // max pairs per unit (kIvfLmQT SIMT, 128 tensor cores)
+    const int32_t* chunks = nullptr;   // [nlist] row chunks per list (nullable: 1); a unit is
+                                       // (list, pair range, chunk) -> int4 (list, first pair, pairs, chunk)
 };
+// long lists cut into row chunks (tensor-core IVF scan): per pair, the first of its
+// 2 * chunks(list) buffers; per query, the offsets of its flat buffer range
+cudaError_t launch_ivf_pair_subs(const int32_t* probes, int64_t nq, int nprobe, const int32_t* chunks,
+                                 int64_t* sub_off, int64_t* pair_base, void* tmp, size_t tmp_bytes,
+                                 cudaStream_t s);
+size_t ivf_pair_subs_temp_bytes(int64_t nq);
 size_t ivf_group_temp_bytes(int64_t npairs, int nlist);
 int64_t ivf_max_units(int64_t nq, int nprobe, int nlist, int unit_pairs);
 cudaError_t launch_ivf_group(const IvfGroupArgs& g, cudaStream_t s);

@@ -571,7 +571,10 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
 
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const int64_t q = blockIdx.x;
-    const int C = p.cb.C, nsub = p.cb.n_sub;
+    const int C = p.cb.C;
+    // buffers of this query: fixed n_sub per query, or a flat range (IVF list chunks)
+    const int64_t bbase = p.cb.sub_off ? p.cb.sub_off[q] : q * (int64_t)p.cb.n_sub;
+    const int nsub = p.cb.sub_off ? (int)(p.cb.sub_off[q + 1] - bbase) : p.cb.n_sub;
     const int d = p.d;
     const bool warp_path = d >= 8 && d <= WARP_D_MAX;
     if (warp_path) {
@@ -591,13 +594,13 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
         for (int i = tid; i < d; i += NT) qs[i] = qg[i];
     long long tot = 0;
     for (int s = tid; s < nsub; s += NT) {
-        const int c = p.cb.cnt[q * nsub + s];
+        const int c = p.cb.cnt[bbase + s];
         cnts[s] = c;
         tot += c;
     }
     tot = block_sum_ll(tot, sm.red);  // includes __syncthreads
-    const float* ckey = p.cb.key + q * nsub * (int64_t)C;
-    const uint32_t* cpos = p.cb.pos + q * nsub * (int64_t)C;
+    const float* ckey = p.cb.key + bbase * (int64_t)C;
+    const uint32_t* cpos = p.cb.pos + bbase * (int64_t)C;
     uint32_t* spos = p.s_pos + q * p.s_cap;
     uint64_t* skey = p.s_key + q * p.s_cap;
     int64_t* sid = p.s_id + q * p.s_cap;

@@ -109,6 +109,8 @@ struct Params {
     int nprobe;
     const uint32_t* pbits;          // nullable: filter bit per payload position
     int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
+    int64_t chunk_rows;             // MODE 2: rows per list chunk (0: whole lists)
+    const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
     int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
                                     // appends per thread instead of cooperatively
 };
@@ -122,6 +124,7 @@ struct Item {
     int64_t b_end;
     int64_t s;          // data split (MODE 0/1)
     int npairs;
+    int chunk;          // MODE 2: row chunk of the list
 };
 template <int MODE, int QTILE>
 __device__ __forceinline__ Item decode_item(const Params& p, int64_t it) {
@@ -131,11 +134,12 @@ __device__ __forceinline__ Item decode_item(const Params& p, int64_t it) {
         const int64_t off = p.list_off[un.x];
         const int64_t n = p.list_off[un.x + 1] - off;
         r.a_row = un.y;
-        r.b_row0 = off;
-        r.ntile = (n + BN - 1) / BN;
-        r.b_end = off + n;
+        r.b_row0 = off + (p.chunk_rows ? (int64_t)un.w * p.chunk_rows : 0);
+        r.b_end = p.chunk_rows ? min(off + n, r.b_row0 + p.chunk_rows) : off + n;
+        r.ntile = (r.b_end - r.b_row0 + BN - 1) / BN;
         r.s = 0;
         r.npairs = un.z;
+        r.chunk = un.w;
     } else {
         const int qt = (int)(it % p.qtiles);
         r.s = it / p.qtiles;
@@ -146,6 +150,7 @@ __device__ __forceinline__ Item decode_item(const Params& p, int64_t it) {
         r.ntile = t1 - t0;
         r.b_end = p.nsel;
         r.npairs = 0;
+        r.chunk = 0;
     }
     return r;
 }
@@ -515,7 +520,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (row >= item.npairs) return false;
                 const int code = __ldg(p.pair_codes + item.a_row + row);
                 q = code / p.nprobe;
-                sub = (int64_t)(code % p.nprobe) * 2 + half;
+                // flat buffer index with list chunks, else the sub of (query, probe rank)
+                sub = p.pair_base ? __ldg(p.pair_base + code) + 2 * item.chunk + half
+                                  : (int64_t)(code % p.nprobe) * 2 + half;
                 return true;
             }
             q = item.a_row + (int64_t)rank * BM + row;
@@ -538,7 +545,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const Item item = decode_item<MODE, QTILE>(p, it);
             int64_t q = 0, sub = 0;
             const bool qv = row_query(item, q, sub);
-            const int64_t cbase = qv ? ((q * p.cb.n_sub + sub) * (int64_t)C) : 0;
+            const int64_t bufidx = (MODE == 2 && p.pair_base) ? sub : q * p.cb.n_sub + sub;
+            const int64_t cbase = qv ? bufidx * (int64_t)C : 0;
             float* ckey = p.cb.key + cbase;
             uint32_t* cpos = p.cb.pos + cbase;
             const float qmargin = qv ? p.margin[q] : 0.f;
@@ -695,7 +703,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 else mbar_arrive(&S.tempty[acc]);
             }
             if (qv) {
-                p.cb.cnt[q * p.cb.n_sub + sub] = cnt;
+                p.cb.cnt[bufidx] = cnt;
                 if (ovf) p.cb.overflow[q] = 1;
             }
         }
@@ -1180,20 +1188,23 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     }
     // room for one half-tile of appends (128) beyond the kept band
     int64_t C = pow2ceil(2 * a.k + 96 + tc::BN / 2) << (ctx->opt_slack + a.cshift);
-    // one buffer per (pair, column half): a column half sees <= 128 rows per tile
-    const int64_t cap = pow2ceil((a.max_list + tc::BN - 1) / tc::BN * (tc::BN / 2) + 64);
+    // one buffer per (pair, [chunk,] column half): a column half sees <= 128 rows per tile
+    const int64_t rows_seen = a.chunk_rows ? std::min(a.max_list, a.chunk_rows) : a.max_list;
+    const int64_t cap = pow2ceil((rows_seen + tc::BN - 1) / tc::BN * (tc::BN / 2) + 64);
     out->exhaustive = C >= cap;
     if (C > cap) C = cap;
     CandBuf c;
-    c.n_sub = 2 * a.nprobe;
     c.C = (int)C;
-    const size_t slots = (size_t)a.nq * c.n_sub * C;
+    const int64_t nbuf = a.pair_base ? a.total_subs : a.nq * 2 * (int64_t)a.nprobe;
+    c.n_sub = a.pair_base ? a.max_subs : 2 * a.nprobe;
+    c.sub_off = a.pair_base ? a.sub_off : nullptr;
+    const size_t slots = (size_t)nbuf * C;
     CKS(arena_alloc(ctx, slots, &c.key));
     CKS(arena_alloc(ctx, slots, &c.pos));
-    CKS(arena_alloc(ctx, (size_t)a.nq * c.n_sub, &c.cnt));
+    CKS(arena_alloc(ctx, (size_t)nbuf, &c.cnt));
     CKS(arena_alloc(ctx, (size_t)a.nq, &c.overflow));
     CK(cudaMemsetAsync(c.overflow, 0, a.nq * sizeof(int), st));
-    CK(cudaMemsetAsync(c.cnt, 0, (size_t)a.nq * c.n_sub * sizeof(int), st));
+    CK(cudaMemsetAsync(c.cnt, 0, (size_t)nbuf * sizeof(int), st));
     CUtensorMap ma, mb;
     if (!make_map(&ma, qp, std::max<int64_t>(a.npairs, 1), d, dp, tc::BM) ||
         !make_map(&mb, a.payload, a.n_total, d, d, tc::BN))
@@ -1224,6 +1235,8 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     pr.pbits = a.pbits;
     static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
     pr.pf_boxes = pf_env;
+    pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
+    pr.pair_base = a.pair_base;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.max_units, ctx->sm_count));
     static const bool dbg_on = getenv("VS_TC_DEBUG") != nullptr;
     if (dbg_on) {

@@ -59,6 +59,12 @@ struct TcIvfArgs {
     int ip;
     int cshift;
     int timer_class;
+    // long lists cut into row chunks (nullable / 0: whole lists)
+    int64_t chunk_rows = 0;
+    const int64_t* pair_base = nullptr;   // [nq*nprobe] first flat buffer of each pair
+    const int64_t* sub_off = nullptr;     // [nq+1] flat buffer range of each query
+    int64_t total_subs = 0;
+    int max_subs = 0;                     // bound on buffers per query
 };
 struct TcIvfOut {
     CandBuf cb;

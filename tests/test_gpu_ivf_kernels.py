@@ -189,3 +189,33 @@ def test_sample_trained_index_assign_and_borrowed_payload():
     for kernel in (2, 3):
         _check(idx, q, trained.centroids, parts, [rounded[offs[c]:offs[c + 1]] for c in range(nlist)],
                4, 12, "squared_l2", mask, kernel)
+
+
+@pytest.mark.parametrize("chunk_rows", [300, 1024])
+def test_tensor_core_scan_long_lists_cut_into_row_chunks(chunk_rows):
+    """Long lists split into row chunks (each its own work unit and candidate
+    buffers, variable buffers per query in phase B): identical to the oracle,
+    including a skewed index whose largest list spans many chunks."""
+    rng = np.random.default_rng(chunk_rows)
+    n, d, nlist = 16000, 64, 12
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    xb = torch.from_numpy(data).to(torch.bfloat16)
+    rounded = xb.float().numpy()
+    cen = rounded[rng.choice(n, nlist, replace=False)].copy()
+    cen[0] = 0.0                                            # one giant list
+    assign = np.argmin(O.pairwise_sq_l2_fast(rounded, cen), axis=1)
+    parts = [np.flatnonzero(assign == c).astype(np.int64) for c in range(nlist)]
+    assert max(len(p) for p in parts) > 4 * chunk_rows
+    order = torch.from_numpy(np.concatenate(parts))
+    payload = xb[order].cuda().contiguous()
+    idx = vs.IvfIndex.from_device_lists(cen, [len(p) for p in parts], order.numpy(), payload, count=n)
+    q = rng.standard_normal((150, d)).astype(np.float32) * 0.2
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_IVF_CHUNK_ROWS, chunk_rows)
+    try:
+        for mask in (None, rng.random(n) < 0.4):
+            for metric_k in ((3, 25), (nlist, 10)):
+                _check(idx, q, cen, parts, [rounded[p] for p in parts], metric_k[0], metric_k[1],
+                       "squared_l2", mask, 3)
+    finally:
+        ctx.set_option(N.OPT_IVF_CHUNK_ROWS, 0)
