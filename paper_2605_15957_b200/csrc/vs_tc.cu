@@ -110,6 +110,7 @@ struct Params {
     const uint32_t* pbits;          // nullable: filter bit per payload position
     int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
     int64_t chunk_rows;             // MODE 2: rows per list chunk (0: whole lists)
+    int l2_hints;                   // MODE 2: L2 evict-first for B, evict-last for A
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
     int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
                                     // appends per thread instead of cooperatively
@@ -185,6 +186,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// TMA load with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 // TMA prefetch of one box into L2 (no shared memory, no barrier)
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
@@ -348,6 +368,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             long long w_empty = 0;
+            const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
             for (int64_t it = unit; it < nitems; it += nunits) {
                 const Item item = decode_item<MODE, QTILE>(p, it);
                 // MODE 2: the B operand streams from HBM exactly once, so the
@@ -377,8 +398,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                              brow + (int)rank * (BN / 2));
                         } else {
                             mbar_expect_tx(&S.full[stage], STAGE_BYTES);
-                            tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row);
-                            tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow);
+                            if (MODE == 2 && p.l2_hints) {
+                                // B (the payload) streams once: evict first; A (the unit's
+                                // queries) is re-read for every tile of the list: evict last
+                                tma_load_2d_hint(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row, pol_a);
+                                tma_load_2d_hint(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow, pol_b);
+                            } else {
+                                tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row);
+                                tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow);
+                            }
                         }
                         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
                     }
@@ -1236,6 +1264,8 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
     pr.pf_boxes = pf_env;
     pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
+    static const int hints_env = getenv("VS_TC_L2HINTS") ? atoi(getenv("VS_TC_L2HINTS")) : 1;
+    pr.l2_hints = hints_env;
     pr.pair_base = a.pair_base;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.max_units, ctx->sm_count));
     static const bool dbg_on = getenv("VS_TC_DEBUG") != nullptr;
