@@ -110,7 +110,8 @@ struct Params {
     const uint32_t* pbits;          // nullable: filter bit per payload position
     int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
     int64_t chunk_rows;             // MODE 2: rows per list chunk (0: whole lists)
-    int l2_hints;                   // MODE 2: L2 evict-first for B, evict-last for A
+    int l2_hints;                   // MODE 2: L2 evict-first for B, evict-last for A (always on)
+    int a32;                        // MODE 2: map_a32 (32-row A boxes) is valid
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
     int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
                                     // appends per thread instead of cooperatively
@@ -313,7 +314,8 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t* r) {
 template <bool IP, int MODE, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_enn_scan_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                  Params p) {
+                  Params p, const __grid_constant__ CUtensorMap map_a32,
+                  const __grid_constant__ CUtensorMap map_a64) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ __align__(16) float xn_w[8][BN / 2];  // per epilogue warp: its column half's row norms
     __shared__ __align__(16) float app_w[8][32];     // per epilogue warp: one lane's chunk keys (appends)
@@ -397,13 +399,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             tma_load_2d_pair(sa + A_BYTES, &map_b, &S.full[stage], kb * BK,
                                              brow + (int)rank * (BN / 2));
                         } else {
-                            mbar_expect_tx(&S.full[stage], STAGE_BYTES);
-                            if (MODE == 2 && p.l2_hints) {
-                                // B (the payload) streams once: evict first; A (the unit's
-                                // queries) is re-read for every tile of the list: evict last
-                                tma_load_2d_hint(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row, pol_a);
+                            if (MODE == 2) {
+                                // A: only the unit's pair rows (32-row box for <= 32 pairs;
+                                // the MMA's other A rows hold stale data whose accumulator
+                                // rows the epilogue ignores). B (the payload) streams once:
+                                // evict first; A is re-read for every tile: evict last.
+                                const int arows = !p.a32 ? BM : item.npairs <= 32 ? 32 : item.npairs <= 64 ? 64 : BM;
+                                mbar_expect_tx(&S.full[stage], STAGE_BYTES - A_BYTES + arows * BK * 2);
+                                tma_load_2d_hint(sa, arows == 32 ? &map_a32 : arows == 64 ? &map_a64 : &map_a,
+                                                 &S.full[stage], kb * BK, (int)item.a_row, pol_a);
                                 tma_load_2d_hint(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow, pol_b);
                             } else {
+                                mbar_expect_tx(&S.full[stage], STAGE_BYTES);
                                 tma_load_2d(sa, &map_a, &S.full[stage], kb * BK, (int)item.a_row);
                                 tma_load_2d(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow);
                             }
@@ -921,7 +928,10 @@ bool make_map(CUtensorMap* map, const void* gaddr, int64_t rows, int d, int dp, 
 // launch one variant of the phase-A kernel; CTA pairs go out as clusters of 2
 template <bool IP, int MODE, bool PAIR>
 cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& pr, unsigned grid,
-                      cudaStream_t st) {
+                      cudaStream_t st, const CUtensorMap* ma32 = nullptr, const CUtensorMap* ma64 = nullptr);
+template <bool IP, int MODE, bool PAIR>
+cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Params& pr, unsigned grid,
+                      cudaStream_t st, const CUtensorMap* ma32, const CUtensorMap* ma64) {
     auto kern = tc::k_enn_scan_tc<IP, MODE, PAIR>;
     const size_t sm = tc::smem_bytes<PAIR>();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -942,7 +952,7 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const tc::Pa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = PAIR ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, ma, mb, pr);
+    return cudaLaunchKernelEx(&cfg, kern, ma, mb, pr, ma32 ? *ma32 : ma, ma64 ? *ma64 : ma);
 }
 
 // CTA pairs unless disabled (VS_TC_PAIR=0) or the batch fits one 128-query tile
@@ -1234,8 +1244,11 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     CK(cudaMemsetAsync(c.overflow, 0, a.nq * sizeof(int), st));
     CK(cudaMemsetAsync(c.cnt, 0, (size_t)nbuf * sizeof(int), st));
     CUtensorMap ma, mb;
+    CUtensorMap ma32, ma64;
     if (!make_map(&ma, qp, std::max<int64_t>(a.npairs, 1), d, dp, tc::BM) ||
-        !make_map(&mb, a.payload, a.n_total, d, d, tc::BN))
+        !make_map(&mb, a.payload, a.n_total, d, d, tc::BN) ||
+        !make_map(&ma32, qp, std::max<int64_t>(a.npairs, 1), d, dp, 32) ||
+        !make_map(&ma64, qp, std::max<int64_t>(a.npairs, 1), d, dp, 64))
         return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     tc::Params pr{};
     pr.nq = a.nq;
@@ -1264,8 +1277,9 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
     pr.pf_boxes = pf_env;
     pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
-    static const int hints_env = getenv("VS_TC_L2HINTS") ? atoi(getenv("VS_TC_L2HINTS")) : 1;
-    pr.l2_hints = hints_env;
+    pr.l2_hints = 1;
+    static const int a32_env = getenv("VS_TC_A32") ? atoi(getenv("VS_TC_A32")) : 1;
+    pr.a32 = a32_env;
     pr.pair_base = a.pair_base;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.max_units, ctx->sm_count));
     static const bool dbg_on = getenv("VS_TC_DEBUG") != nullptr;
@@ -1275,8 +1289,8 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     }
     {
         KTimer kt(ctx, a.timer_class);
-        if (a.ip) CK((launch_tc<true, 2, false>(ma, mb, pr, grid, st)));
-        else CK((launch_tc<false, 2, false>(ma, mb, pr, grid, st)));
+        if (a.ip) CK((launch_tc<true, 2, false>(ma, mb, pr, grid, st, &ma32, &ma64)));
+        else CK((launch_tc<false, 2, false>(ma, mb, pr, grid, st, &ma32, &ma64)));
     }
     ctx->stats[VS_STAT_LAUNCHES] += 1;
     if (dbg_on) {
