@@ -112,6 +112,7 @@ struct Params {
     int64_t chunk_rows;             // MODE 2: rows per list chunk (0: whole lists)
     int l2_hints;                   // MODE 2: L2 evict-first for B, evict-last for A (always on)
     int a32;                        // MODE 2: map_a32 (32-row A boxes) is valid
+    int lim0;                       // first compaction point (0: 2k + 64)
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
     int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
                                     // appends per thread instead of cooperatively
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // data is live: compact when the next half-tile (<= 128 appends) could
             // push the buffer past lim (2k + 64 initially, then 2x the kept count)
             const int cap_t = C - BN / 2;
-            const int lim0 = 2 * p.k + 64;
+            const int lim0 = p.lim0 > 0 ? p.lim0 : 2 * p.k + 64;
             int lim = lim0;
             float tau = __int_as_float(0x7f800000);
             for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
@@ -1093,6 +1094,8 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     pr.argmin_out = nullptr;
     // short splits append densely (the per-split fill is a larger share):
     // per-thread appends there, warp-cooperative ones for long splits (measured)
+    static const int lim0_env = getenv("VS_TC_LIM0") ? atoi(getenv("VS_TC_LIM0")) : 0;
+    pr.lim0 = lim0_env;
     static const int direct_env = getenv("VS_TC_DIRECT") ? atoi(getenv("VS_TC_DIRECT")) : 0;
     pr.direct_lanes = direct_env ? direct_env : ((per >= 8 && per < 128) ? 16 : 33);
     KTimer kt_scan(ctx, timer_class);
