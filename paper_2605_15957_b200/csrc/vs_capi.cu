@@ -116,6 +116,8 @@ struct EnnJob {
     int64_t id_offset;
     const int64_t* id_map = nullptr;   // staged position -> base row (streamed chunks)
     bool narrow = false;               // 128-row tensor-core tiles (IVF coarse quantizer)
+    cudaEvent_t q_ready = nullptr;     // queries still being copied in (copy stream)
+    float* margin_todo = nullptr;      // SIMT margins to compute once the queries have landed
     // outputs (device, nullable)
     int64_t* out_ids;
     double* out_dist;
@@ -186,8 +188,24 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
     sp.ip = job.ip;
     sp.k = job.k;
     sp.tau_g = nullptr;
+    sp.q_ready = nullptr;
     const bool use_tc = ctx->opt_enn_kernel != 1 && vs::tc_supported(job.d, job.dtype, job.ip) &&
                         (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d));
+    if (job.q_ready) {
+        if (use_tc && cshift == 0) {
+            // the tensor-core path stages rows before it needs the queries and
+            // replaces the SIMT margins with its own
+            sp.q_ready = job.q_ready;
+        } else {
+            CK(cudaStreamWaitEvent(ctx->stream, job.q_ready, 0));
+        }
+    }
+    if (job.margin_todo && !(use_tc && cshift == 0)) {
+        if (sp.q_ready) CK(cudaStreamWaitEvent(ctx->stream, job.q_ready, 0));
+        CK(vs::launch_query_margins(job.q, job.nq, job.d, job.xmax, eps_simt(job.d), job.ip, job.margin_todo,
+                                    nullptr, ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
     bool exhaustive = false;
     {
         if (use_tc) {
@@ -314,6 +332,14 @@ int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bo
     CKS(arena_alloc(ctx, (size_t)m * job.d, &d_q));
     CKS(arena_alloc(ctx, (size_t)m, &d_m));
     CK(cudaMemcpyAsync(d_idx, which.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (job.margin_todo) {
+        // the tensor-core phase A skipped the SIMT margins (queries were still in
+        // flight then; they have landed since): the re-run needs them
+        CK(vs::launch_query_margins(job.q, job.nq, job.d, job.xmax, eps_simt(job.d), job.ip, job.margin_todo,
+                                    nullptr, ctx->stream));
+        margin = job.margin_todo;
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
     {
         int blocks = (int)std::min<int64_t>((m * job.d + 255) / 256, 4096);
         k_gather_queries<<<blocks, 256, 0, ctx->stream>>>(job.q, d_idx, m, job.d, d_q);
@@ -325,6 +351,8 @@ int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bo
     EnnJob sub = job;
     sub.q = d_q;
     sub.nq = m;
+    sub.q_ready = nullptr;
+    sub.margin_todo = nullptr;
     const int k = job.k;
     if (job.out_ids) CKS(arena_alloc(ctx, (size_t)m * k, &sub.out_ids));
     if (job.out_dist) CKS(arena_alloc(ctx, (size_t)m * k, &sub.out_dist));
@@ -735,7 +763,29 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     CK(ctx->arena.reset());
     std::vector<OutBuf> pending;
     const float* dq = nullptr;
-    CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+    // host queries of a large batch: copy them in on the copy stream while the
+    // filter and the row staging run (phase A waits on q_ready)
+    cudaEvent_t q_ready = nullptr;
+    {
+        cudaPointerAttributes at{};
+        const bool host_q = queries && cudaPointerGetAttributes(&at, queries) == cudaSuccess &&
+                            at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged;
+        cudaGetLastError();
+        if (host_q && !data->host_resident && (size_t)nq * d * 4 >= ((size_t)1 << 22)) {
+            float* buf = nullptr;
+            CKS(arena_alloc(ctx, (size_t)nq * d, &buf));
+            if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            if (!ctx->q_event) CK(cudaEventCreateWithFlags(&ctx->q_event, cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->q_event, ctx->stream));            // earlier work on the buffer
+            CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->q_event, 0));
+            CK(cudaMemcpyAsync(buf, queries, (size_t)nq * d * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
+            CK(cudaEventRecord(ctx->q_event, ctx->copy_stream));
+            q_ready = ctx->q_event;
+            dq = buf;
+        } else {
+            CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+        }
+    }
     int64_t* sel = nullptr;
     int64_t nsel = data->n;
     if (bitmap) {
@@ -749,10 +799,14 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     CKS(ensure_norms(col));
     float* margin = nullptr;
     CKS(arena_alloc(ctx, (size_t)nq, &margin));
-    CK(vs::launch_query_margins(dq, nq, d, col->max_norm_bits, eps_simt(d), metric, margin, nullptr,
-                                ctx->stream));
-    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    if (!q_ready) {
+        CK(vs::launch_query_margins(dq, nq, d, col->max_norm_bits, eps_simt(d), metric, margin, nullptr,
+                                    ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
     EnnJob job;
+    job.q_ready = q_ready;
+    job.margin_todo = q_ready ? margin : nullptr;
     job.q = dq;
     job.nq = nq;
     job.d = d;

@@ -129,7 +129,8 @@ struct vs_ctx {
     int64_t opt_stream_chunk = 0;    // host-resident search: selected rows per chunk (0 = auto)
     int64_t opt_ivf_chunk_rows = 0;  // tensor-core IVF scan: rows per list chunk (0 = 131072)
     int sm_reserve = 0;              // SMs left free by persistent kernels (streamed gathers)
-    cudaStream_t copy_stream = nullptr;   // host-resident search: gathers over PCIe
+    cudaStream_t copy_stream = nullptr;   // host-resident search: gathers over PCIe; query uploads
+    cudaEvent_t q_event = nullptr;        // queries landed (copy stream)
     // CUDA-event timing of kernel classes (resolved after each call's final sync)
     struct PendingTimer {
         int cls;

@@ -62,6 +62,8 @@ struct EnnScanParams {
     CandBuf cb;
     unsigned* tau_g = nullptr;  // tensor-core path: per-query global admission bound
     int verify = 0;             // phase A kept local top-k only: phase B must verify
+    cudaEvent_t q_ready = nullptr;  // nullable: queries still in flight (host->device on a copy
+                                    // stream); phase A stages the rows first, then waits
 };
 template <typename T>
 cudaError_t launch_enn_scan_simt(const EnnScanParams& p, cudaStream_t s);

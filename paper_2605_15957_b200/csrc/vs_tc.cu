@@ -1002,9 +1002,8 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     {
         KTimer kt(ctx, VS_K_STAGE);
         CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));
-        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-            sp.Q, nq, d, dp, qa, qerr);
-        CK(cudaGetLastError());
+        // rows first: they do not need the queries, whose host->device copy may
+        // still be in flight on the copy stream (sp.q_ready)
         const unsigned blocks = (unsigned)std::min<int64_t>((nsel * 32 + 255) / 256, 148 * 64);
         if (dtype == VS_DTYPE_F32)
             tc::k_stage_rows<float><<<blocks, 256, 0, st>>>((const float*)sp.X, sp.sel, nsel, d, dp, sp.xnorm, xb,
@@ -1012,6 +1011,10 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
         else
             tc::k_stage_rows<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)sp.X, sp.sel, nsel, d,
                                                                     dp, sp.xnorm, xb, sp.ip ? nullptr : xn, xmax2);
+        CK(cudaGetLastError());
+        if (sp.q_ready) CK(cudaStreamWaitEvent(st, sp.q_ready, 0));
+        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+            sp.Q, nq, d, dp, qa, qerr);
         CK(cudaGetLastError());
         tc::k_tc_margins<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qerr, nq, d, xmax, xmax2, sp.ip, margin);
         CK(cudaGetLastError());

@@ -86,3 +86,32 @@ def test_tc_duplicates_and_retry(tc_kernel):
     q = np.ones((130, 64), np.float32)
     nt = vs.enn_search(q, base, vs.SearchParams(k=40))
     assert_same(nt, O.enn_search(q, base, 40))
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 2])
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("force_retry", [0, 1])
+def test_large_host_query_batch_async_upload(kernel, pinned, force_retry):
+    """A >= 4 MB host query batch is copied in on the copy stream while the
+    filter and the row staging run; every phase-A kernel (and the re-run of
+    forced-overflow queries, which needs the deferred SIMT margins) must give
+    the reference result."""
+    import torch
+    rng = np.random.default_rng(70 + kernel)
+    n, d, nq, k = 12000, 1024, 1100, 20
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((nq, d)).astype(np.float32)
+    mask = rng.random(n) < 0.5
+    qin = torch.from_numpy(q).pin_memory() if pinned else q
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_ENN_KERNEL, kernel)
+    ctx.set_option(N.OPT_FORCE_RETRY, force_retry)
+    try:
+        nt = vs.enn_search(qin, data, vs.SearchParams(k=k), row_filter=mask)
+    finally:
+        ctx.set_option(N.OPT_ENN_KERNEL, 0)
+        ctx.set_option(N.OPT_FORCE_RETRY, 0)
+    idx = np.arange(0, nq, 37)
+    ref = O.enn_filtered(q[idx], data, mask, k)
+    assert np.array_equal(nt.data_row.reshape(nq, k)[idx].reshape(-1), ref.data_row)
+    assert np.array_equal(nt.distance.reshape(nq, k)[idx].reshape(-1), ref.distance)
