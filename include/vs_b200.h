@@ -240,6 +240,45 @@ int vs_bitmap_isin(vs_ctx* ctx, const int64_t* keys, int64_t n, const uint32_t* 
 int vs_bitmap_combine(vs_ctx* ctx, const uint32_t* a, const uint32_t* b, int64_t nwords,
                       int32_t op, uint32_t* out);
 
+/* ---- the step after the search ------------------------------
+ * All on the padded result layout the searches write ([nq][k_prime] ids and
+ * float64 distances, counts[nq] valid entries; counts may be NULL = k_prime).
+ *
+ * vs_postfilter replaces oversample_postfilter (vecsearch.py:155-202): per
+ * query, the first k results in rank order that satisfy every given keep
+ * condition (each nullable, ANDed):
+ *   keep_bits  packed bitmap over the n_data data rows (data-side predicates,
+ *              semi joins: vs_bitmap_compare / vs_bitmap_isin);
+ *   keep_pos   one byte per result slot [nq][k_prime] (any predicate over the
+ *              joined output);
+ *   data_key[data_row] <key_op> query_key[query] (cross-side comparison, e.g.
+ *              Q11's "im_imagekey_d != im_imagekey", plans.py:537; key_op as
+ *              vs_bitmap_compare).
+ * Writes out_ids/out_dist/out_rank [nq][k] (out_rank = the kept row's slot in
+ * k_prime, i.e. its vs_rank) and out_count[nq]; shortfall = k - out_count.
+ * A data row id outside [0, n_data) with keep_bits or data_key given is
+ * VS_ERR_PARAMETER.
+ *
+ * vs_results_flatten replaces the NeighborTable assembly (vecindex.py:95-106):
+ * the flat arrays sorted by (query, rank), query_row = query + query_offset,
+ * rank = rank[slot] (NULL: the slot). Outputs hold nq * k_prime entries;
+ * *n_out = the number written.
+ *
+ * vs_gather_rows is the column gather of build_vs_output (vecsearch.py:123-152):
+ * dst[i] = src[idx[i]] for rows of row_bytes bytes (any fixed-width column,
+ * embeddings included); an index outside [0, n_src) is VS_ERR_PARAMETER. */
+int vs_postfilter(vs_ctx* ctx, const int64_t* ids, const double* dist, const int32_t* counts,
+                  int64_t nq, int32_t k_prime, const uint32_t* keep_bits, const uint8_t* keep_pos,
+                  const int64_t* data_key, const int64_t* query_key, int32_t key_op, int64_t n_data,
+                  int32_t k, int64_t* out_ids, double* out_dist, int32_t* out_rank,
+                  int32_t* out_count);
+int vs_results_flatten(vs_ctx* ctx, const int64_t* ids, const double* dist, const int32_t* rank,
+                       const int32_t* counts, int64_t nq, int32_t k_prime, int64_t query_offset,
+                       int64_t* query_row, int64_t* data_row, double* distance, int64_t* out_rank,
+                       int64_t* n_out);
+int vs_gather_rows(vs_ctx* ctx, const void* src, int64_t n_src, int64_t row_bytes, const int64_t* idx,
+                   int64_t n, void* dst);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,7 @@ from .vecindex import (INNER_PRODUCT, NON_OWNING, OWNING, SQUARED_L2, FlatIndex,
                        IvfIndex, NeighborTable, SearchParams, enn_search, load_index, save_index)
 from .vecsearch import VsStats, oversample_postfilter, vector_search_operator  # noqa: F401
 from . import predicate  # noqa: F401,E402
+from . import output  # noqa: F401,E402
 
 __all__ = [
     "SearchParams", "NeighborTable", "enn_search", "FlatIndex", "IvfIndex", "save_index",

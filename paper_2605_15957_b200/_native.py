@@ -59,6 +59,11 @@ SIGNATURES = {
     "vs_bitmap_compare": (C.c_int, [_vp, _vp, _i32, _i64, _i32, C.c_double, _vp, _vp]),
     "vs_bitmap_isin": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64, _vp]),
     "vs_bitmap_combine": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "vs_postfilter": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _i64, _i32,
+                                _vp, _vp, _vp, _vp]),
+    "vs_results_flatten": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i64, _vp, _vp, _vp, _vp,
+                                     C.POINTER(_i64)]),
+    "vs_gather_rows": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "vs_topk_merge": (C.c_int, [_vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _i32,
                                 _vp, _vp, _vp]),
     "vs_ivf_create": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp,

@@ -1048,6 +1048,121 @@ int vs_bitmap_isin(vs_ctx* ctx, const int64_t* keys, int64_t n, const uint32_t* 
     return VS_OK;
 }
 
+// ---- after the search: post-filter, flat output table, row gather (vs_output.cu) -----
+int vs_postfilter(vs_ctx* ctx, const int64_t* ids, const double* dist, const int32_t* counts, int64_t nq,
+                  int32_t k_prime, const uint32_t* keep_bits, const uint8_t* keep_pos, const int64_t* data_key,
+                  const int64_t* query_key, int32_t key_op, int64_t n_data, int32_t k, int64_t* out_ids,
+                  double* out_dist, int32_t* out_rank, int32_t* out_count) {
+    if (!ctx || ((!ids || !dist) && nq > 0)) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (nq < 0 || k_prime < 0 || n_data < 0) return set_err(VS_ERR_PARAMETER, "negative size");
+    if (k < 1) return set_err(VS_ERR_PARAMETER, "k must be >= 1, got %d", k);
+    if (!data_key != !query_key) return set_err(VS_ERR_PARAMETER, "data_key and query_key go together");
+    if (data_key && (key_op < 0 || key_op > 5)) return set_err(VS_ERR_PARAMETER, "unknown comparison %d", key_op);
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    vs::PostfilterArgs a{};
+    const size_t slots = (size_t)nq * k_prime;
+    CKS(stage_in(ctx, ids, slots, &a.ids));
+    CKS(stage_in(ctx, dist, slots, &a.dist));
+    CKS(stage_in(ctx, counts, (size_t)nq, &a.counts));
+    CKS(stage_in(ctx, keep_bits, (size_t)(n_data + 31) / 32, &a.bitmap));
+    CKS(stage_in(ctx, keep_pos, slots, &a.keep_pos));
+    CKS(stage_in(ctx, data_key, (size_t)n_data, &a.data_key));
+    CKS(stage_in(ctx, query_key, (size_t)nq, &a.query_key));
+    a.nq = nq;
+    a.kp = k_prime;
+    a.key_op = key_op;
+    a.n_data = n_data;
+    a.k = k;
+    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &a.out_ids, pending));
+    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &a.out_dist, pending));
+    CKS(stage_out(ctx, out_rank, (size_t)nq * k, &a.out_rank, pending));
+    CKS(stage_out(ctx, out_count, (size_t)nq, &a.out_count, pending));
+    CKS(arena_alloc(ctx, 1, &a.bad));
+    CK(cudaMemsetAsync(a.bad, 0, sizeof(int), ctx->stream));
+    {
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_postfilter(a, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, a.bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CKS(flush_out(ctx, pending));
+    if (bad) return set_err(VS_ERR_PARAMETER, "data row id outside [0, %lld)", (long long)n_data);
+    return VS_OK;
+}
+
+int vs_results_flatten(vs_ctx* ctx, const int64_t* ids, const double* dist, const int32_t* rank,
+                       const int32_t* counts, int64_t nq, int32_t k_prime, int64_t query_offset,
+                       int64_t* query_row, int64_t* data_row, double* distance, int64_t* out_rank,
+                       int64_t* n_out) {
+    if (!ctx || !n_out || ((!ids || !dist) && nq > 0)) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (nq < 0 || k_prime < 0) return set_err(VS_ERR_PARAMETER, "negative size");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    vs::FlattenArgs a{};
+    const size_t slots = (size_t)nq * k_prime;
+    CKS(stage_in(ctx, ids, slots, &a.ids));
+    CKS(stage_in(ctx, dist, slots, &a.dist));
+    CKS(stage_in(ctx, rank, slots, &a.in_rank));
+    CKS(stage_in(ctx, counts, (size_t)nq, &a.counts));
+    a.nq = nq;
+    a.kp = k_prime;
+    a.query_offset = query_offset;
+    CKS(stage_out(ctx, query_row, slots, &a.query_row, pending));
+    CKS(stage_out(ctx, data_row, slots, &a.data_row, pending));
+    CKS(stage_out(ctx, distance, slots, &a.distance, pending));
+    CKS(stage_out(ctx, out_rank, slots, &a.rank, pending));
+    int64_t *c64 = nullptr, *off = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq + 1, &c64));
+    CKS(arena_alloc(ctx, (size_t)nq + 1, &off));
+    const size_t tb = vs::flatten_temp_bytes(nq);
+    char* tmp = nullptr;
+    CKS(arena_alloc(ctx, tb, &tmp));
+    {
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_flatten(a, c64, off, tmp, tb, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 3;
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, off + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto& o : pending) o.bytes = (size_t)total * 8;   // every flat column is 8 bytes wide
+    CKS(flush_out(ctx, pending));
+    *n_out = total;
+    return VS_OK;
+}
+
+int vs_gather_rows(vs_ctx* ctx, const void* src, int64_t n_src, int64_t row_bytes, const int64_t* idx, int64_t n,
+                   void* dst) {
+    if (!ctx || ((!src || !idx || !dst) && n > 0 && row_bytes > 0)) return set_err(VS_ERR_PARAMETER, "null argument");
+    if (n_src < 0 || row_bytes < 0 || n < 0) return set_err(VS_ERR_PARAMETER, "negative size");
+    DevGuard g(ctx->device);
+    CK(ctx->arena.reset());
+    std::vector<OutBuf> pending;
+    const char* dsrc = nullptr;
+    const int64_t* didx = nullptr;
+    CKS(stage_in(ctx, static_cast<const char*>(src), (size_t)(n_src * row_bytes), &dsrc));
+    CKS(stage_in(ctx, idx, (size_t)n, &didx));
+    char* ddst = nullptr;
+    CKS(stage_out(ctx, static_cast<char*>(dst), (size_t)(n * row_bytes), &ddst, pending));
+    int* bad = nullptr;
+    CKS(arena_alloc(ctx, 1, &bad));
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    {
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_gather(dsrc, n_src, row_bytes, didx, n, ddst, bad, ctx->stream));
+    }
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    int h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CKS(flush_out(ctx, pending));
+    if (h_bad) return set_err(VS_ERR_PARAMETER, "gather index outside [0, %lld)", (long long)n_src);
+    return VS_OK;
+}
+
 int vs_bitmap_combine(vs_ctx* ctx, const uint32_t* a, const uint32_t* b, int64_t nwords, int32_t op,
                       uint32_t* out) {
     if (!ctx || ((!a || !b || !out) && nwords > 0)) return set_err(VS_ERR_PARAMETER, "null argument");

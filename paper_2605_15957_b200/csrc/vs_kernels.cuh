@@ -235,6 +235,46 @@ cudaError_t launch_visited_count(const int32_t* probes, int64_t nq, int nprobe, 
 
 // ---- relational filters -> packed bitmaps (vs_predicate.cu) ------------------------------
 // vtype: 0 int32, 1 int64, 2 float32, 3 float64; op: 0 <, 1 <=, 2 ==, 3 !=, 4 >=, 5 >
+// ---- after the search (vs_output.cu): post-filter, flat output, row gather ----
+struct PostfilterArgs {
+    const int64_t* ids;        // [nq][kp] data rows
+    const double* dist;        // [nq][kp]
+    const int32_t* counts;     // [nq] valid entries per query (nullable: kp)
+    int64_t nq;
+    int kp;
+    const uint32_t* bitmap;    // keep: bit data_row set (nullable)
+    const uint8_t* keep_pos;   // keep: per result slot (nullable)
+    const int64_t* data_key;   // keep: data_key[data_row] <key_op> query_key[q] (nullable)
+    const int64_t* query_key;
+    int key_op;
+    int64_t n_data;            // bitmap bits / data_key length (row-id bound)
+    int k;
+    int64_t* out_ids;          // [nq][k]
+    double* out_dist;
+    int32_t* out_rank;         // original rank (slot in k') of each kept row
+    int32_t* out_count;        // [nq]
+    int* bad;                  // set when a data row id is out of range
+};
+struct FlattenArgs {
+    const int64_t* ids;
+    const double* dist;
+    const int32_t* in_rank;    // nullable: the slot index
+    const int32_t* counts;     // nullable: kp
+    int64_t nq;
+    int kp;
+    int64_t query_offset;
+    int64_t* query_row;        // [R] outputs (each nullable)
+    int64_t* data_row;
+    double* distance;
+    int64_t* rank;
+};
+cudaError_t launch_postfilter(const PostfilterArgs& a, cudaStream_t s);
+size_t flatten_temp_bytes(int64_t nq);
+cudaError_t launch_flatten(const FlattenArgs& a, int64_t* c64, int64_t* off, void* tmp, size_t tmp_bytes,
+                           cudaStream_t s);
+cudaError_t launch_gather(const void* src, int64_t n_src, int64_t row_bytes, const int64_t* idx, int64_t n,
+                          void* dst, int* bad, cudaStream_t s);
+
 cudaError_t launch_bitmap_compare(const void* values, int vtype, int64_t n, int op, double value,
                                   const uint32_t* valid, uint32_t* out, cudaStream_t s);
 size_t bitmap_isin_temp_bytes(int64_t nset);

@@ -407,8 +407,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                 // evict first; A is re-read for every tile: evict last.
                                 const int arows = !p.a32 ? BM : item.npairs <= 32 ? 32 : item.npairs <= 64 ? 64 : BM;
                                 mbar_expect_tx(&S.full[stage], STAGE_BYTES - A_BYTES + arows * BK * 2);
-                                tma_load_2d_hint(sa, arows == 32 ? &map_a32 : arows == 64 ? &map_a64 : &map_a,
-                                                 &S.full[stage], kb * BK, (int)item.a_row, pol_a);
+                                const CUtensorMap* ma = arows == 32 ? &map_a32 : arows == 64 ? &map_a64 : &map_a;
+                                // l2_hints 2: no hint on A; 3: evict-last, demoted to
+                                // evict-first on the unit's last tile (its last use)
+                                if (p.l2_hints == 2)
+                                    tma_load_2d(sa, ma, &S.full[stage], kb * BK, (int)item.a_row);
+                                else
+                                    tma_load_2d_hint(sa, ma, &S.full[stage], kb * BK, (int)item.a_row,
+                                                     (p.l2_hints == 3 && t + 1 == item.ntile) ? pol_b : pol_a);
                                 tma_load_2d_hint(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow, pol_b);
                             } else {
                                 mbar_expect_tx(&S.full[stage], STAGE_BYTES);
@@ -1283,7 +1289,8 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
     pr.pf_boxes = pf_env;
     pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
-    pr.l2_hints = 1;
+    static const int l2h_env = getenv("VS_TC_L2HINT") ? atoi(getenv("VS_TC_L2HINT")) : 1;
+    pr.l2_hints = l2h_env;
     static const int a32_env = getenv("VS_TC_A32") ? atoi(getenv("VS_TC_A32")) : 1;
     pr.a32 = a32_env;
     pr.pair_base = a.pair_base;

@@ -57,6 +57,47 @@ def capture_vs(query: str, ds):
     return run, calls
 
 
+def make_postfilter_golden():
+    from sqlvs.table import Schema, Table, embedding
+    from sqlvs.vecsearch import oversample_postfilter, vector_search_operator
+    r2 = np.random.default_rng(77)
+    nd, nq, d, kp, k = 400, 23, 16, 12, 4
+    data = r2.standard_normal((nd, d)).astype(np.float32)
+    qrows = r2.choice(nd, nq, replace=False)             # queries are data rows (self matches)
+    dkey = np.arange(nd, dtype=np.int64) * 3 + 1
+    dpart = r2.integers(0, 40, nd).astype(np.int64)
+    dval = r2.standard_normal(nd)
+    dt = Table(Schema([("key", "int64"), ("part", "int64"), ("val", "float64"), ("emb", embedding(d))]),
+               {"key": dkey, "part": dpart, "val": dval, "emb": EmbeddingColumn(data)})
+    qt = Table(Schema([("key", "int64"), ("qemb", embedding(d))]),
+               {"key": dkey[qrows], "qemb": EmbeddingColumn(data[qrows])})
+    out, _ = vector_search_operator(qt, "qemb", dt, "emb", SearchParams(k=k, k_prime=kp))
+    keep_parts = np.array([3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37], np.int64)
+    keep_set = Table(Schema([("p", "int64")]), {"p": keep_parts})
+    res = {"data": data, "qrows": qrows, "dkey": dkey, "dpart": dpart, "dval": dval,
+           "keep_parts": keep_parts, "kp": kp, "k": k,
+           "out_query_row": np.asarray(out.column("vs_query_row")),
+           "out_data_row": np.asarray(out.column("vs_data_row")),
+           "out_distance": np.asarray(out.column("vs_distance")),
+           "out_rank": np.asarray(out.column("vs_rank")),
+           "out_key_d": np.asarray(out.column("key_d")), "out_val": np.asarray(out.column("val"))}
+    cases = {
+        "self": dict(keep="key_d != key"),                              # Q11 (plans.py:537)
+        "semi": dict(keep=None, keep_set=keep_set, semi_keys=("part", "p")),   # Q15 (plans.py:574)
+        "rank": dict(keep="vs_rank >= 3"),
+        "both": dict(keep="key_d != key", keep_set=keep_set, semi_keys=("part", "p")),
+    }
+    for name, kw in cases.items():
+        kept, short = oversample_postfilter(out, kw.pop("keep"), k, **kw)
+        res[f"{name}_query_row"] = np.asarray(kept.column("vs_query_row"))
+        res[f"{name}_data_row"] = np.asarray(kept.column("vs_data_row"))
+        res[f"{name}_distance"] = np.asarray(kept.column("vs_distance"))
+        res[f"{name}_rank"] = np.asarray(kept.column("vs_rank"))
+        res[f"{name}_short_q"] = np.array(sorted(short), np.int64)
+        res[f"{name}_short_n"] = np.array([short[q] for q in sorted(short)], np.int64)
+    np.savez_compressed(HERE / "postfilter.npz", **res)
+
+
 def main():
     meta = {}
     # --- synth pins ---------------------------------------------------------
@@ -182,9 +223,17 @@ def main():
     save_index(idx, HERE / "svix_ivf_owning.bin")
     meta["svix_seed"] = 5
 
+    # --- the step after the search: vector_search_operator + oversample_postfilter
+    # (vecsearch.py:64-202) on small tables: Q11's cross-side "key_d != key",
+    # Q15's semi join, a rank predicate, shortfalls (k' rows that do not survive)
+    make_postfilter_golden()
+
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print("golden fixtures written to", HERE)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["postfilter"]:
+        make_postfilter_golden()
+    else:
+        main()

@@ -112,3 +112,21 @@ def test_config1_sample(golden):
     res = O.enn_filtered(q[g["queries_idx"]], emb, mask, 10)
     assert np.array_equal(res.data_row.reshape(-1, 10), g["ids"])
     assert np.array_equal(res.distance.reshape(-1, 10), g["dist"])
+
+
+def test_postfilter(golden):
+    """oversample_postfilter over the reference's own vector_search_operator
+    output (Q11 self-match exclusion, Q15 semi join, rank predicate, both)."""
+    g = golden("postfilter.npz")
+    qr, rank = g["out_query_row"], g["out_rank"]
+    self_mask = g["out_key_d"] != g["dkey"][g["qrows"]][qr]
+    semi_mask = np.isin(g["dpart"][g["out_data_row"]], g["keep_parts"])
+    masks = {"self": self_mask, "semi": semi_mask, "rank": rank >= 3, "both": self_mask & semi_mask}
+    for name, m in masks.items():
+        kept, short = O.oversample_postfilter(qr, m, int(g["k"]))
+        assert np.array_equal(qr[kept], g[f"{name}_query_row"]), name
+        assert np.array_equal(g["out_data_row"][kept], g[f"{name}_data_row"]), name
+        assert np.array_equal(g["out_distance"][kept], g[f"{name}_distance"]), name
+        assert np.array_equal(rank[kept], g[f"{name}_rank"]), name
+        assert sorted(short) == g[f"{name}_short_q"].tolist(), name
+        assert [short[q] for q in sorted(short)] == g[f"{name}_short_n"].tolist(), name
