@@ -685,6 +685,14 @@ class IvfWorkload:
             uniq = uniq[self.owned[uniq] == 1]
         s = 4 if self.index_dtype == "f32" else 2
         self.unique_lists = int(uniq.size)
+        # probe skew: lists probed by more queries than one query tile (128)
+        # are scanned once per tile
+        pairs = np.bincount(np.asarray(probes).ravel(), minlength=len(self.list_sizes))
+        passes = np.ceil(pairs[uniq] / 128.0)
+        rows = self.sel_per_list[uniq]
+        self.list_pairs = {"mean": round(float(pairs[uniq].mean()), 1), "p99": int(np.percentile(pairs[uniq], 99)),
+                           "max": int(pairs.max()),
+                           "row_passes": round(float(np.sum(passes * rows) / max(np.sum(rows), 1)), 4)}
         bitmap = self.list_sizes[uniq] / 8.0 if self.bits is not None else 0.0
         return float(np.sum(bitmap + self.sel_per_list[uniq] * self.d * s))
 
@@ -707,6 +715,7 @@ class IvfWorkload:
         return {"workload": c["name"], "n_rows": c["n"], "dim": self.d, "queries": self.nq, "k": self.k,
                 "nlist": c["nlist"], "nprobe": self.nprobe, "selectivity": c["sel"],
                 "n_selected": self.n_sel_total, "unique_probed_lists": getattr(self, "unique_lists", None),
+                "pairs_per_list": getattr(self, "list_pairs", None),
                 "build_s": round(self.build_s, 2),
                 "list_rows": {"mean": round(float(np.mean(self.list_sizes)), 1),
                               "p99": int(np.percentile(self.list_sizes, 99)),

@@ -111,7 +111,9 @@ struct Params {
     int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
     int64_t chunk_rows;             // MODE 2: rows per list chunk (0: whole lists)
     int l2_hints;                   // MODE 2: L2 evict-first for B, evict-last for A (always on)
-    int a32;                        // MODE 2: map_a32 (32-row A boxes) is valid
+    int a32;                        // MODE 2 A boxes: 0 full 128 rows; 1 32/64-row boxes;
+                                    // 2 (default) spread: <= 64 pairs as four 8/16-row boxes, one per TMEM lane quadrant
+                                    // (measured: 15.5 -> 14.7 ms on config 4)
     int lim0;                       // first compaction point (0: 2k + 64)
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
     int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
@@ -405,16 +407,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                 // the MMA's other A rows hold stale data whose accumulator
                                 // rows the epilogue ignores). B (the payload) streams once:
                                 // evict first; A is re-read for every tile: evict last.
-                                const int arows = !p.a32 ? BM : item.npairs <= 32 ? 32 : item.npairs <= 64 ? 64 : BM;
-                                mbar_expect_tx(&S.full[stage], STAGE_BYTES - A_BYTES + arows * BK * 2);
-                                const CUtensorMap* ma = arows == 32 ? &map_a32 : arows == 64 ? &map_a64 : &map_a;
-                                // l2_hints 2: no hint on A; 3: evict-last, demoted to
-                                // evict-first on the unit's last tile (its last use)
-                                if (p.l2_hints == 2)
-                                    tma_load_2d(sa, ma, &S.full[stage], kb * BK, (int)item.a_row);
-                                else
-                                    tma_load_2d_hint(sa, ma, &S.full[stage], kb * BK, (int)item.a_row,
-                                                     (p.l2_hints == 3 && t + 1 == item.ntile) ? pol_b : pol_a);
+                                if (p.a32 == 2 && item.npairs <= 64) {
+                                    // spread: quarter q of the unit's pairs (8 or 16 rows)
+                                    // lands in TMEM lane quadrant q, so all four epilogue
+                                    // lane quadrants (SMSPs) share the appends
+                                    const int qb = item.npairs <= 32 ? 8 : 16;
+                                    mbar_expect_tx(&S.full[stage], STAGE_BYTES - A_BYTES + 4 * qb * BK * 2);
+                                    const CUtensorMap* ma = qb == 8 ? &map_a32 : &map_a64;
+#pragma unroll
+                                    for (int qd = 0; qd < 4; ++qd)
+                                        tma_load_2d_hint(sa + qd * 32 * BK * 2, ma, &S.full[stage], kb * BK,
+                                                         (int)item.a_row + qd * qb, pol_a);
+                                } else {
+                                    const int arows = !p.a32 ? BM : item.npairs <= 32 ? 32 : item.npairs <= 64 ? 64 : BM;
+                                    mbar_expect_tx(&S.full[stage], STAGE_BYTES - A_BYTES + arows * BK * 2);
+                                    const CUtensorMap* ma = arows == 32 ? &map_a32 : arows == 64 ? &map_a64 : &map_a;
+                                    tma_load_2d_hint(sa, ma, &S.full[stage], kb * BK, (int)item.a_row, pol_a);
+                                }
                                 tma_load_2d_hint(sa + A_BYTES, &map_b, &S.full[stage], kb * BK, brow, pol_b);
                             } else {
                                 mbar_expect_tx(&S.full[stage], STAGE_BYTES);
@@ -559,8 +568,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // of work item `item`; false for padding rows
         auto row_query = [&](const Item& item, int64_t& q, int64_t& sub) -> bool {
             if (MODE == 2) {
-                if (row >= item.npairs) return false;
-                const int code = __ldg(p.pair_codes + item.a_row + row);
+                int pr = row;
+                if (p.a32 == 2 && item.npairs <= 64) {   // spread placement (producer)
+                    const int qb = item.npairs <= 32 ? 8 : 16;
+                    const int li = row & 31;
+                    if (li >= qb) return false;
+                    pr = (row >> 5) * qb + li;
+                }
+                if (pr >= item.npairs) return false;
+                const int code = __ldg(p.pair_codes + item.a_row + pr);
                 q = code / p.nprobe;
                 // flat buffer index with list chunks, else the sub of (query, probe rank)
                 sub = p.pair_base ? __ldg(p.pair_base + code) + 2 * item.chunk + half
@@ -1256,11 +1272,12 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     CK(cudaMemsetAsync(c.overflow, 0, a.nq * sizeof(int), st));
     CK(cudaMemsetAsync(c.cnt, 0, (size_t)nbuf * sizeof(int), st));
     CUtensorMap ma, mb;
+    static const int a32_env = getenv("VS_TC_A32") ? atoi(getenv("VS_TC_A32")) : 2;
     CUtensorMap ma32, ma64;
     if (!make_map(&ma, qp, std::max<int64_t>(a.npairs, 1), d, dp, tc::BM) ||
         !make_map(&mb, a.payload, a.n_total, d, d, tc::BN) ||
-        !make_map(&ma32, qp, std::max<int64_t>(a.npairs, 1), d, dp, 32) ||
-        !make_map(&ma64, qp, std::max<int64_t>(a.npairs, 1), d, dp, 64))
+        !make_map(&ma32, qp, std::max<int64_t>(a.npairs, 1), d, dp, a32_env == 2 ? 8 : 32) ||
+        !make_map(&ma64, qp, std::max<int64_t>(a.npairs, 1), d, dp, a32_env == 2 ? 16 : 64))
         return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     tc::Params pr{};
     pr.nq = a.nq;
@@ -1289,9 +1306,7 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
     pr.pf_boxes = pf_env;
     pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
-    static const int l2h_env = getenv("VS_TC_L2HINT") ? atoi(getenv("VS_TC_L2HINT")) : 1;
-    pr.l2_hints = l2h_env;
-    static const int a32_env = getenv("VS_TC_A32") ? atoi(getenv("VS_TC_A32")) : 1;
+    pr.l2_hints = 1;
     pr.a32 = a32_env;
     pr.pair_base = a.pair_base;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.max_units, ctx->sm_count));
