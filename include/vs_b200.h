@@ -69,12 +69,13 @@ enum vs_kernel_class {
     VS_K_SELECT = 0,      /* bitmap -> selection vector / permuted bitmap       */
     VS_K_ENN_SCAN = 1,    /* phase A of the exhaustive search                   */
     VS_K_RERANK = 2,      /* phase B (exact float64 re-rank + top-k)            */
-    VS_K_COARSE = 3,      /* IVF coarse quantizer (phase A + B over centroids)  */
+    VS_K_COARSE = 3,      /* IVF coarse quantizer, phase A over the centroids   */
     VS_K_IVF_SCAN = 4,    /* IVF list scan (phase A)                            */
     VS_K_IVF_RERANK = 5,  /* IVF phase B                                        */
     VS_K_MERGE = 6,       /* cross-shard merge                                  */
     VS_K_STAGE = 7,       /* tensor-core operand staging (bf16 compaction)      */
-    VS_K_N = 8
+    VS_K_COARSE_RERANK = 8, /* IVF coarse quantizer, exact phase B (probes)     */
+    VS_K_N = 9
 };
 
 /* counters (vs_ctx_stats) */

@@ -26,7 +26,8 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 OPT_ENN_KERNEL, OPT_IVF_KERNEL, OPT_CAND_SLACK, OPT_FORCE_RETRY, OPT_TIMING = 1, 2, 3, 4, 5
 OPT_STREAM_CHUNK = 6
 OPT_IVF_CHUNK_ROWS = 7
-KERNEL_CLASSES = ("select", "enn_scan", "rerank", "coarse", "ivf_scan", "ivf_rerank", "merge", "stage")
+KERNEL_CLASSES = ("select", "enn_scan", "rerank", "coarse", "ivf_scan", "ivf_rerank", "merge", "stage",
+                  "coarse_rerank")
 STAT_LAUNCHES, STAT_OVERFLOW_QUERIES, STAT_SURVIVORS, STAT_LAST_ENN_KERNEL = 0, 1, 2, 3
 
 _vp = C.c_void_p
@@ -190,9 +191,10 @@ class Context:
 
     def kernel_times(self, reset: bool = False) -> dict:
         """{class: (total_ns, launches)} of CUDA-event-timed kernel classes."""
-        ns = np.zeros(8, np.int64)
-        cnt = np.zeros(8, np.int64)
-        check(load().vs_ctx_kernel_times(self.handle, ns.ctypes.data, cnt.ctypes.data, 8, int(reset)))
+        n = len(KERNEL_CLASSES)
+        ns = np.zeros(n, np.int64)
+        cnt = np.zeros(n, np.int64)
+        check(load().vs_ctx_kernel_times(self.handle, ns.ctypes.data, cnt.ctypes.data, n, int(reset)))
         return {name: (int(ns[i]), int(cnt[i])) for i, name in enumerate(KERNEL_CLASSES)}
 
     def stats(self) -> list:

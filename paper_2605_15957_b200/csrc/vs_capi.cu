@@ -1787,7 +1787,7 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     cj.out_ids32 = probes;
     cj.out_count = nullptr;
     cj.cls_scan = VS_K_COARSE;
-    cj.cls_rerank = VS_K_COARSE;
+    cj.cls_rerank = VS_K_COARSE_RERANK;
     cj.narrow = !getenv("VS_COARSE_WIDE");
     CKS(run_enn(ctx, cj, cm, 0, false));
     }

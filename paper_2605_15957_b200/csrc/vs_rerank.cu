@@ -614,9 +614,46 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     if (p.ext_thr && ext_o != f2o(__int_as_float(0x7f800000))) pre = min(pre, f2o(__fadd_ru(p.ext_thr[q], p.margin[q])));
 
     RR_MARK(0);
-    // 0. live candidates -> shared memory (one warp per buffer, coalesced)
     float* lkey = reinterpret_cast<float*>(u);
     uint32_t* lpos = reinterpret_cast<uint32_t*>(u + LCAP * 4);
+    // -1. more candidates than shared memory holds (e.g. exhaustive buffers of
+    //    short splits): bound the union's k-th key from above by the k-th key
+    //    of a subset — the first m keys of every buffer — and tighten the live
+    //    filter to that bound + margin. The k smallest keys and every key within
+    //    the margin of the k-th stay live, so the result is unchanged.
+    if (tot > LCAP && tot > p.k) {
+        const int m = max(1, (LCAP / 2) / max(nsub, 1));
+        if (tid == 0) sm.counter = 0;
+        __syncthreads();
+        for (int s = w; s < nsub; s += NWARP) {
+            const int cs = min(cnts[s], m);
+            const float* bk = ckey + (int64_t)s * C;
+            for (int j = lane; j - lane < cs; j += 32) {
+                const float kv = j < cs ? bk[j] : 0.f;
+                const bool live = j < cs && f2o(kv) <= pre;
+                const unsigned b = __ballot_sync(VS_FULL, live);
+                if (!b) continue;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
+                base = __shfl_sync(VS_FULL, base, 0);
+                const int slot = base + __popc(b & lanemask_lt());
+                if (live && slot < LCAP) lkey[slot] = kv;
+            }
+        }
+        __syncthreads();
+        const int nsamp = min(sm.counter, LCAP);
+        __syncthreads();
+        if (nsamp >= p.k) {
+            const uint32_t kth_s = block_radix_kth(
+                [&](auto fn) {
+                    for (int i = tid; i < nsamp; i += NT) fn(f2o(lkey[i]));
+                },
+                (unsigned)p.k, hist, sm);
+            pre = min(pre, f2o(__fadd_ru(o2f(kth_s), p.margin[q])));
+        }
+        __syncthreads();
+    }
+    // 0. live candidates -> shared memory (one warp per buffer, coalesced)
     if (tid == 0) sm.counter = 0;
     __syncthreads();
     for (int s = w; s < nsub; s += NWARP) {
@@ -657,6 +694,12 @@ __global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
     __syncthreads();
     const int nl = sm.counter;
     __syncthreads();
+#ifdef VS_RERANK_PROFILE
+    if (tid == 0) {
+        atomicAdd(&g_rr_prof[5], (unsigned long long)tot);   // candidates in the buffers
+        atomicAdd(&g_rr_prof[6], (unsigned long long)nl);    // live (key <= pre)
+    }
+#endif
     int64_t ns = 0;
     if (nl <= LCAP) {
         RR_MARK(1);

@@ -35,5 +35,4 @@ names = ["setup", "gather", "select", "score", "topk"]
 ctas = wl.nq * steps * (2 if "nlist" in conf else 1)
 for i, n in enumerate(names):
     print(f"{n:8s} {buf[i] / ctas:12.0f} cycles/CTA")
-if buf[6]:
-    print(f"score fn {buf[5] / buf[6]:12.0f} cycles/row (warp 0, includes waiting on the row loads)")
+print(f"candidates {buf[5] / ctas:10.0f} per CTA, live (key <= pre) {buf[6] / ctas:10.0f}")
