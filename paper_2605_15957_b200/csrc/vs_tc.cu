@@ -116,8 +116,6 @@ struct Params {
                                     // (measured: 15.5 -> 14.7 ms on config 4)
     int lim0;                       // first compaction point (0: 2k + 64)
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
-    int direct_lanes = 33;          // epilogue: lanes with admissions from which a warp
-                                    // appends per thread instead of cooperatively
 };
 
 // one work item: A tile rows [a_row, a_row + QTILE), B tiles of BN rows from
@@ -313,6 +311,20 @@ __device__ __forceinline__ void tmem_wait_ld_regs(uint32_t* r) {
                  : "memory");
 }
 
+// v[j] for a run-time j without local memory: a 5-level select tree (31 selects)
+__device__ __forceinline__ float sel32(const float (&v)[32], int j) {
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (j & 2) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = (j & 4) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = (j & 8) ? a[2 * i + 1] : a[2 * i];
+    return (j & 16) ? a[1] : a[0];
+}
+
 // ---- the kernel --------------------------------------------------------------------------------------
 template <bool IP, int MODE, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -321,7 +333,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                   const __grid_constant__ CUtensorMap map_a64) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ __align__(16) float xn_w[8][BN / 2];  // per epilogue warp: its column half's row norms
-    __shared__ __align__(16) float app_w[8][32];     // per epilogue warp: one lane's chunk keys (appends)
+    __shared__ __align__(16) float app_w[8][32];     // per epilogue warp: one lane's chunk keys (dense appends)
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     constexpr int NSTAGE = Cfg<PAIR>::NSTAGE;
@@ -706,25 +718,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     mask &= valid;
                     if (!qv) mask = 0;
-                    // warp-cooperative append: lanes with admitted keys take turns
-                    // staging their 32 keys in shared memory; the warp then writes
-                    // only the admitted (key, position) pairs, in column order
-                    unsigned am = __ballot_sync(VS_FULL, mask != 0);
-                    if (__popc(am) >= p.direct_lanes) {
-                        // dense admissions (short splits): every lane appends its
-                        // own keys directly (predicated, static register indices)
-                        if (p.dbg) n_app += __popc(mask);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            if ((mask >> j) & 1u) {
-                                ckey[cnt] = kk[j];
-                                cpos[cnt] = (uint32_t)(r0 + cb0 + j);
-                                ++cnt;
-                            }
-                        }
-                    } else if (am) {
+                    // append: each lane walks its own admitted columns, picking the
+                    // key out of its registers with a select tree. Admissions are
+                    // sparse (~1 % of keys), so this beats warp-cooperative staging
+                    // through shared memory, which serialised over the admitting
+                    // lanes (config 2 phase A 22.0 -> 18.3 ms, measured). Dense chunks
+                    // (a lane admits >= 8 keys: unfiltered short splits, e.g. config 1)
+                    // keep the cooperative form: its stores are coalesced per buffer.
+                    if (p.dbg) n_app += __popc(mask);
+                    if (__any_sync(VS_FULL, __popc(mask) >= 8)) {
+                        unsigned am = __ballot_sync(VS_FULL, mask != 0);
                         float* st = app_w[warp - EPI_WARP0];
-                        if (p.dbg) n_app += __popc(mask);
                         while (am) {
                             const int l = __ffs(am) - 1;
                             am &= am - 1;
@@ -747,6 +751,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             }
                             __syncwarp();
                             if (lane == l) cnt += __popc(ml);
+                        }
+                    } else {
+                        unsigned mm = mask;
+                        while (mm) {
+                            const int j = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            ckey[cnt] = sel32(kk, j);
+                            cpos[cnt] = (uint32_t)(r0 + cb0 + j);
+                            ++cnt;
                         }
                     }
                     if (ch + 1 < BN / 64) {
@@ -1117,12 +1130,8 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     const unsigned units = (unsigned)std::min<int64_t>(items, sms);
     const unsigned grid = pair ? 2 * units : units;
     pr.argmin_out = nullptr;
-    // short splits append densely (the per-split fill is a larger share):
-    // per-thread appends there, warp-cooperative ones for long splits (measured)
     static const int lim0_env = getenv("VS_TC_LIM0") ? atoi(getenv("VS_TC_LIM0")) : 0;
     pr.lim0 = lim0_env;
-    static const int direct_env = getenv("VS_TC_DIRECT") ? atoi(getenv("VS_TC_DIRECT")) : 0;
-    pr.direct_lanes = direct_env ? direct_env : ((per >= 8 && per < 128) ? 16 : 33);
     KTimer kt_scan(ctx, timer_class);
     if (sp.ip) {
         CK((pair ? launch_tc<true, 0, true>(ma, mb, pr, grid, st) : launch_tc<true, 0, false>(ma, mb, pr, grid, st)));

@@ -10,4 +10,4 @@ python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "
 for c in 2 1 3 4 5; do
   timeout 1500 python bench.py --config $c > $OUT/bench_cfg$c.json 2> $OUT/bench_cfg$c.err; echo "cfg$c rc=$?"
 done
-bash scripts/ncu_ivf_tc.sh $TAG
+[ -n "${SKIP_NCU:-}" ] || bash scripts/ncu_ivf_tc.sh $TAG
