@@ -139,64 +139,81 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // buffer (`*overflow` = 1).
 //
 // Buffers of up to 32 x REG_PER_LANE entries are compacted from registers
-// (one load of the keys, then a 32-step bitwise binary search on the
-// register copy); larger buffers fall back to streaming the keys.
+// (one load of the keys into 8, 16 or 32 registers per lane, then a bisection
+// over the live keys' [min, max] on the register copy); larger buffers fall
+// back to streaming the keys.
 constexpr int COMPACT_REG_PER_LANE = 32;
+
+// register-resident compaction of n <= 32 * R entries
+template <int R>
+__device__ __forceinline__ int warp_compact_reg(float* keys, uint32_t* pos, int n, int k, float margin,
+                                                int limit, float* thr, int* overflow) {
+    const int lane = threadIdx.x & 31;
+    // one coalesced load of keys and positions, then selection, counting and
+    // compaction without further memory reads
+    uint32_t ko[R];
+    uint32_t po[R];
+    uint32_t vmin = 0xffffffffu, vmax = 0u;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int j = lane + 32 * i;
+        ko[i] = (j < n) ? f2o(keys[j]) : 0xffffffffu;
+        po[i] = (j < n) ? pos[j] : 0u;
+        if (j < n) {
+            vmin = min(vmin, ko[i]);
+            vmax = max(vmax, ko[i]);
+        }
+    }
+    // the k-th smallest lies in [min, max] of the live keys: bisect only that range
+    uint32_t lo = __reduce_min_sync(VS_FULL, vmin);
+    uint32_t hi = n >= k ? __reduce_max_sync(VS_FULL, vmax) : 0xffffffffu;
+    while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) c += (ko[i] <= mid);
+        c = warp_sum(c);  // padding (0xffffffff) only counts at the very top
+        if (c >= k) hi = mid; else lo = mid + 1;
+    }
+    const float kth = o2f(lo);
+    uint32_t to = f2o(__fadd_ru(kth, margin));
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) c += (ko[i] <= to);
+    c = warp_sum(c);
+    if (c > limit) {  // margin set cannot fit: keep the k-th bound, flag a re-run
+        *overflow = 1;
+        to = lo;
+        c = 0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) c += (ko[i] <= to);
+        c = warp_sum(c);
+        if (c > limit) c = limit;
+    }
+    __syncwarp();
+    int base = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const bool keep = ko[i] <= to;   // entries are in position order: i-major
+        const unsigned b = __ballot_sync(VS_FULL, keep);
+        const int dst = base + __popc(b & lanemask_lt());
+        if (keep && dst < limit) {
+            keys[dst] = o2f(ko[i]);
+            pos[dst] = po[i];
+        }
+        base += __popc(b);
+    }
+    *thr = o2f(to);
+    return min(base, limit);
+}
 
 __device__ __forceinline__ int warp_compact(float* keys, uint32_t* pos, int n, int k, float margin,
                                             int limit, float* thr, int* overflow) {
     const int lane = threadIdx.x & 31;
-    if (n <= 32 * COMPACT_REG_PER_LANE) {
-        // register-resident: one coalesced load of keys and positions, then
-        // selection, counting and compaction without further memory reads
-        uint32_t ko[COMPACT_REG_PER_LANE];
-        uint32_t po[COMPACT_REG_PER_LANE];
-#pragma unroll
-        for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) {
-            const int j = lane + 32 * i;
-            ko[i] = (j < n) ? f2o(keys[j]) : 0xffffffffu;
-            po[i] = (j < n) ? pos[j] : 0u;
-        }
-        uint32_t lo = 0u, hi = 0xffffffffu;
-        while (lo < hi) {
-            const uint32_t mid = lo + ((hi - lo) >> 1);
-            int c = 0;
-#pragma unroll
-            for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) c += (ko[i] <= mid);
-            c = warp_sum(c);  // padding (0xffffffff) only counts at the very top
-            if (c >= k) hi = mid; else lo = mid + 1;
-        }
-        const float kth = o2f(lo);
-        uint32_t to = f2o(__fadd_ru(kth, margin));
-        int c = 0;
-#pragma unroll
-        for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) c += (ko[i] <= to);
-        c = warp_sum(c);
-        if (c > limit) {  // margin set cannot fit: keep the k-th bound, flag a re-run
-            *overflow = 1;
-            to = lo;
-            c = 0;
-#pragma unroll
-            for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) c += (ko[i] <= to);
-            c = warp_sum(c);
-            if (c > limit) c = limit;
-        }
-        __syncwarp();
-        int base = 0;
-#pragma unroll
-        for (int i = 0; i < COMPACT_REG_PER_LANE; ++i) {
-            const bool keep = ko[i] <= to;   // entries are in position order: i-major
-            const unsigned b = __ballot_sync(VS_FULL, keep);
-            const int dst = base + __popc(b & lanemask_lt());
-            if (keep && dst < limit) {
-                keys[dst] = o2f(ko[i]);
-                pos[dst] = po[i];
-            }
-            base += __popc(b);
-        }
-        *thr = o2f(to);
-        return min(base, limit);
-    }
+    if (n <= 32 * 8) return warp_compact_reg<8>(keys, pos, n, k, margin, limit, thr, overflow);
+    if (n <= 32 * 16) return warp_compact_reg<16>(keys, pos, n, k, margin, limit, thr, overflow);
+    if (n <= 32 * COMPACT_REG_PER_LANE)
+        return warp_compact_reg<COMPACT_REG_PER_LANE>(keys, pos, n, k, margin, limit, thr, overflow);
     uint32_t lo = 0u, hi = 0xffffffffu;
     while (lo < hi) {
         const uint32_t mid = lo + ((hi - lo) >> 1);

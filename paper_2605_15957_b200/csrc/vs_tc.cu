@@ -115,6 +115,7 @@ struct Params {
                                     // 2 (default) spread: <= 64 pairs as four 8/16-row boxes, one per TMEM lane quadrant
                                     // (measured: 15.5 -> 14.7 ms on config 4)
     int lim0;                       // first compaction point (0: 2k + 64)
+    int dense_direct;               // epilogue: dense chunks append per lane (else cooperatively)
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
 };
 
@@ -723,10 +724,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     // sparse (~1 % of keys), so this beats warp-cooperative staging
                     // through shared memory, which serialised over the admitting
                     // lanes (config 2 phase A 22.0 -> 18.3 ms, measured). Dense chunks
-                    // (a lane admits >= 8 keys: unfiltered short splits, e.g. config 1)
-                    // keep the cooperative form: its stores are coalesced per buffer.
+                    // (a lane admits >= 8 keys) append from static register indices
+                    // (splits of 8..127 tiles, measured) or cooperatively with
+                    // coalesced stores (one-tile splits, e.g. config 1).
                     if (p.dbg) n_app += __popc(mask);
-                    if (__any_sync(VS_FULL, __popc(mask) >= 8)) {
+                    const bool dense = __any_sync(VS_FULL, __popc(mask) >= 8);
+                    if (dense && p.dense_direct) {
+                        // dense, longer splits (e.g. the coarse quantizer's first
+                        // tiles): every lane appends its own keys, static indices
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if ((mask >> j) & 1u) {
+                                ckey[cnt] = kk[j];
+                                cpos[cnt] = (uint32_t)(r0 + cb0 + j);
+                                ++cnt;
+                            }
+                        }
+                    } else if (dense) {
                         unsigned am = __ballot_sync(VS_FULL, mask != 0);
                         float* st = app_w[warp - EPI_WARP0];
                         while (am) {
@@ -1132,6 +1146,7 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     pr.argmin_out = nullptr;
     static const int lim0_env = getenv("VS_TC_LIM0") ? atoi(getenv("VS_TC_LIM0")) : 0;
     pr.lim0 = lim0_env;
+    pr.dense_direct = (per >= 8 && per < 128) ? 1 : 0;
     KTimer kt_scan(ctx, timer_class);
     if (sp.ip) {
         CK((pair ? launch_tc<true, 0, true>(ma, mb, pr, grid, st) : launch_tc<true, 0, false>(ma, mb, pr, grid, st)));
@@ -1316,6 +1331,7 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     pr.pf_boxes = pf_env;
     pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
     pr.l2_hints = 1;
+    pr.dense_direct = 0;
     pr.a32 = a32_env;
     pr.pair_base = a.pair_base;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.max_units, ctx->sm_count));
