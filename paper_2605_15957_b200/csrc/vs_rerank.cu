@@ -26,12 +26,15 @@ namespace {
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
 constexpr int KMAX = 2048;      // == vs_topk_cap(): sort capacity
-constexpr int LCAP = 8192;      // live candidates staged in shared memory per query
+// live candidates staged in shared memory per query: the wide build (large k)
+// stages 8192 at 2 CTAs/SM, the narrow one 4096 at 3 CTAs/SM
+template <bool WIDE> constexpr int lcap() { return WIDE ? 8192 : 4096; }
 constexpr int MAXLEAF = 32;     // numpy pairwise leaves (>= 64 elements each) -> d <= 2048 on the warp path
 constexpr int WARP_D_MAX = 2048;
 // union of: live candidates (LCAP x 8 B), staged rows (NWARP x d x 4 B),
 // sort buffers (KMAX x 16 B)
-constexpr size_t UNION_BYTES = 65536;
+constexpr size_t UNION_BYTES = 32768;   // narrow build; the wide one doubles it
+template <bool WIDE> constexpr size_t union_min() { return WIDE ? 2 * UNION_BYTES : UNION_BYTES; }
 // staged row stride (elements): padded d plus the leaf skews (32 B per leaf;
 // leaves hold >= 64 elements, so at most d / 64 + 1 of them)
 __host__ __device__ __forceinline__ int row_stride(int d) { return ((d + 7) & ~7) + 16 * (d / 64 + 1); }
@@ -47,9 +50,10 @@ inline int np_nleaf(int n) {
 // register path of the exact scorer: every lane owns two chains of one leaf
 // for the whole row (<= 8 leaves), rows read straight from global memory
 inline bool reg_path_ok(int d) { return d >= 8 && d <= 1024 && d % 2 == 0 && np_nleaf(d) <= 8; }
-inline size_t union_bytes(int d) {
+inline size_t union_bytes(int d, bool wide) {
     const size_t rows = (size_t)NWARP * 2 * (size_t)row_stride(d) * 4;   // two staged rows per warp
-    return (d <= WARP_D_MAX && !reg_path_ok(d) && rows > UNION_BYTES) ? rows : UNION_BYTES;
+    const size_t base = wide ? union_min<true>() : union_min<false>();
+    return (d <= WARP_D_MAX && !reg_path_ok(d) && rows > base) ? rows : base;
 }
 
 constexpr int HBINS = 2048;     // radix-select histogram bins (11 bits)
@@ -554,17 +558,19 @@ __device__ unsigned long long g_rr_prof[8];
 #define RR_MARK(i) do {} while (0)
 #endif
 
-template <typename T, bool IP>
-__global__ void __launch_bounds__(NT, 2) k_rerank(RerankParams p) {
+template <typename T, bool IP, bool WIDE>
+__global__ void __launch_bounds__(NT, WIDE ? 2 : 3) k_rerank(RerankParams p) {
+    constexpr int LCAP = lcap<WIDE>();
 #ifdef VS_RERANK_PROFILE
     long long rr_t = clock64();
 #endif
     extern __shared__ __align__(16) unsigned char smraw[];
     Small& sm = *reinterpret_cast<Small*>(smraw);
     unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));       // union region
+    // chain / leaf buffers of the staged scorer (absent on the register path)
     double* cbuf = reinterpret_cast<double*>(u + p.ubytes);                  // [NWARP][8*MAXLEAF]
-    double* lbuf = cbuf + NWARP * 8 * MAXLEAF;                               // [NWARP][2*MAXLEAF]
-    float* qs = reinterpret_cast<float*>(lbuf + NWARP * 2 * MAXLEAF);        // [q_stride] (skewed)
+    double* lbuf = cbuf + (p.reg_path ? 0 : NWARP * 8 * MAXLEAF);            // [NWARP][2*MAXLEAF]
+    float* qs = reinterpret_cast<float*>(lbuf + (p.reg_path ? 0 : NWARP * 2 * MAXLEAF));   // [q_stride] (skewed)
     int* cnts = reinterpret_cast<int*>(qs + q_stride(p.d));                  // [nsub]
     unsigned* hist = reinterpret_cast<unsigned*>(cnts + ((p.cb.n_sub + 3) & ~3));   // [HBINS]
     double* qd = reinterpret_cast<double*>(hist + HBINS);                    // [q_stride] float64, skewed
@@ -966,10 +972,19 @@ __global__ void __launch_bounds__(NT) k_union_kth(const float* __restrict__ keys
     if (threadIdx.x == 0) out[q] = o2f(ukeys[k - 1]);
 }
 
-static size_t rerank_smem(int d, int nsub) {
-    return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d) + (size_t)NWARP * 8 * MAXLEAF * 8 +
-           (size_t)NWARP * 2 * MAXLEAF * 8 + (size_t)q_stride(d) * 4 +
+static size_t rerank_smem(int d, int nsub, bool wide) {
+    const size_t chains = reg_path_ok(d) ? 0 : (size_t)NWARP * 8 * MAXLEAF * 8 + (size_t)NWARP * 2 * MAXLEAF * 8;
+    return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d, wide) + chains + (size_t)q_stride(d) * 4 +
            (size_t)((nsub + 3) & ~3) * 4 + (size_t)HBINS * 4 + (size_t)q_stride(d) * 8 + 16;
+}
+
+template <typename T, bool IP, bool WIDE>
+static cudaError_t launch_rerank_v(const RerankParams& p, cudaStream_t s) {
+    const size_t smem = rerank_smem(p.d, p.cb.n_sub, WIDE);
+    cudaError_t e = cudaFuncSetAttribute(k_rerank<T, IP, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_rerank<T, IP, WIDE><<<(unsigned)p.nq, NT, smem, s>>>(p);
+    return cudaGetLastError();
 }
 
 template <typename T>
@@ -977,20 +992,13 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     if (p0.nq == 0) return cudaSuccess;
     RerankParams p = p0;
     if (p.d >= 8 && p.d <= WARP_D_MAX) np_leaves(p.d, p.plan);
-    p.ubytes = (int)union_bytes(p.d);
     p.reg_path = reg_path_ok(p.d) ? 1 : 0;
-    const size_t smem = rerank_smem(p.d, p.cb.n_sub);
-    cudaError_t e;
-    if (p.ip) {
-        e = cudaFuncSetAttribute(k_rerank<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_rerank<T, true><<<(unsigned)p.nq, NT, smem, s>>>(p);
-    } else {
-        e = cudaFuncSetAttribute(k_rerank<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k_rerank<T, false><<<(unsigned)p.nq, NT, smem, s>>>(p);
-    }
-    return cudaGetLastError();
+    // large k (many survivors and live candidates per query): the wide build;
+    // small k (probes, IVF lists, config 1): 3 CTAs/SM hide more latency (measured)
+    const bool wide = p.k > 64;
+    p.ubytes = (int)union_bytes(p.d, wide);
+    if (wide) return p.ip ? launch_rerank_v<T, true, true>(p, s) : launch_rerank_v<T, false, true>(p, s);
+    return p.ip ? launch_rerank_v<T, true, false>(p, s) : launch_rerank_v<T, false, false>(p, s);
 }
 #ifdef VS_RERANK_PROFILE
 extern "C" int vs_debug_rerank_profile(unsigned long long* out, int reset) {
