@@ -157,7 +157,9 @@ int scatter_rows(vs_ctx* ctx, const T* src, const int32_t* idx, int64_t n, int w
     return VS_OK;
 }
 
-int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force);
+struct PhaseBHooks;
+int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force,
+            const PhaseBHooks* hk = nullptr);
 
 // phase A result kept between the two halves of a search
 struct PhaseA {
@@ -254,11 +256,12 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
 
 // phase A + phase B for the rows [0, nsel) of one job, then re-run overflowed
 // queries with 4x larger candidate buffers (cshift + 2) until none remain.
-int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force) {
+int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force,
+            const PhaseBHooks* hk) {
     if (job.nq == 0) return VS_OK;
     PhaseA st;
     CKS(enn_phase_a(ctx, job, margin, cshift, &st));
-    return enn_phase_b(ctx, job, st, cshift, allow_force, PhaseBHooks{});
+    return enn_phase_b(ctx, job, st, cshift, allow_force, hk ? *hk : PhaseBHooks{});
 }
 
 int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bool allow_force,
@@ -638,6 +641,32 @@ static int merge_parts(vs_ctx* ctx, int nparts, int64_t nq, int k_in, const int6
 // into chunks; chunk c+1 is gathered by a few SMs over PCIe (zero-copy 16-byte
 // reads, copy stream) while chunk c is searched on the remaining SMs; the
 // per-chunk top-k are merged with the cross-shard merge kernel (same tie rule).
+// Streamed chunks arrive in ascending row order, so a later chunk's row can
+// only enter the final top-k with an exact distance below the k-th of any
+// earlier chunk's (full) top-k. thr[q] keeps that bound in approximate-key
+// space (key = dist - ||q||^2, or -score for inner product), rounded up; the
+// next chunks' phase B keeps only candidates within the margin of it.
+__global__ void k_chunk_bound(const double* __restrict__ dist, const int32_t* __restrict__ cnt, int64_t nq, int k,
+                              const float* __restrict__ Q, int d, int ip, float* __restrict__ thr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (q >= nq || cnt[q] < k) return;
+    double qq = 0.0;
+    if (!ip) {
+        for (int i = lane; i < d; i += 32) {
+            const double a = (double)Q[q * d + i];
+            qq = fma(a, a, qq);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
+    }
+    if (lane == 0) {
+        const double dk = dist[q * k + k - 1];
+        const float t = __double2float_ru(ip ? -dk : dk - qq * (1.0 - 1e-12));
+        thr[q] = fminf(thr[q], t);
+    }
+}
+
 static int enn_search_streamed(vs_ctx* ctx, vs_column* col, const float* dq, int64_t nq, int d,
                                const int64_t* sel, int64_t nsel, int k, int metric, int64_t id_offset,
                                const float* margin, int64_t* out_ids, double* out_dist, int32_t* out_count) {
@@ -674,6 +703,13 @@ static int enn_search_streamed(vs_ctx* ctx, vs_column* col, const float* dq, int
     CKS(arena_alloc(ctx, (size_t)nchunks * nq * k, &cids));
     CKS(arena_alloc(ctx, (size_t)nchunks * nq * k, &cdist));
     CKS(arena_alloc(ctx, (size_t)nchunks * nq, &ccnt));
+    float* thr = nullptr;
+    if (nchunks > 1) {
+        CKS(arena_alloc(ctx, (size_t)nq, &thr));
+        std::vector<float> inf(nq, std::numeric_limits<float>::infinity());
+        CK(cudaMemcpyAsync(thr, inf.data(), nq * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     cudaEvent_t ready[2], done[2];
     for (int b = 0; b < 2; ++b) {
         CK(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
@@ -727,7 +763,15 @@ static int enn_search_streamed(vs_ctx* ctx, vs_column* col, const float* dq, int
         job.out_dist = cdist + c * nq * k;
         job.out_ids32 = nullptr;
         job.out_count = ccnt + c * nq;
-        if ((rc = run_enn(ctx, job, margin, 0, true)) != VS_OK) break;
+        PhaseBHooks hk;
+        hk.ext_thr = c > 0 ? thr : nullptr;
+        if ((rc = run_enn(ctx, job, margin, 0, true, &hk)) != VS_OK) break;
+        if (thr && c + 1 < nchunks) {
+            k_chunk_bound<<<(unsigned)((nq * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+                job.out_dist, job.out_count, nq, k, dq, d, metric, thr);
+            CK(cudaGetLastError());
+            ctx->stats[VS_STAT_LAUNCHES] += 1;
+        }
         cudaEventRecord(done[b], ctx->stream);
     }
     ctx->sm_reserve = 0;

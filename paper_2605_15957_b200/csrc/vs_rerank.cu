@@ -949,7 +949,10 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 3) k_rerank(RerankParams p) {
                 const uint64_t* sk = reinterpret_cast<const uint64_t*>(u);  // sorted keys left by the top-k
                 double kth = keff > 0 ? o2d(sk[keff - 1]) : 0.0;             // exact key (-score for IP)
                 if (!IP) kth -= qq * (1.0 + 1e-12);  // approx keys omit ||q||^2
-                if (keff < p.k || !(kth < bound - slack)) p.cb.overflow[q] = 1;
+                // an external bound T (earlier chunks' k-th) at or below every
+                // dropped candidate's exact key also settles it: none can enter
+                const bool settled = p.ext_thr && (double)p.ext_thr[q] <= bound - slack;
+                if (!settled && (keff < p.k || !(kth < bound - slack))) p.cb.overflow[q] = 1;
             }
         }
     }
