@@ -110,7 +110,6 @@ struct Params {
     const uint32_t* pbits;          // nullable: filter bit per payload position
     int pf_boxes;                   // MODE 2: L2 prefetch distance (B boxes)
     int64_t chunk_rows;             // MODE 2: rows per list chunk (0: whole lists)
-    int l2_hints;                   // MODE 2: L2 evict-first for B, evict-last for A (always on)
     int a32;                        // MODE 2 A boxes: 0 full 128 rows; 1 32/64-row boxes;
                                     // 2 (default) spread: <= 64 pairs as four 8/16-row boxes, one per TMEM lane quadrant
                                     // (measured: 15.5 -> 14.7 ms on config 4)
@@ -1330,7 +1329,6 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     static const int pf_env = getenv("VS_TC_PF") ? atoi(getenv("VS_TC_PF")) : tc::PF_BOXES;
     pr.pf_boxes = pf_env;
     pr.chunk_rows = a.pair_base ? a.chunk_rows : 0;
-    pr.l2_hints = 1;
     pr.dense_direct = 0;
     pr.a32 = a32_env;
     pr.pair_base = a.pair_base;
