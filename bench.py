@@ -855,10 +855,18 @@ def run_ours(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: VS_BENCH_ONE_GPU=1 puts every rank on cuda:0 and talks gloo,
+    # which exercises the N > 1 code path on a one-GPU box (never for numbers)
+    one_gpu = os.environ.get("VS_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     H = Harness(world, dev)
     wl = (IvfBf16Workload if cfg.get("bf16") else IvfWorkload if "nlist" in cfg else ExactWorkload)(
         args, cfg, rank, world, dev)

@@ -102,7 +102,9 @@ int32_t vs_version(void);
 /* ---- context: one per GPU (one process per GPU) -------------------------- */
 int vs_ctx_create(int32_t device, vs_ctx** out);
 int vs_ctx_destroy(vs_ctx* ctx);
-/* run on a caller stream (cudaStream_t); NULL restores the context stream */
+/* run on a caller stream (cudaStream_t); NULL restores the context's own
+ * (non-blocking) stream, so the legacy default stream must be passed as
+ * cudaStreamLegacy ((void*)0x1) to order the library after work queued there */
 int vs_ctx_set_stream(vs_ctx* ctx, void* stream);
 int vs_ctx_synchronize(vs_ctx* ctx);
 int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value);

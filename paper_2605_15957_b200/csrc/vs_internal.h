@@ -30,10 +30,12 @@ inline int cuda_err(cudaError_t e, const char* what) {
     return set_err(VS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+#define VS_STR2(x) #x
+#define VS_STR(x) VS_STR2(x)
 #define CK(call)                                                   \
     do {                                                           \
         cudaError_t _e = (call);                                   \
-        if (_e != cudaSuccess) { cudaGetLastError(); return cuda_err(_e, #call); } \
+        if (_e != cudaSuccess) { cudaGetLastError(); return cuda_err(_e, #call " @" VS_STR(__LINE__) " " __FILE__); } \
     } while (0)
 #define CKS(call)                                     \
     do {                                              \

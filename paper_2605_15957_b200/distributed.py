@@ -62,10 +62,11 @@ def all_gather_topk(ids, dist, counts, group=None):
         if dist_.get_backend(group) == "nccl":
             o = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
             dist_.all_gather_into_tensor(o, t, group=group)
-        else:  # gloo (CPU tests): list form
-            parts = [torch.empty_like(t) for _ in range(world)]
-            dist_.all_gather(parts, t, group=group)
-            o = torch.stack(parts)
+        else:  # gloo (CPU tests): list form over host copies
+            h = t.cpu()
+            parts = [torch.empty_like(h) for _ in range(world)]
+            dist_.all_gather(parts, h, group=group)
+            o = torch.stack(parts).to(t.device)
         outs.append(o)
     return tuple(outs)
 
@@ -136,6 +137,12 @@ class TorchComm:
 
     def allreduce_min(self, t):
         import torch.distributed as dist_
+        if dist_.get_backend(self.group) != "nccl" and t.is_cuda:
+            # gloo: reduce a host copy (device tensors only via NCCL)
+            h = t.cpu()
+            dist_.all_reduce(h, op=dist_.ReduceOp.MIN, group=self.group)
+            t.copy_(h)
+            return t
         dist_.all_reduce(t, op=dist_.ReduceOp.MIN, group=self.group)
         return t
 
@@ -148,9 +155,10 @@ class TorchComm:
             o = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
             dist_.all_gather_into_tensor(o, t, group=self.group)
             return o
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist_.all_gather(parts, t, group=self.group)
-        return torch.stack(parts)
+        h = t.cpu()
+        parts = [torch.empty_like(h) for _ in range(world)]
+        dist_.all_gather(parts, h, group=self.group)
+        return torch.stack(parts).to(t.device)
 
     def allgather_topk(self, ids, dist, counts):
         return all_gather_topk(ids, dist, counts, self.group)
@@ -183,8 +191,11 @@ def two_phase_search(shard, comm, queries, k: int, metric: str = "squared_l2", r
     gi, gd, gc = comm.allgather_topk(ids, dist, cnt)
     mi, md, mc = merge(gi, gd, gc, k, metric)
     comm.allreduce_min(bound)
-    bad = torch.nonzero(~_merged_is_exact(md, mc, bound, k, metric)).flatten()
-    # every rank holds the same merged result and bounds: the same re-run set
+    # the re-run set is agreed collectively (MIN of the per-rank verdicts), so
+    # every rank takes part in the same collectives even if a verdict differed
+    ok = _merged_is_exact(md, mc, bound, k, metric).to(torch.int32)
+    comm.allreduce_min(ok)
+    bad = torch.nonzero(ok == 0).flatten()
     if bad.numel():
         sub_q = queries[bad] if hasattr(queries, "index_select") else queries[bad.cpu().numpy()]
         ri, rd, rc = shard.plain(sub_q, k, metric, row_filter, id_offset)

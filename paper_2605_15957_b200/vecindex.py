@@ -237,7 +237,11 @@ class _Stream:
     def __enter__(self):
         if self.on:
             import torch
-            self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream)
+            # torch's default stream has handle 0, which the ABI reads as "the
+            # library's own stream": pass cudaStreamLegacy (0x1) instead, so the
+            # library is ordered after torch's pending work (e.g. non_blocking
+            # host->device copies of the inputs)
+            self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream or 1)
         return self
 
     def __exit__(self, *exc):

@@ -181,3 +181,43 @@ def test_ivf_list_sharded_query_sliced_probing(world):
         ids, dist, _ = _flat(results[r])
         assert np.array_equal(ids, ref.data_row)
         assert np.array_equal(dist, ref.distance)
+
+
+def test_inputs_from_async_copies_on_the_default_stream():
+    """Device inputs produced by non_blocking host->device copies on torch's
+    default stream (handle 0) right before the call: the library must be
+    ordered after them (it runs on cudaStreamLegacy then, not its own stream)."""
+    rng = np.random.default_rng(11)
+    n, d, nq, k = 200000, 256, 3000, 10
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((nq, d)).astype(np.float32)
+    mask = rng.random(n) < 0.2
+    col = vs.EmbeddingColumn.from_device(torch.from_numpy(data).cuda())
+    qh = torch.from_numpy(q).pin_memory()
+    bh = torch.from_numpy(vs.vecindex.pack_bitmap(mask).view(np.int32)).pin_memory()
+    shard = ShardSearch(col)
+
+    class One:
+        def size(self):
+            return 1
+
+        def rank(self):
+            return 0
+
+        def allreduce_min(self, t):
+            return t
+
+        def allgather(self, t):
+            return t.unsqueeze(0)
+
+        def allgather_topk(self, i, dd, c):
+            return i.unsqueeze(0), dd.unsqueeze(0), c.unsqueeze(0)
+
+    ref = O.enn_filtered(q[::97], data, mask, k)
+    for _ in range(3):
+        qq = qh.to("cuda", non_blocking=True)
+        bb = bh.to("cuda", non_blocking=True)
+        ids, dist, cnt = two_phase_search(shard, One(), qq, k, "squared_l2", row_filter=bb)
+        ids, dist = ids.cpu().numpy()[::97].reshape(-1), dist.cpu().numpy()[::97].reshape(-1)
+        assert np.array_equal(ids, ref.data_row)
+        assert np.array_equal(dist, ref.distance)
