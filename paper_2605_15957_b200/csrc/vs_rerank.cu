@@ -27,7 +27,7 @@ constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
 constexpr int KMAX = 2048;      // == vs_topk_cap(): sort capacity
 // live candidates staged in shared memory per query: the wide build (large k)
-// stages 8192 at 2 CTAs/SM, the narrow one 4096 at 3 CTAs/SM
+// stages 8192 at 2 CTAs/SM, the narrow one 4096 at 4 CTAs/SM (64 registers)
 template <bool WIDE> constexpr int lcap() { return WIDE ? 8192 : 4096; }
 constexpr int MAXLEAF = 32;     // numpy pairwise leaves (>= 64 elements each) -> d <= 2048 on the warp path
 constexpr int WARP_D_MAX = 2048;
@@ -559,7 +559,7 @@ __device__ unsigned long long g_rr_prof[8];
 #endif
 
 template <typename T, bool IP, bool WIDE>
-__global__ void __launch_bounds__(NT, WIDE ? 2 : 3) k_rerank(RerankParams p) {
+__global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
     constexpr int LCAP = lcap<WIDE>();
 #ifdef VS_RERANK_PROFILE
     long long rr_t = clock64();
@@ -997,7 +997,7 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     if (p.d >= 8 && p.d <= WARP_D_MAX) np_leaves(p.d, p.plan);
     p.reg_path = reg_path_ok(p.d) ? 1 : 0;
     // large k (many survivors and live candidates per query): the wide build;
-    // small k (probes, IVF lists, config 1): 3 CTAs/SM hide more latency (measured)
+    // small k (probes, IVF lists, config 1): 4 CTAs/SM hide more latency (measured)
     const bool wide = p.k > 64;
     p.ubytes = (int)union_bytes(p.d, wide);
     if (wide) return p.ip ? launch_rerank_v<T, true, true>(p, s) : launch_rerank_v<T, false, true>(p, s);
