@@ -168,15 +168,8 @@ def measured_peaks() -> dict:
 # ---- workloads ---------------------------------------------------------------------------------
 
 def pack_bits_torch(mask):
-    import torch
-    n = mask.numel()
-    pad = (-n) % 32
-    if pad:
-        mask = torch.cat([mask, torch.zeros(pad, dtype=torch.bool, device=mask.device)])
-    w = mask.view(-1, 32).to(torch.int64)
-    shifts = torch.arange(32, device=mask.device, dtype=torch.int64)
-    words = (w << shifts).sum(dim=1)
-    return (words - ((words >> 31) << 32)).to(torch.int32).contiguous()  # two's complement uint32
+    from paper_2605_15957_b200.synth import pack_bits_torch as _p
+    return _p(mask)
 
 
 def build_cfg2(rank, world, cfg):
@@ -205,49 +198,17 @@ def build_cfg2(rank, world, cfg):
 
 
 def _device_slice(n, d, lo, hi, dev):
-    import torch
-
-    from paper_2605_15957_b200 import synth
-    chunk = 1 << 20
-    # regenerate global chunks covering [lo, hi) with per-chunk seeds
-    g = torch.Generator(device=dev)
-    g.manual_seed(42)
-    c = torch.randn(64, d, generator=g, device=dev)
-    c /= c.norm(dim=1, keepdim=True)
-    out = torch.empty(hi - lo, d, device=dev)
-    for ci in range(lo // chunk, (hi + chunk - 1) // chunk):
-        a, b = ci * chunk, min(n, (ci + 1) * chunk)
-        gg = torch.Generator(device=dev)
-        gg.manual_seed(100_000 + ci)
-        asg = torch.randint(0, 64, (b - a,), generator=gg, device=dev)
-        v = c[asg] + 0.55 * torch.randn(b - a, d, generator=gg, device=dev)
-        v /= v.norm(dim=1, keepdim=True)
-        s, e = max(a, lo), min(b, hi)
-        out[s - lo:e - lo] = v[s - a:e - a]
-    del synth
-    return out, c
+    from paper_2605_15957_b200.synth import device_rows
+    return device_rows(n, d, lo, hi, dev)
 
 
 def _device_slice_bf16(n, d, lo, hi, dev):
-    """Rows [lo, hi) of the mixture law drawn chunk by chunk straight into
-    bfloat16 (the float32 collection would not fit next to the index)."""
+    """Rows [lo, hi) drawn chunk by chunk straight into bfloat16 (the float32
+    collection would not fit next to the index)."""
     import torch
-    chunk = 1 << 20
-    g = torch.Generator(device=dev)
-    g.manual_seed(42)
-    c = torch.randn(64, d, generator=g, device=dev)
-    c /= c.norm(dim=1, keepdim=True)
-    out = torch.empty(hi - lo, d, device=dev, dtype=torch.bfloat16)
-    for ci in range(lo // chunk, (hi + chunk - 1) // chunk):
-        a, b = ci * chunk, min(n, (ci + 1) * chunk)
-        gg = torch.Generator(device=dev)
-        gg.manual_seed(100_000 + ci)
-        asg = torch.randint(0, 64, (b - a,), generator=gg, device=dev)
-        v = c[asg] + 0.55 * torch.randn(b - a, d, generator=gg, device=dev)
-        v /= v.norm(dim=1, keepdim=True)
-        s_, e_ = max(a, lo), min(b, hi)
-        out[s_ - lo:e_ - lo] = v[s_ - a:e_ - a].to(torch.bfloat16)
-    return out, c
+
+    from paper_2605_15957_b200.synth import device_rows
+    return device_rows(n, d, lo, hi, dev, dtype=torch.bfloat16)
 
 
 # ---- CPU legs (oracle port; test infrastructure only) --------------------------------------------

@@ -144,10 +144,14 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data,
 
 /* ---- two-phase exact search of one row shard (multi-GPU) -----
  * begin: selection + phase A (tensor cores) on this shard, and out_keys
- * [nq][k] = the shard's k smallest approximate keys (ascending, +inf padded).
- * The caller all-gathers the keys of every shard and takes T = the k-th
- * smallest of their union (vs_union_kth): the global k-th approximate key.
- * finish(T): phase B re-ranks only candidates with key <= T + margin, so the
+ * [nq][k] = upper bounds on the exact keys of the shard's k smallest
+ * approximate keys (approx + this shard's margin/2, rounded up; ascending,
+ * +inf padded). The caller all-gathers the keys of every shard and takes
+ * T = the k-th smallest of their union (vs_union_kth): an upper bound on the
+ * global k-th exact key, valid even when shards have different margins
+ * (different max norms or phase-A kernels).
+ * finish(T): phase B re-ranks only candidates with key <= T + margin/2 (its
+ * own margin), so the
  * exact float64 work is split across the shards instead of repeated on each;
  * returns the shard's rows (possibly fewer than k) and out_bound[q]: every
  * candidate this shard dropped in phase A has exact key (distance; -score

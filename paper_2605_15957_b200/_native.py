@@ -170,6 +170,19 @@ class Context:
         self.handle = h
         self.device = int(device)
 
+    def close(self) -> None:
+        """Destroy the library context (its scratch arena and stream). Columns
+        and indexes created through it keep it alive (they hold a reference)."""
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            load().vs_ctx_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     @classmethod
     def get(cls, device: int | None = None) -> "Context":
         if device is None:

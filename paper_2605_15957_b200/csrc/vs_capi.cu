@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <mutex>
 #include <limits>
 #include <cmath>
 #include <cstdarg>
@@ -421,6 +422,8 @@ int build_selection(vs_ctx* ctx, const uint32_t* d_bm, int64_t nbits, int64_t** 
 
 }  // namespace
 
+void pending_erase(const vs_ctx* ctx);
+
 // =====================================================================================
 extern "C" {
 
@@ -451,6 +454,7 @@ int vs_ctx_create(int32_t device, vs_ctx** out) {
 
 int vs_ctx_destroy(vs_ctx* ctx) {
     if (!ctx) return VS_OK;
+    pending_erase(ctx);   // a later context at the same address must not inherit it
     DevGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     ctx->arena.release();
@@ -878,9 +882,11 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
 }
 
 // ---- two-phase exact search for row-sharded collections --------------------------
-// begin: phase A on this shard + the shard-local k-th approximate key per
-// query; the caller all-reduces (MIN) those keys into a global bound T; finish:
-// phase B re-ranks only the candidates with key <= min(K*, T) + margin, so the
+// begin: phase A on this shard + upper bounds on the exact keys of the
+// shard's k smallest approximate keys (approx + margin/2); the caller takes the
+// k-th of their union over shards, T >= the global k-th exact key; finish:
+// phase B re-ranks only the candidates with key <= min(K* + margin, T +
+// margin/2) (this shard's own margin), so the
 // exact work per shard shrinks with the number of shards. out_bound returns,
 // per query, a value below which no dropped candidate of this shard lies
 // (key space: distance, or -score); the merged k-th key must stay below the
@@ -892,11 +898,31 @@ struct PendingEnn {
     PhaseA st;
     bool active = false;
 };
+// begin/finish state per context. Contexts are driven from different threads
+// (one per shard) and ctypes releases the GIL, so the map is guarded; entries
+// are node-stable, so a reference stays valid while its context is in use.
+std::mutex& pending_mu() {
+    static std::mutex m;
+    return m;
+}
 std::unordered_map<const vs_ctx*, PendingEnn>& pending_map() {
     static std::unordered_map<const vs_ctx*, PendingEnn> m;
     return m;
 }
+PendingEnn& pending_of(const vs_ctx* ctx) {
+    std::lock_guard<std::mutex> lk(pending_mu());
+    return pending_map()[ctx];
+}
+PendingEnn* pending_find(const vs_ctx* ctx) {
+    std::lock_guard<std::mutex> lk(pending_mu());
+    auto it = pending_map().find(ctx);
+    return it == pending_map().end() ? nullptr : &it->second;
+}
 }  // namespace
+void pending_erase(const vs_ctx* ctx) {
+    std::lock_guard<std::mutex> lk(pending_mu());
+    pending_map().erase(ctx);
+}
 extern "C" {
 
 int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries, int64_t nq, int32_t d,
@@ -914,7 +940,7 @@ int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries
     DevGuard g(ctx->device);
     vs_column* col = const_cast<vs_column*>(data);
     CK(ctx->arena.reset());
-    PendingEnn& pe = pending_map()[ctx];
+    PendingEnn& pe = pending_of(ctx);
     pe.active = false;
     std::vector<OutBuf> pending;
     const float* dq = nullptr;
@@ -991,11 +1017,11 @@ int vs_union_kth(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k, const float
 int vs_enn_search_finish(vs_ctx* ctx, const float* thresholds, int64_t id_offset, int64_t* out_ids,
                          double* out_dist, int32_t* out_count, double* out_bound) {
     if (!ctx) return set_err(VS_ERR_PARAMETER, "null ctx");
-    auto it = pending_map().find(ctx);
-    if (it == pending_map().end() || !it->second.active)
+    PendingEnn* pf = pending_find(ctx);
+    if (!pf || !pf->active)
         return set_err(VS_ERR_PARAMETER, "vs_enn_search_finish without vs_enn_search_begin");
     DevGuard g(ctx->device);
-    PendingEnn& pe = it->second;
+    PendingEnn& pe = *pf;
     pe.active = false;
     EnnJob job = pe.job;
     const int64_t nq = job.nq;

@@ -173,7 +173,8 @@ __device__ void bitonic_sort_u32(uint32_t* key, int P) {
 // distributed protocol, phase 1: this shard's k smallest approximate keys,
 // ascending, +inf padded (keys <= kth are gathered into `a` (HBINS slots))
 template <class ForEach>
-__device__ void write_local_topk_keys(ForEach foreach, uint32_t kth, int k, unsigned* a, Small& sm, float* out) {
+__device__ void write_local_topk_keys(ForEach foreach, uint32_t kth, int k, unsigned* a, Small& sm, float half_margin,
+                                      float* out) {
     const int tid = threadIdx.x;
     if (tid == 0) sm.counter = 0;
     __syncthreads();
@@ -190,7 +191,9 @@ __device__ void write_local_topk_keys(ForEach foreach, uint32_t kth, int k, unsi
     for (int i = c + tid; i < P; i += NT) a[i] = 0xffffffffu;
     __syncthreads();
     bitonic_sort_u32(a, P);
-    for (int i = tid; i < k; i += NT) out[i] = i < c ? o2f(a[i]) : __int_as_float(0x7f800000);
+    // upper bounds on the exact keys (approx + this shard's margin / 2, rounded
+    // up): the k-th of their union over shards bounds the global k-th exact key
+    for (int i = tid; i < k; i += NT) out[i] = i < c ? __fadd_ru(o2f(a[i]), half_margin) : __int_as_float(0x7f800000);
 }
 
 // bitonic sort of P (power of two) (key, id) pairs in shared memory
@@ -614,10 +617,14 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
     // verify mode: tau_g is the smallest local k-th key, an upper bound on the
     // global one; survivors need key <= K* + margin <= tau_g + margin
     uint32_t pre = (p.verify && tg != 0xffffffffu) ? f2o(__fadd_ru(o2f(tg), p.margin[q])) : tg;
-    // distributed protocol: the global bound T on the k-th key (the smallest
-    // shard-local k-th); survivors need key <= min(K*, T) + margin
-    const uint32_t ext_o = p.ext_thr ? f2o(p.ext_thr[q]) : 0xffffffffu;
-    if (p.ext_thr && ext_o != f2o(__int_as_float(0x7f800000))) pre = min(pre, f2o(__fadd_ru(p.ext_thr[q], p.margin[q])));
+    // external bound T: an upper bound on the k-th EXACT key of the final
+    // result (distributed protocol: the k-th smallest of every shard's
+    // approx-key + its own margin/2; streamed chunks: an earlier chunk's exact
+    // k-th). A row of the result has exact key <= T, so approx key <= T +
+    // margin/2 with THIS shard's margin (shards may differ in margin).
+    const bool has_ext = p.ext_thr && f2o(p.ext_thr[q]) != f2o(__int_as_float(0x7f800000));
+    const uint32_t ext_o = has_ext ? f2o(__fadd_ru(p.ext_thr[q], 0.5f * p.margin[q])) : 0xffffffffu;
+    pre = min(pre, ext_o);
 
     RR_MARK(0);
     float* lkey = reinterpret_cast<float*>(u);
@@ -724,11 +731,11 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
                 [&](auto fn) {
                     for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
                 },
-                kth, p.k, hist, sm, p.out_kth + q * (int64_t)p.k);
+                kth, p.k, hist, sm, 0.5f * p.margin[q], p.out_kth + q * (int64_t)p.k);
             return;
         }
-        if (p.ext_thr) kth = min(kth, ext_o);
-        if (kth != 0xffffffffu && (nl > p.k || p.ext_thr)) thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
+        if (kth != 0xffffffffu && nl > p.k) thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
+        thr_o = min(thr_o, ext_o);
         if (tid == 0) sm.counter = 0;
         __syncthreads();
         for (int i = tid; i < nl; i += NT) {
@@ -762,12 +769,12 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
                                 if (o <= pre) fn(o);
                             }
                     },
-                    kth, p.k, hist, sm, p.out_kth + q * (int64_t)p.k);
+                    kth, p.k, hist, sm, 0.5f * p.margin[q], p.out_kth + q * (int64_t)p.k);
                 return;
             }
-            if (p.ext_thr) kth = min(kth, ext_o);
             thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
         }
+        thr_o = min(thr_o, ext_o);
         if (tid == 0) sm.counter = 0;
         __syncthreads();
         for (int s = w; s < nsub; s += NWARP)

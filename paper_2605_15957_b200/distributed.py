@@ -111,14 +111,17 @@ def sharded_search(local_search, k: int, metric: str, merge=None, group=None):
 #
 # Plain row sharding re-ranks every shard's full local top-k (k + margin band
 # survivors per query per shard), so the exact float64 work per GPU does not
-# shrink with the shard count. The two-phase protocol first exchanges each
-# shard's k smallest APPROXIMATE keys per query (k floats); the k-th smallest
-# of their union is exactly the global k-th approximate key K* (every key of
-# the global top-k is in its own shard's top-k), so each shard re-ranks only
-# its candidates with key <= K* + margin: the single-GPU survivor set, split
-# across the shards. Rows a shard dropped in phase A (local top-k mode) have
-# exact key > that shard's bound, which is checked against the merged k-th
-# key; a failing query is re-run with the one-phase search on every shard.
+# shrink with the shard count. The two-phase protocol first exchanges, per
+# query, k floats per shard: upper bounds on the exact keys of the shard's k
+# smallest APPROXIMATE keys (approx + that shard's margin/2, rounded up). The
+# k-th smallest of their union, U*, bounds the global k-th exact key from
+# above (k rows have exact key <= U*), so a row of the global top-k has approx
+# key <= U* + m_s/2 on its shard s whatever the other shards' margins (their
+# max norms or phase-A kernels may differ). Each shard re-ranks only those
+# candidates: the single-GPU survivor set, split across the shards. Rows a
+# shard dropped in phase A (local top-k mode) have exact key > that shard's
+# bound, which is checked against the merged k-th key; a failing query is
+# re-run with the one-phase search on every shard.
 
 
 class TorchComm:
@@ -185,8 +188,8 @@ def two_phase_search(shard, comm, queries, k: int, metric: str = "squared_l2", r
     the global result on every rank (torch tensors on the shard's device)."""
     import torch
     merge = merge or gpu_merge
-    keys = shard.begin(queries, k, metric, row_filter)        # [Q, k] shard-local approx keys
-    T = shard.union_kth(comm.allgather(keys))               # [Q] global k-th approx key
+    keys = shard.begin(queries, k, metric, row_filter)        # [Q, k] upper bounds on exact keys
+    T = shard.union_kth(comm.allgather(keys))               # [Q] >= global k-th exact key
     ids, dist, cnt, bound = shard.finish(T, id_offset)
     gi, gd, gc = comm.allgather_topk(ids, dist, cnt)
     mi, md, mc = merge(gi, gd, gc, k, metric)

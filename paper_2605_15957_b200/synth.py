@@ -210,3 +210,53 @@ def device_queries(centers_t, n: int, seed: int = 7, noise: float = 0.55):
                                                  device=centers_t.device)
     v /= v.norm(dim=1, keepdim=True)
     return v.float().contiguous()
+
+
+def device_rows(n: int, d: int, lo: int, hi: int, device, dtype=None, chunk: int = 1 << 20):
+    """Rows [lo, hi) of the N-row bench collection (mixture law, 64 unit
+    centres, noise 0.55, L2-normalised), drawn on the GPU in global 2^20-row
+    chunks with per-chunk seeds: every row shard / world size sees the same
+    global collection. dtype bfloat16 rounds each normalised chunk (config 4).
+    Returns (rows, centres)."""
+    import torch
+
+    dtype = dtype or torch.float32
+    g = torch.Generator(device=device)
+    g.manual_seed(42)
+    c = torch.randn(64, d, generator=g, device=device)
+    c /= c.norm(dim=1, keepdim=True)
+    out = torch.empty(hi - lo, d, device=device, dtype=dtype)
+    for ci in range(lo // chunk, (hi + chunk - 1) // chunk):
+        a, b = ci * chunk, min(n, (ci + 1) * chunk)
+        gg = torch.Generator(device=device)
+        gg.manual_seed(100_000 + ci)
+        asg = torch.randint(0, 64, (b - a,), generator=gg, device=device)
+        v = c[asg] + 0.55 * torch.randn(b - a, d, generator=gg, device=device)
+        v /= v.norm(dim=1, keepdim=True)
+        s_, e_ = max(a, lo), min(b, hi)
+        out[s_ - lo:e_ - lo] = v[s_ - a:e_ - a].to(dtype)
+    return out, c
+
+
+def device_bernoulli(n: int, p: float, seed: int, device):
+    """The bench filters: Bernoulli(p) row mask drawn on the GPU."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return torch.rand(n, generator=g, device=device) < p
+
+
+def pack_bits_torch(mask):
+    """bool [n] -> packed uint32 words (LSB-first) as an int32 tensor."""
+    import torch
+
+    n = mask.numel()
+    pad = (-n) % 32
+    if pad:
+        mask = torch.cat([mask, torch.zeros(pad, dtype=torch.bool, device=mask.device)])
+    w = mask.view(-1, 32).to(torch.int64)
+    shifts = torch.arange(32, device=mask.device, dtype=torch.int64)
+    words = (w << shifts).sum(dim=1)
+    return (words - ((words >> 31) << 32)).to(torch.int32).contiguous()  # two's complement uint32
+

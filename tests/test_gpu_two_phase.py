@@ -62,7 +62,7 @@ class ThreadComm:
         return _R()
 
 
-def _run(world, data, q, mask, k, metric, shard_cls=ShardSearch):
+def _run(world, data, q, mask, k, metric, shard_cls=ShardSearch, kernels=None):
     n = data.shape[0]
     xd = torch.from_numpy(data).cuda()
     qd = torch.from_numpy(q).cuda()
@@ -73,6 +73,8 @@ def _run(world, data, q, mask, k, metric, shard_cls=ShardSearch):
         try:
             lo, hi = row_shard(n, r, world)
             ctx = N.Context(0)
+            if kernels is not None:
+                ctx.set_option(N.OPT_ENN_KERNEL, kernels[r])
             shard = shard_cls(vs.EmbeddingColumn.from_device(xd[lo:hi].contiguous()), ctx)
             shards[r] = shard
             results[r] = two_phase_search(shard, comm.rank(r), qd, k, metric,
@@ -113,6 +115,31 @@ def test_two_phase_equals_unsharded(world, metric):
         ids, dist, _ = _flat(results[r])
         assert np.array_equal(ids, whole.data_row)
         assert np.array_equal(dist, whole.distance)
+
+
+@pytest.mark.parametrize("kernels", [(2, 2), (2, 1, 2), (1, 2, 1, 2)])
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+def test_two_phase_forced_and_mixed_phase_a_kernels(kernels, metric):
+    """Every shard on the tensor-core phase A (local top-k + verification
+    bounds at world > 1), and shards mixing tensor-core (bf16, wide margin) and
+    SIMT (fp32, narrow margin) phase A at small d, with shards of very
+    different max norms: the exchanged bounds must hold across margins."""
+    world = len(kernels)
+    rng = np.random.default_rng(70 + world + 10 * (metric == "inner_product"))
+    n, d, k = 24000, 64, 40
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    for r in range(world):                     # shard r's rows scaled by 1 + 2r
+        lo, hi = row_shard(n, r, world)
+        data[lo:hi] *= np.float32(1 + 2 * r)
+    q = rng.standard_normal((150, d)).astype(np.float32)
+    mask = rng.random(n) < 0.5
+    results, shards = _run(world, data, q, mask, k, metric, kernels=list(kernels))
+    for r in range(world):
+        assert shards[r].ctx.stats()[N.STAT_LAST_ENN_KERNEL] == kernels[r]
+    ref = O.enn_filtered(q, data, mask, k, metric)
+    ids, dist, _ = _flat(results[0])
+    assert np.array_equal(ids, ref.data_row)
+    assert np.array_equal(dist, ref.distance)
 
 
 def test_two_phase_rerun_path_and_empty_shard():
