@@ -23,6 +23,7 @@
 
 #include "vs_internal.h"
 #include "vs_tc.cuh"
+#include "vs_wide.cuh"
 
 using namespace vs_internal;
 
@@ -257,9 +258,46 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
 
 // phase A + phase B for the rows [0, nsel) of one job, then re-run overflowed
 // queries with 4x larger candidate buffers (cshift + 2) until none remain.
+// k' above the candidate-buffer top-k: device-wide select / score / sort (vs_wide.cu)
+int run_enn_wide(vs_ctx* ctx, const EnnJob& job, const float* margin) {
+    if (job.q_ready) CK(cudaStreamWaitEvent(ctx->stream, job.q_ready, 0));
+    if (job.margin_todo) {
+        CK(vs::launch_query_margins(job.q, job.nq, job.d, job.xmax, eps_simt(job.d), job.ip, job.margin_todo,
+                                    nullptr, ctx->stream));
+        margin = job.margin_todo;
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
+    vs::WideJob w{};
+    w.q = job.q;
+    w.nq = job.nq;
+    w.d = job.d;
+    w.rows = job.rows;
+    w.dtype = job.dtype;
+    w.sel = job.sel;
+    w.ncand = job.nsel;
+    w.xnorm = job.xnorm;
+    w.margin = margin;
+    w.ip = job.ip;
+    w.k = job.k;
+    w.id_map = nullptr;
+    w.id_offset = job.id_offset;
+    w.out_ids = job.out_ids;
+    w.out_dist = job.out_dist;
+    w.out_ids32 = job.out_ids32;
+    w.out_count = job.out_count;
+    w.cls_scan = job.cls_scan;
+    w.cls_rerank = job.cls_rerank;
+    ctx->stats[VS_STAT_LAST_ENN_KERNEL] = 3;
+    return vs::wide_enn(ctx, w);
+}
+
 int run_enn(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift, bool allow_force,
             const PhaseBHooks* hk) {
     if (job.nq == 0) return VS_OK;
+    if (job.k > kTopkCap) {
+        if (hk) return set_err(VS_ERR_CAP_EXCEEDED, "two-phase search supports k' <= %d", kTopkCap);
+        return run_enn_wide(ctx, job, margin);
+    }
     PhaseA st;
     CKS(enn_phase_a(ctx, job, margin, cshift, &st));
     return enn_phase_b(ctx, job, st, cshift, allow_force, hk ? *hk : PhaseBHooks{});
@@ -385,9 +423,10 @@ int validate_metric(int32_t metric) {
         return set_err(VS_ERR_PARAMETER, "unknown metric %d", metric);
     return VS_OK;
 }
+// any k' >= 1: k' <= kTopkCap runs the candidate-buffer path, larger k' the
+// wide path (vs_wide.cu)
 int validate_k(int32_t k) {
     if (k < 1) return set_err(VS_ERR_PARAMETER, "k must be >= 1, got %d", k);
-    if (k > kTopkCap) return set_err(VS_ERR_CAP_EXCEEDED, "k'=%d exceeds device top-k cap %d", k, kTopkCap);
     return VS_OK;
 }
 
@@ -424,6 +463,20 @@ int build_selection(vs_ctx* ctx, const uint32_t* d_bm, int64_t nbits, int64_t** 
 
 void pending_erase(const vs_ctx* ctx);
 
+void ctx_ref(vs_ctx* ctx) {
+    std::lock_guard<std::mutex> lk(ctx->life_mu);
+    ++ctx->live_objects;
+}
+void ctx_unref(vs_ctx* ctx) {
+    {
+        std::lock_guard<std::mutex> lk(ctx->life_mu);
+        if (--ctx->live_objects > 0 || !ctx->destroyed) return;
+    }
+    DevGuard g(ctx->device);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
 // =====================================================================================
 extern "C" {
 
@@ -455,11 +508,24 @@ int vs_ctx_create(int32_t device, vs_ctx** out) {
 int vs_ctx_destroy(vs_ctx* ctx) {
     if (!ctx) return VS_OK;
     pending_erase(ctx);   // a later context at the same address must not inherit it
+    {
+        DevGuard g(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        ctx->arena.release();
+        resolve_timers(ctx);
+        for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+        ctx->event_pool.clear();
+        if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+        if (ctx->q_event) cudaEventDestroy(ctx->q_event);
+        ctx->copy_stream = nullptr;
+        ctx->q_event = nullptr;
+    }
+    {
+        std::lock_guard<std::mutex> lk(ctx->life_mu);
+        ctx->destroyed = true;
+        if (ctx->live_objects > 0) return VS_OK;   // the last column / index free deletes it
+    }
     DevGuard g(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    ctx->arena.release();
-    resolve_timers(ctx);
-    for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return VS_OK;
@@ -541,6 +607,7 @@ int vs_column_create(vs_ctx* ctx, const void* src, int64_t n, int32_t d, int32_t
             return cuda_err(e, "column upload");
         }
     }
+    ctx_ref(ctx);
     *out = c;
     return VS_OK;
 }
@@ -558,6 +625,7 @@ int vs_column_wrap(vs_ctx* ctx, void* dev_ptr, int64_t n, int32_t d, int32_t dty
     c->d = d;
     c->dtype = dtype;
     c->owned = false;
+    ctx_ref(ctx);
     *out = c;
     return VS_OK;
 }
@@ -589,6 +657,7 @@ int vs_column_wrap_host(vs_ctx* ctx, void* host_ptr, int64_t n, int32_t d, int32
     c->host_resident = true;
     c->host_registered = registered;
     c->host_ptr = host_ptr;
+    ctx_ref(ctx);
     *out = c;
     return VS_OK;
 }
@@ -601,7 +670,9 @@ int vs_column_free(vs_column* col) {
     if (col->host_registered) cudaHostUnregister(col->host_ptr);
     if (col->norms) cudaFree(col->norms);
     if (col->max_norm_bits) cudaFree(col->max_norm_bits);
+    vs_ctx* ctx = col->ctx;
     delete col;
+    ctx_unref(ctx);
     return VS_OK;
 }
 
@@ -617,6 +688,8 @@ int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype)
 static int merge_parts(vs_ctx* ctx, int nparts, int64_t nq, int k_in, const int64_t* ids, const double* dist,
                        const int32_t* counts, int k, int metric, int64_t* out_ids, double* out_dist,
                        int32_t* out_count) {
+    if (k > kTopkCap)   // the merge kernel sorts the top k in shared memory
+        return vs::wide_merge(ctx, nparts, nq, k_in, ids, dist, counts, k, metric, out_ids, out_dist, out_count);
     vs::MergeParams p;
     p.nparts = nparts;
     p.nq = nq;
@@ -871,7 +944,7 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
     CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
     job.out_ids32 = nullptr;
-    if (col->host_resident) {
+    if (col->host_resident && k <= kTopkCap) {
         CKS(enn_search_streamed(ctx, col, dq, nq, d, sel, nsel, k, metric, id_offset, margin, job.out_ids,
                                 job.out_dist, job.out_count));
     } else {
@@ -934,6 +1007,8 @@ int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries
     if (d != data->d) return set_err(VS_ERR_SHAPE, "query dim %d != data dim %d", d, data->d);
     if (nq < 0) return set_err(VS_ERR_PARAMETER, "negative query count");
     if (data->host_resident) return set_err(VS_ERR_PARAMETER, "two-phase search needs a device-resident shard");
+    if (k > kTopkCap)
+        return set_err(VS_ERR_CAP_EXCEEDED, "two-phase search supports k' <= %d (use the one-phase search)", kTopkCap);
     if (bitmap && nbits != data->n)
         return set_err(VS_ERR_SHAPE, "bitmap covers %lld rows, column has %lld", (long long)nbits,
                        (long long)data->n);
@@ -1272,11 +1347,17 @@ int vs_topk_merge(vs_ctx* ctx, int32_t nparts, int64_t nq, int32_t k_in, const i
     CKS(stage_in(ctx, ids, n_in, &p.ids));
     CKS(stage_in(ctx, dist, n_in, &p.dist));
     CKS(stage_in(ctx, counts, (size_t)nparts * nq, &p.counts));
-    CKS(arena_alloc(ctx, n_in, &p.s_key));
-    CKS(arena_alloc(ctx, n_in, &p.s_id));
     CKS(stage_out(ctx, out_ids, (size_t)nq * k, &p.out_ids, pending));
     CKS(stage_out(ctx, out_dist, (size_t)nq * k, &p.out_dist, pending));
     CKS(stage_out(ctx, out_count, (size_t)nq, &p.out_count, pending));
+    if (k > kTopkCap) {
+        CKS(vs::wide_merge(ctx, nparts, nq, k_in, p.ids, p.dist, p.counts, k, metric, p.out_ids, p.out_dist,
+                           p.out_count));
+        CKS(flush_out(ctx, pending));
+        return VS_OK;
+    }
+    CKS(arena_alloc(ctx, n_in, &p.s_key));
+    CKS(arena_alloc(ctx, n_in, &p.s_id));
     {
         KTimer kt(ctx, VS_K_MERGE);
         CK(vs::launch_merge(p, ctx->stream));
@@ -1303,6 +1384,7 @@ int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, cons
     if (n_total > 0 && !list_ids) return set_err(VS_ERR_PARAMETER, "null list ids");
     vs_ivf* v = new vs_ivf();
     v->ctx = ctx;
+    ctx_ref(ctx);   // balanced by vs_ivf_free (also on the failure paths below)
     v->nlist = nlist;
     v->d = d;
     v->metric = metric;
@@ -1465,7 +1547,9 @@ int vs_ivf_free(vs_ivf* v) {
     cudaFree(v->pnorms);
     cudaFree(v->pmax);
     if (v->owned) cudaFree(v->owned);
+    vs_ctx* ctx = v->ctx;
     delete v;
+    ctx_unref(ctx);
     return VS_OK;
 }
 
@@ -1816,7 +1900,6 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     CKS(validate_k(k));
     if (nprobe < 1) return set_err(VS_ERR_PARAMETER, "nprobe must be >= 1");
     if (nprobe > ivf->nlist) return set_err(VS_ERR_PARAMETER, "nprobe %d > nlist %d", nprobe, ivf->nlist);
-    if (nprobe > kTopkCap) return set_err(VS_ERR_CAP_EXCEEDED, "nprobe %d exceeds device cap", nprobe);
     if (nq < 0) return set_err(VS_ERR_PARAMETER, "negative query count");
     DevGuard g(ctx->device);
     CK(ctx->arena.reset());
@@ -1898,7 +1981,33 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     if (!job.out_ids) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_ids));
     if (!job.out_dist) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_dist));
     if (!job.out_count) CKS(arena_alloc(ctx, (size_t)nq, &job.out_count));
-    CKS(run_ivf_scan(ctx, job, sm, 0, true));
+    if (k > kTopkCap) {
+        // k' above the candidate buffers: every candidate of the probed lists
+        // is keyed, selected and re-ranked device-wide (vs_wide.cu)
+        if (ivf->n_total > (int64_t)UINT32_MAX) return set_err(VS_ERR_PARAMETER, "wide IVF search: > 2^32 rows");
+        vs::WideJob w{};
+        w.q = dq;
+        w.nq = nq;
+        w.d = d;
+        w.rows = ivf->payload;
+        w.dtype = ivf->dtype;
+        w.margin = sm;
+        w.ip = ivf->metric;
+        w.k = k;
+        w.id_map = ivf->list_ids;
+        w.out_ids = job.out_ids;
+        w.out_dist = job.out_dist;
+        w.out_count = job.out_count;
+        w.cls_scan = VS_K_IVF_SCAN;
+        w.cls_rerank = VS_K_IVF_RERANK;
+        CKS(vs::wide_ivf(ctx, w, probes, nprobe, ivf->list_off, ivf->h_off, ivf->owned, pbits, ivf->pnorms));
+        int32_t* scratch = nullptr;
+        CKS(arena_alloc(ctx, (size_t)ivf->nlist, &scratch));
+        CK(vs::launch_visited_count(probes, nq, nprobe, ivf->list_off, ivf->nlist, ivf->owned, pbits, scratch, vis,
+                                    ctx->stream));
+    } else {
+        CKS(run_ivf_scan(ctx, job, sm, 0, true));
+    }
     unsigned long long h_vis = 0;
     CK(cudaMemcpyAsync(&h_vis, vis, sizeof(h_vis), cudaMemcpyDeviceToHost, ctx->stream));
     CKS(flush_out(ctx, pending));

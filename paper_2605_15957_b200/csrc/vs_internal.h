@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -142,6 +143,12 @@ struct vs_ctx {
     std::vector<cudaEvent_t> event_pool;
     int64_t kt_ns[VS_K_N] = {0};
     int64_t kt_count[VS_K_N] = {0};
+    // columns and indexes created through this context use its device and
+    // stream until they are freed: vs_ctx_destroy with objects alive only
+    // releases the scratch and leaves the struct to the last object's free
+    std::mutex life_mu;
+    int live_objects = 0;
+    bool destroyed = false;
 };
 
 struct vs_column {
@@ -251,6 +258,10 @@ inline void resolve_timers(vs_ctx* ctx) {
 }
 
 }  // namespace vs_internal
+
+// lifetime of a context's dependent objects (vs_capi.cu)
+void ctx_ref(vs_ctx* ctx);
+void ctx_unref(vs_ctx* ctx);
 
 int ivf_make(vs_ctx* ctx, const float* centroids, int32_t nlist, int32_t d, const std::vector<int64_t>& sizes,
              const int64_t* list_ids, const void* list_payload, int32_t dtype, int32_t metric,

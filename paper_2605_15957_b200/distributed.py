@@ -187,7 +187,16 @@ def two_phase_search(shard, comm, queries, k: int, metric: str = "squared_l2", r
     provides allreduce_min and allgather_topk. Returns (ids, dist, counts) of
     the global result on every rank (torch tensors on the shard's device)."""
     import torch
+
+    from . import _native as N
     merge = merge or gpu_merge
+    if k > N.topk_cap():
+        # k' above the candidate buffers (device-wide large-k' path): one phase,
+        # every shard's exact local top-k', all-gather + merge
+        ri, rd, rc = shard.plain(queries, k, metric, row_filter, id_offset)
+        gi, gd, gc = comm.allgather_topk(ri, rd, rc)
+        shard.reruns = 0
+        return merge(gi, gd, gc, k, metric)
     keys = shard.begin(queries, k, metric, row_filter)        # [Q, k] upper bounds on exact keys
     T = shard.union_kth(comm.allgather(keys))               # [Q] >= global k-th exact key
     ids, dist, cnt, bound = shard.finish(T, id_offset)

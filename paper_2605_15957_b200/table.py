@@ -101,6 +101,8 @@ class EmbeddingColumn:
             raise ShapeError("from_device needs a 2-D CUDA tensor")
         if tensor.dtype not in (torch.float32, torch.bfloat16):
             raise ShapeError("device embeddings must be float32 or bfloat16")
+        if tensor.numel() and not bool(torch.isfinite(tensor).all()):   # table.py:110-111
+            raise ShapeError("embedding values contain NaN or Inf")
         obj = cls.__new__(cls)
         obj._values = None
         obj.dim = int(tensor.shape[1])
@@ -249,6 +251,23 @@ class Table:
         return self.columns[name]
 
 
+def _gather_embedding(col, rows):
+    """Rows of an embedding column. A device-resident column is gathered on
+    the GPU (vs_gather_rows) and stays there: its host copy would be the whole
+    collection (e.g. 41 GB), not the result rows."""
+    if getattr(col, "_dev_tensor", None) is not None:
+        import torch
+
+        from .output import gather_rows
+        t = col._dev_tensor
+        idx = torch.from_numpy(rows).to(t.device)
+        return EmbeddingColumn.from_device(gather_rows(t, idx))
+    if getattr(col, "_host_stream", None) is not None:
+        src = col._host_stream
+        return EmbeddingColumn(src[rows].float().numpy() if N_is_torch(src) else np.asarray(src)[rows])
+    return EmbeddingColumn(col.values[rows])
+
+
 def gather(table, rows) -> Table:
     rows = np.asarray(rows, dtype=np.int64)
     if rows.size and (rows.min() < 0 or rows.max() >= table.row_count):
@@ -256,7 +275,7 @@ def gather(table, rows) -> Table:
     cols = {}
     for name, ftype in table.schema.fields:
         col = table.columns[name]
-        cols[name] = EmbeddingColumn(col.values[rows]) if ftype.is_embedding else np.asarray(col)[rows]
+        cols[name] = _gather_embedding(col, rows) if ftype.is_embedding else np.asarray(col)[rows]
     valid = {n: np.asarray(m)[rows] for n, m in table.valid.items()}
     return Table(Schema(list(table.schema.fields)), cols, valid)
 

@@ -16,9 +16,11 @@ uint32 bitmap (LSB-first), or an ascending int64 selection vector. Results
 then carry BASE row ids, identical to the reference composition
 `rows = flatnonzero(mask); nt = enn_search(Q, base[rows]); rows[nt.data_row]`.
 
-Every search runs on the GPU; there is no host fallback (k' above the device
-cap raises CapExceededError, exactly the reference's device contract,
-vecsearch.py:86-87).
+Every search runs on the GPU, for any k' (there is no host fallback): k' up to
+vs_topk_cap() = 2048 uses the candidate-buffer kernels, larger k' (e.g. the
+reference's k' = 500 k oversampling, plans.py:256) the device-wide select /
+re-rank of vs_wide.cu. CapExceededError is the operator's placement contract
+(vecsearch.py:86-87), raised by `vector_search_operator` only.
 """
 
 from __future__ import annotations
@@ -270,9 +272,8 @@ def enn_search_raw(queries, data, k: int, metric: str = SQUARED_L2, row_filter=N
         raise ShapeError(f"query dim {qd} != data dim {d}")
     if n == 0:
         raise EmptyInputError("exhaustive search over empty data side")
-    if k > N.topk_cap():
-        from .errors import CapExceededError
-        raise CapExceededError(k, N.topk_cap())
+    if k < 1:
+        raise ParameterError(f"k must be >= 1, got {k}")
     bm = filter_bitmap(row_filter, n)
     dc = device_column(data, ctx)
     ids, dist, cnt = out if out is not None else _outputs(nq, k)
@@ -521,9 +522,6 @@ class IvfIndex:
         if self.layout == NON_OWNING and self.base is None:
             raise ParameterError("non-owning IVF index has no attached base column")
         k = int(params.k_prime)
-        if k > N.topk_cap():
-            from .errors import CapExceededError
-            raise CapExceededError(k, N.topk_cap())
         if qcol.count == 0:
             return NeighborTable(np.empty(0, np.int64), np.empty(0, np.int64),
                                  np.empty(0, np.float64), np.empty(0, np.int64), 0, self.metric, 0)

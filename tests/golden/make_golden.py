@@ -98,7 +98,61 @@ def make_postfilter_golden():
     np.savez_compressed(HERE / "postfilter.npz", **res)
 
 
+def make_q15_ivf_golden():
+    """The Q15 'ivf' plan (plans.py:571-574) through the reference executor at
+    SF=0.01 with the runner's IVF catalog (runner.py:26-56: nlist =
+    default_nlist(n), seed 0): its vector_search call (k' = 500 k = 50,000 >
+    every candidate) and the semi-join post-filter after it."""
+    from sqlvs.executor import IndexCatalog
+    from sqlvs.runner import default_nlist
+    import sqlvs.vecsearch as vsm
+    ds = generate(DatasetSpec(sf=0.01))
+    col = ds.table("reviews").column("rv_embedding")
+    nlist = min(default_nlist(col.count), col.count)
+    idx = IvfIndex.build(col, nlist=nlist, seed=0)
+    cat = IndexCatalog()
+    cat.register("ivf:reviews", idx, col)
+    calls, posts = [], []
+    orig_vs, orig_pf = ex.vector_search_operator, ex.oversample_postfilter
+
+    def spy(qt, qf, dt, df, params, metric="squared_l2", index=None, **kw):
+        out, stats = orig_vs(qt, qf, dt, df, params, metric=metric, index=index, **kw)
+        calls.append(dict(qt=qt, qf=qf, params=params, out=out, stats=stats))
+        return out, stats
+
+    def spy_pf(vs_output, keep, k, keep_set=None, semi_keys=None):
+        out, short = orig_pf(vs_output, keep, k, keep_set=keep_set, semi_keys=semi_keys)
+        posts.append(dict(out=out, short=short, keep_set=keep_set, semi_keys=semi_keys, k=k))
+        return out, short
+
+    ex.vector_search_operator, ex.oversample_postfilter = spy, spy_pf
+    try:
+        run = ex.execute_base(builtin_plan("Q15", "ivf"), ds, cat)
+    finally:
+        ex.vector_search_operator, ex.oversample_postfilter = orig_vs, orig_pf
+    (c,), (pf,) = calls, posts
+    o, po = c["out"], pf["out"]
+    left, right = pf["semi_keys"]
+    np.savez_compressed(
+        HERE / "q15_ivf.npz", nlist=nlist, centroids=idx.centroids,
+        sizes=np.array([len(p) for p in idx.partitions], np.int64),
+        ids=np.concatenate(idx.partitions).astype(np.int64),
+        queries=c["qt"].column(c["qf"]).values, k=c["params"].k, k_prime=c["params"].k_prime,
+        nprobe=c["params"].nprobe, visited=c["stats"].visited_rows,
+        vs_query_row=np.asarray(o.column("vs_query_row")), vs_data_row=np.asarray(o.column("vs_data_row")),
+        vs_distance=np.asarray(o.column("vs_distance")), vs_rank=np.asarray(o.column("vs_rank")),
+        keep_set=np.asarray(pf["keep_set"].column(right)), semi_left=left, pf_k=pf["k"],
+        pf_data_row=np.asarray(po.column("vs_data_row")), pf_distance=np.asarray(po.column("vs_distance")),
+        pf_rank=np.asarray(po.column("vs_rank")),
+        pf_short=np.array([pf["short"].get(0, 0)], np.int64),
+        final_reviewkey=np.asarray(run.output.column("rv_reviewkey")) if hasattr(run, "output") else
+        np.asarray(run.result.column("rv_reviewkey")))
+
+
 def main():
+    if "--only" in sys.argv:
+        globals()["make_" + sys.argv[sys.argv.index("--only") + 1] + "_golden"]()
+        return
     meta = {}
     # --- synth pins ---------------------------------------------------------
     ds = generate(DatasetSpec(sf=0.01))
@@ -227,6 +281,7 @@ def main():
     # (vecsearch.py:64-202) on small tables: Q11's cross-side "key_d != key",
     # Q15's semi join, a rank predicate, shortfalls (k' rows that do not survive)
     make_postfilter_golden()
+    make_q15_ivf_golden()
 
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print("golden fixtures written to", HERE)

@@ -130,3 +130,43 @@ def test_postfilter(golden):
         assert np.array_equal(rank[kept], g[f"{name}_rank"]), name
         assert sorted(short) == g[f"{name}_short_q"].tolist(), name
         assert [short[q] for q in sorted(short)] == g[f"{name}_short_n"].tolist(), name
+
+
+def test_q15_ivf_plan_vector_search(golden, sf001):
+    """The reference's Q15 'ivf' plan at SF=0.01 (k' = 50,000 over nprobe=32
+    of nlist=1024 lists): the oracle's IVF search over the reference's own
+    index reproduces the operator's vs_* columns and the semi-join post-filter."""
+    g = golden("q15_ivf.npz")
+    sizes = g["sizes"]
+    parts = np.split(g["ids"], np.cumsum(sizes)[:-1])
+    reviews = sf001["reviews"]
+    res = O.ivf_search(g["queries"], g["centroids"], parts, lambda c: reviews[parts[c]], int(g["nprobe"]),
+                       int(g["k_prime"]))
+    assert res.visited_rows == int(g["visited"])
+    assert np.array_equal(res.data_row, g["vs_data_row"])
+    assert np.array_equal(res.distance, g["vs_distance"])
+    assert np.array_equal(res.rank, g["vs_rank"])
+    keep = np.isin(sf001["review_partkeys"][res.data_row], g["keep_set"])
+    kept, short = O.oversample_postfilter(res.query_row, keep, int(g["pf_k"]))
+    assert np.array_equal(res.data_row[kept], g["pf_data_row"])
+    assert np.array_equal(res.distance[kept], g["pf_distance"])
+    assert short.get(0, 0) == int(g["pf_short"][0])
+
+
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+def test_pruned_oracle_equals_enn_search(metric):
+    """oracle.enn_pruned (the large-N checker of the scale tests) == enn_search,
+    duplicates and ties included."""
+    r = np.random.default_rng(9)
+    x = r.standard_normal((30000, 48)).astype(np.float32)
+    x[100] = x[5]
+    x[7] = x[5]
+    x[200:260] = x[300]
+    q = np.concatenate([r.standard_normal((4, 48)), x[[5, 300]]]).astype(np.float32)
+    ids = np.sort(r.choice(90000, 30000, replace=False))
+    for k in (1, 64, 2500):
+        a = O.enn_search(q, x, k, metric, row_ids=ids)
+        b = O.enn_pruned(q, x, k, metric, row_ids=ids, block=7000)
+        assert np.array_equal(a.query_row, b.query_row)
+        assert np.array_equal(a.data_row, b.data_row)
+        assert np.array_equal(a.distance, b.distance)
