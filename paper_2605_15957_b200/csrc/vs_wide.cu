@@ -415,7 +415,8 @@ int wide_finish(vs_ctx* ctx, const WideJob& j, const float* keys, const int64_t*
     if (S > 0) {
         LeafPlan plan;
         np_leaves(j.d, plan);
-        const bool warp = plan.nleaf <= 32;
+        // leaves shorter than 8 (d < 8) are plain sequential sums: per-thread path
+        const bool warp = plan.nleaf <= 32 && j.d >= 8;
         const int64_t units = warp ? (S + WS_NT / 32 - 1) / (WS_NT / 32) : (S + WS_NT - 1) / WS_NT;
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)ctx->sm_count * 8));
         const float* Qc = j.q + (q0 + (qa - q0)) * (int64_t)j.d;   // s_q is relative to qa

@@ -101,8 +101,11 @@ class EmbeddingColumn:
             raise ShapeError("from_device needs a 2-D CUDA tensor")
         if tensor.dtype not in (torch.float32, torch.bfloat16):
             raise ShapeError("device embeddings must be float32 or bfloat16")
-        if tensor.numel() and not bool(torch.isfinite(tensor).all()):   # table.py:110-111
-            raise ShapeError("embedding values contain NaN or Inf")
+        # table.py:110-111; in row chunks so the check's temporaries stay small
+        step = max(1, (1 << 26) // max(1, int(tensor.shape[1])))
+        for i in range(0, int(tensor.shape[0]), step):
+            if not bool(torch.isfinite(tensor[i:i + step]).all()):
+                raise ShapeError("embedding values contain NaN or Inf")
         obj = cls.__new__(cls)
         obj._values = None
         obj.dim = int(tensor.shape[1])
