@@ -43,10 +43,11 @@ enum vs_status {
     VS_ERR_SHAPE = 1,        /* ShapeError: dim mismatch                      */
     VS_ERR_EMPTY_INPUT = 2,  /* EmptyInputError: exhaustive search, no rows   */
     VS_ERR_PARAMETER = 3,    /* ParameterError: bad k / nprobe / nlist / ...  */
-    VS_ERR_CAP_EXCEEDED = 4, /* CapExceededError: k' > vs_topk_cap()          */
+    VS_ERR_CAP_EXCEEDED = 4, /* CapExceededError (two-phase search, k' > cap) */
     VS_ERR_PLACEMENT = 5,    /* PlacementError: device memory exhausted       */
     VS_ERR_CUDA = 6,         /* CUDA runtime / launch failure                 */
-    VS_ERR_INTERNAL = 7
+    VS_ERR_INTERNAL = 7,
+    VS_ERR_NCCL = 8          /* NCCL failure in a device-group exchange       */
 };
 
 enum vs_metric { VS_METRIC_SQUARED_L2 = 0, VS_METRIC_INNER_PRODUCT = 1 };
@@ -93,9 +94,12 @@ typedef struct vs_ivf vs_ivf;
 
 /* thread-local message for the last non-OK status */
 const char* vs_last_error(void);
-/* device top-k cap: k' above it returns VS_ERR_CAP_EXCEEDED
- * (reference: HardwareProfile.gpu_topk_cap = 2048, placement.py:56;
- *  vecsearch.py:86-87) */
+/* top-k of the candidate-buffer kernels (= the reference's default
+ * HardwareProfile.gpu_topk_cap, placement.py:56). Searches accept any k'
+ * >= 1: above this value they run the device-wide large-k' path
+ * (vs_wide.cu). VS_ERR_CAP_EXCEEDED remains only for the two-phase
+ * protocol (k' <= cap); the operator's placement cap (vecsearch.py:86-87)
+ * is a host-side check. */
 int32_t vs_topk_cap(void);
 int32_t vs_version(void);
 
@@ -230,6 +234,55 @@ int vs_ivf_search_probed(vs_ctx* ctx, const vs_ivf* ivf, const float* queries, i
                          const int32_t* probes, int32_t k, int64_t* out_ids, double* out_dist,
                          int32_t* out_count, int64_t* out_visited);
 int vs_ivf_free(vs_ivf* ivf);
+
+/* ---- single-process device groups ------------------
+ * One interpreter driving several GPUs (the reference's executor runs the
+ * operator from one process, executor.py:109-181): a group holds one
+ * context per device (vs_group_ctx: create each member's shard column / index
+ * part with it) and, for distinct devices, an NCCL clique (ncclCommInitAll;
+ * NCCL is dlopen'ed, failures -> VS_ERR_NCCL). A group search runs every
+ * member's shard search concurrently (one host thread each), all-gathers the
+ * [Q, k] (id, distance, count) triples with ncclAllGather inside one
+ * ncclGroupStart/End, and merges them on member 0 (tie rule). A group that
+ * repeats a device (or VS_GROUP_NO_NCCL=1) gathers with peer copies; the
+ * results are identical either way and equal the one-GPU search.
+ *   vs_group_enn_search: shards[i] = rows [row_lo[i], row_lo[i] + n_i) of the
+ *     collection, contiguous, row_lo[i] % 32 == 0 when a bitmap is given (the
+ *     global host bitmap is sliced by words); ids are global rows.
+ *   vs_group_ivf_search: parts[i] = member i's index over the lists it owns
+ *     (same centroids everywhere, other lists empty, e.g. LPT-assigned).
+ * Queries, bitmaps and outputs are host memory. */
+typedef struct vs_group vs_group;
+int vs_group_create(int32_t ndev, const int32_t* devices, vs_group** out);
+int vs_group_destroy(vs_group* g);
+int vs_group_info(const vs_group* g, int32_t* ndev, int32_t* uses_nccl);
+vs_ctx* vs_group_ctx(vs_group* g, int32_t member);
+int vs_group_enn_search(vs_group* g, vs_column* const* shards, const int64_t* row_lo, const float* queries,
+                        int64_t nq, int32_t d, const uint32_t* bitmap, int64_t nbits, int32_t k,
+                        int32_t metric, int64_t* out_ids, double* out_dist, int32_t* out_count,
+                        int64_t* out_visited);
+int vs_group_ivf_search(vs_group* g, vs_ivf* const* parts, const float* queries, int64_t nq,
+                        const uint32_t* bitmap, int64_t nbits, int32_t nprobe, int32_t k,
+                        int64_t* out_ids, double* out_dist, int32_t* out_count, int64_t* out_visited);
+
+/* ---- native loaders: reference file formats straight into device buffers --
+ * (one contiguous copy per file section, not
+ * 5 nlist + 1). Every section streams through a pinned double buffer (disk
+ * read of chunk i + 1 overlaps the copy of chunk i).
+ *   vs_ivf_load: an SVIX IVF file (save_index, vecindex.py:495-579 / load_index
+ *     :539-579) -> device IVF; list ids and the owning payload land in their
+ *     final device buffers (the payload is adopted, not copied again).
+ *     Non-owning files need `base` (rows gathered into the list-contiguous
+ *     layout on the device). info (nullable) [6] = kind, metric, layout,
+ *     nlist, dim, count. Bad magic / version / kind -> VS_ERR_PARAMETER
+ *     (the reference's ParameterError).
+ *   vs_emb_info: header of a .emb file (write_embeddings, datagen.py:351-372):
+ *     count, dim and the byte offset of the float32 rows.
+ *   vs_file_to_device: `bytes` of a file from `offset` into dst (device or
+ *     host memory), e.g. the rows of a .emb file into a device column. */
+int vs_ivf_load(vs_ctx* ctx, const char* path, const vs_column* base, int64_t* info, vs_ivf** out);
+int vs_emb_info(const char* path, int64_t* count, int32_t* dim, int64_t* data_offset);
+int vs_file_to_device(vs_ctx* ctx, const char* path, int64_t offset, int64_t bytes, void* dst);
 
 /* ---- relational filters -> packed row bitmaps (the step before the search) -
  * Output words are the row_filter format above. valid_bits (nullable) is the

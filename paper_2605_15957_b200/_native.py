@@ -20,7 +20,7 @@ LIB_NAME = "libvsb200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 
 VS_OK, VS_ERR_SHAPE, VS_ERR_EMPTY_INPUT, VS_ERR_PARAMETER = 0, 1, 2, 3
-VS_ERR_CAP_EXCEEDED, VS_ERR_PLACEMENT, VS_ERR_CUDA, VS_ERR_INTERNAL = 4, 5, 6, 7
+VS_ERR_CAP_EXCEEDED, VS_ERR_PLACEMENT, VS_ERR_CUDA, VS_ERR_INTERNAL, VS_ERR_NCCL = 4, 5, 6, 7, 8
 METRIC_CODE = {"squared_l2": 0, "inner_product": 1}
 DTYPE_F32, DTYPE_BF16 = 0, 1
 OPT_ENN_KERNEL, OPT_IVF_KERNEL, OPT_CAND_SLACK, OPT_FORCE_RETRY, OPT_TIMING = 1, 2, 3, 4, 5
@@ -81,6 +81,17 @@ SIGNATURES = {
     "vs_ivf_search_probed": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp,
                                        C.POINTER(_i64)]),
     "vs_ivf_free": (C.c_int, [_vp]),
+    "vs_group_create": (C.c_int, [_i32, _vp, C.POINTER(_vp)]),
+    "vs_group_destroy": (C.c_int, [_vp]),
+    "vs_group_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "vs_group_ctx": (_vp, [_vp, _i32]),
+    "vs_group_enn_search": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp,
+                                      C.POINTER(_i64)]),
+    "vs_group_ivf_search": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp,
+                                      C.POINTER(_i64)]),
+    "vs_ivf_load": (C.c_int, [_vp, C.c_char_p, _vp, _vp, C.POINTER(_vp)]),
+    "vs_emb_info": (C.c_int, [C.c_char_p, C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64)]),
+    "vs_file_to_device": (C.c_int, [_vp, C.c_char_p, _i64, _i64, _vp]),
 }
 
 _lib = None
@@ -129,6 +140,8 @@ def check(status: int, what: str = "") -> None:
         raise err
     if status == VS_ERR_PLACEMENT:
         raise E.PlacementError(msg)
+    if status == VS_ERR_NCCL:
+        raise E.CollectiveError(msg)
     raise E.DeviceError(f"status {status}: {msg}")
 
 
@@ -170,9 +183,20 @@ class Context:
         self.handle = h
         self.device = int(device)
 
+    @classmethod
+    def borrowed(cls, handle, device: int, owner=None) -> "Context":
+        """A member context of a device group (the group destroys it)."""
+        obj = cls.__new__(cls)
+        obj.handle = _vp(handle)
+        obj.device = int(device)
+        obj._owner = owner       # keeps the group alive while the member is used
+        return obj
+
     def close(self) -> None:
-        """Destroy the library context (its scratch arena and stream). Columns
-        and indexes created through it keep it alive (they hold a reference)."""
+        """Destroy the library context (scratch arena, streams). Columns and
+        indexes created through it stay valid until they are freed."""
+        if getattr(self, "_owner", None) is not None:
+            return
         h, self.handle = getattr(self, "handle", None), None
         if h:
             load().vs_ctx_destroy(h)

@@ -292,3 +292,56 @@ def project(table, names: Sequence[str]) -> Table:
 def filter_rows(table, mask) -> Table:
     """Order-preserving row subset (table.py:326-331)."""
     return gather(table, np.flatnonzero(np.asarray(mask, dtype=bool)))
+
+
+# ---- .emb files (datagen.py:351-372) ----------------------------------------------------------
+
+_EMB_MAGIC = b"SVEC"
+
+
+def write_embeddings(path, column) -> None:
+    """The reference's .emb writer: magic, <HBBQI header, float32 rows."""
+    import struct
+    values = column.values if hasattr(column, "values") else np.asarray(column, np.float32)
+    with open(path, "wb") as f:
+        f.write(_EMB_MAGIC)
+        f.write(struct.pack("<HBBQI", 1, 0, 0, values.shape[0], values.shape[1]))
+        f.write(np.ascontiguousarray(values, dtype="<f4").tobytes())
+
+
+def read_embeddings(path, device=None) -> EmbeddingColumn:
+    """Read a .emb file. device=None: a host column (the reference's reader).
+    With a device (CUDA ordinal or library Context) the rows stream from the
+    file through a pinned double buffer straight into a device column
+    (vs_file_to_device): no host copy of the collection."""
+    from . import _native as N
+    from .errors import ParameterError
+    count, dim, off = C_i64(), C_i32(), C_i64()
+    N.check(N.load().vs_emb_info(str(path).encode(), count, dim, off), "emb_info")
+    n, d = int(count.value), int(dim.value)
+    if device is None:
+        with open(path, "rb") as f:
+            f.seek(int(off.value))
+            raw = f.read(n * d * 4)
+        if len(raw) != n * d * 4:
+            raise ParameterError("embedding file truncated")
+        return EmbeddingColumn(np.frombuffer(raw, dtype="<f4").reshape(n, d).copy())
+    import torch
+
+    from .vecindex import _ctx
+    ctx = _ctx(device)
+    t = torch.empty((n, d), dtype=torch.float32, device=torch.device("cuda", ctx.device))
+    N.check(N.load().vs_file_to_device(ctx.handle, str(path).encode(), int(off.value), n * d * 4,
+                                       t.data_ptr()), "file_to_device")
+    return EmbeddingColumn.from_device(t)
+
+
+def C_i64():
+    import ctypes
+    return ctypes.c_int64(0)
+
+
+def C_i32():
+    import ctypes
+    return ctypes.c_int32(0)
+

@@ -119,6 +119,30 @@ def _ctx(device=None) -> N.Context:
     return N.Context.get(device)
 
 
+def _group(device):
+    """The device group a search runs on: an explicit DeviceGroup, or the
+    default set by group.use_devices() when no device is named."""
+    from .group import DeviceGroup, default_group
+    if isinstance(device, DeviceGroup):
+        return device
+    if device is None:
+        return default_group()
+    return None
+
+
+def _into(out, res):
+    """Copy a group search's host result into caller-provided buffers."""
+    if out is None:
+        return res
+    for dst, src in zip(out, res[:3]):
+        if N.is_torch(dst):
+            import torch
+            dst.copy_(torch.from_numpy(src))
+        else:
+            dst[...] = src
+    return tuple(out) + tuple(res[3:])
+
+
 def _dims(col):
     return int(col.count), int(col.dim)
 
@@ -264,6 +288,12 @@ def enn_search_raw(queries, data, k: int, metric: str = SQUARED_L2, row_filter=N
     counts [nq], visited). `out` may supply (ids, dist, counts) buffers
     (host numpy, pinned or CUDA torch tensors)."""
     check_metric(metric)
+    grp = _group(device)
+    if grp is not None:
+        if int(k) < 1:
+            raise ParameterError(f"k must be >= 1, got {k}")
+        res = grp.enn_search_raw(queries, data, int(k), metric, row_filter)
+        return _into(out, res)
     ctx = _ctx(device)
     data = _as_column(data)
     n, d = _dims(data)
@@ -533,6 +563,11 @@ class IvfIndex:
                    out=None, want_probes=True, probes_in=None):
         """Padded device-layout search. `probes_in` ([nq, nprobe] int32, host
         or device) skips the coarse quantizer (multi-GPU query-sliced probing)."""
+        grp = _group(device) if list_owned is None and probes_in is None else None
+        if grp is not None:
+            ids, dist, cnt, vis = grp.ivf_search_raw(self, queries, int(k), int(nprobe), row_filter)
+            out = _into(out, (ids, dist, cnt))
+            return out[0], out[1], out[2], None, vis
         ctx = _ctx(device)
         div = self.device_index(ctx, list_owned)
         q, nq, d = _query_buffer(queries)
@@ -669,8 +704,21 @@ def save_index(index, path) -> None:
                 _write_array(f, np.concatenate(list(index.payload), axis=0).reshape(-1), "<f4")
 
 
-def load_index(path, base=None):
-    """Load an index; non-owning layouts need the base column re-attached."""
+def load_index(path, base=None, device=None):
+    """Load an index; non-owning layouts need the base column re-attached.
+
+    device=None: the reference's host load (per-list numpy arrays). With a
+    device (CUDA ordinal or library Context), an IVF file goes through the
+    native loader (vs_ivf_load): its sections stream through one pinned
+    double buffer straight into the device index (one contiguous copy per
+    section); centroids and partitions are exported back
+    for the host-side fields, the payload stays on the device (`.payload`
+    exports it on first access)."""
+    if device is not None:
+        with open(path, "rb") as f:
+            head = f.read(9)
+        if len(head) == 9 and head[:4] == _MAGIC and head[6] == _KIND_CODE["ivf"]:
+            return _load_ivf_device(path, base, device)
     with open(path, "rb") as f:
         magic = f.read(4)
         if magic != _MAGIC:
@@ -698,3 +746,28 @@ def load_index(path, base=None):
                        (np.split(flat_payload, np.cumsum(sizes)[:-1]) if p1 > 1 else [flat_payload])]
         return IvfIndex(p1, dim, count, metric, layout, centroids, partitions, payload,
                         base=base if layout == NON_OWNING else None)
+
+
+def _load_ivf_device(path, base, device):
+    ctx = _ctx(device)
+    info = np.zeros(6, np.int64)
+    dc = device_column(_as_column(base), ctx) if base is not None else None
+    h = C.c_void_p()
+    N.check(N.load().vs_ivf_load(ctx.handle, str(path).encode(), dc.handle if dc is not None else None,
+                                 N.ptr(info), C.byref(h)), "ivf_load")
+    div = N.DeviceIvf(ctx, h)
+    _, metric_code, layout_code, nlist, dim, count = (int(v) for v in info)
+    metric = {v: k for k, v in _METRIC_CODE.items()}[metric_code]
+    layout = {v: k for k, v in _LAYOUT_CODE.items()}[layout_code]
+    centroids = np.empty((nlist, dim), np.float32)
+    sizes = np.empty(nlist, np.int64)
+    ids = np.empty(div.n_total, np.int64)
+    N.check(N.load().vs_ivf_export(h, N.ptr(centroids), N.ptr(sizes), N.ptr(ids), None), "ivf_export")
+    partitions = np.split(ids, np.cumsum(sizes)[:-1]) if nlist > 1 else [ids]
+    idx = IvfIndex(nlist, dim, count, metric, layout, centroids, partitions, None,
+                   base=_as_column(base) if layout == NON_OWNING and base is not None else None)
+    idx._dev[ctx.device] = div
+    if layout == OWNING:
+        idx.payload = _LazyPayload(idx)
+    return idx
+

@@ -149,6 +149,13 @@ def make_q15_ivf_golden():
         np.asarray(run.result.column("rv_reviewkey")))
 
 
+def make_emb_golden():
+    """A small .emb file written by the reference's writer (datagen.py:355-360)."""
+    from sqlvs.datagen import write_embeddings
+    x = np.random.default_rng(17).standard_normal((500, 48)).astype(np.float32)
+    write_embeddings(HERE / "ref_small.emb", EmbeddingColumn(x))
+
+
 def main():
     if "--only" in sys.argv:
         globals()["make_" + sys.argv[sys.argv.index("--only") + 1] + "_golden"]()
@@ -282,6 +289,7 @@ def main():
     # Q15's semi join, a rank predicate, shortfalls (k' rows that do not survive)
     make_postfilter_golden()
     make_q15_ivf_golden()
+    make_emb_golden()
 
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print("golden fixtures written to", HERE)
