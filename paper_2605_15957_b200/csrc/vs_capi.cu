@@ -1756,7 +1756,47 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         CKS(arena_alloc(ctx, (size_t)job.nq * n_sub, &cb.cnt));
         CKS(arena_alloc(ctx, (size_t)job.nq, &cb.overflow));
         CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
-        if (lmajor) {
+        static const int sel_env = getenv("VS_IVF_SEL") ? atoi(getenv("VS_IVF_SEL")) : 1;
+        if (lmajor && job.pbits && sel_env && v->n_total < (int64_t)UINT32_MAX) {
+            // filtered: pre-selected rows per list, one round trip per unit (vs_ivf_sel.cu)
+            IvfGroups gr;
+            CKS(ivf_group(ctx, job, vs::kIvfLmQT, &gr));
+            CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
+            vs::IvfSelLaunch a;
+            a.Q = job.q;
+            a.nq = job.nq;
+            a.d = v->d;
+            a.payload = v->payload;
+            a.list_off = v->list_off;
+            a.nlist = v->nlist;
+            a.pbits = job.pbits;
+            a.nprobe = job.nprobe;
+            a.pair_codes = gr.pair_codes;
+            a.units = gr.units;
+            a.n_units = gr.uoff + v->nlist;
+            a.max_units = gr.max_units;
+            a.margin = margin;
+            a.ip = v->metric;
+            a.k = job.k;
+            a.cb = cb;
+            a.visited = vis;
+            CKS(arena_alloc(ctx, (size_t)v->nlist, &a.lsel));
+            CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.lsel64));
+            CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.sel_off));
+            CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(v->n_total, 1), &a.spos));
+            char* recs = nullptr;
+            CKS(arena_alloc(ctx, (size_t)gr.max_units * vs::kIvfSelRecBytes, &recs));
+            a.recs = recs;
+            a.tmp_bytes = vs::ivf_sel_temp_bytes(v->nlist);
+            char* tmp = nullptr;
+            CKS(arena_alloc(ctx, a.tmp_bytes, &tmp));
+            a.tmp = tmp;
+            a.sm_count = ctx->sm_count;
+            KTimer kt(ctx, VS_K_IVF_SCAN);
+            if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_sel<float>(a, ctx->stream));
+            else CK(vs::launch_ivf_scan_sel<__nv_bfloat16>(a, ctx->stream));
+            ctx->stats[VS_STAT_LAUNCHES] += 5;
+        } else if (lmajor) {
             IvfGroups gr;
             CKS(ivf_group(ctx, job, vs::kIvfLmQT, &gr));
             int* work = nullptr;

@@ -1,0 +1,396 @@
+// Phase A of the FILTERED IVF search, list-major over pre-selected rows.
+//
+// With a selective filter (config 3: 1 %), a probed list of ~610 rows holds
+// ~6 selected rows, and the scan is a stream of tiny, independent units:
+// (list, <= 8 (query, probe) pairs) x (selected rows of the list). The
+// list-major kernel (vs_ivf_lmajor.cu) spent its time on dependent global
+// round trips per unit (work ticket, unit, pair codes, queries, bitmap words,
+// selected positions, rows). Here every unit needs ONE:
+//   1. once per search, the selected payload positions of every list are
+//      compacted in list order (k_list_sel_positions: one warp per list over
+//      the permuted bitmap), and every unit gets a 128-byte record with its
+//      list, pair codes, selected-row count and first 16 positions
+//      (k_make_recs);
+//   2. a CTA walks its units in a fixed stride (no work-counter atomics); the
+//      record of its NEXT unit is loaded while the current one is scored, so
+//      at the top of a unit the row positions and the queries are known: the
+//      selected rows (cp.async, 16 bytes, coalesced) and the unit's queries
+//      (into registers) are requested together and arrive in one round trip;
+//   3. scoring and candidate appends are those of the list-major kernel: two
+//      queries per warp held in registers, staged rows from shared memory,
+//      fp32 direct form (error bound eps_simt), one butterfly transpose-
+//      reduction per chunk, per-pair candidate buffers.
+// Reference: IvfIndex.search, vecindex.py:230-258, with the filtered
+// extension rows = rows[mask[rows]].
+#include <cub/cub.cuh>
+
+#include "vs_common.cuh"
+#include "vs_kernels.cuh"
+
+namespace vs {
+
+namespace {
+constexpr int NT = 128;
+constexpr int NW = NT / 32;
+constexpr int QT = kIvfLmQT;   // pairs per unit: two per warp
+constexpr int RS = 8;          // staged rows per chunk
+constexpr int TMAX = kIvfLmDMax / 128;
+constexpr int RPOS = 16;       // row positions carried in a unit record
+static_assert(QT == 2 * NW, "two query slots per warp");
+
+// 128-byte unit record
+struct __align__(16) UnitRec {
+    int32_t list, np, nsel, first_pair;
+    uint32_t sel_off, pad0, pad1, pad2;
+    int32_t code[QT];
+    uint32_t pos[RPOS];
+};
+static_assert(sizeof(UnitRec) == 128, "one 128-byte record per unit");
+
+template <typename T>
+struct V4;
+template <>
+struct V4<float> {
+    static __device__ __forceinline__ float4 lds(const float* p) { return *reinterpret_cast<const float4*>(p); }
+};
+template <>
+struct V4<__nv_bfloat16> {
+    static __device__ __forceinline__ float4 lds(const __nv_bfloat16* p) {
+        const uint2 u = *reinterpret_cast<const uint2*>(p);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        return make_float4(a.x, a.y, b.x, b.y);
+    }
+};
+
+template <bool IP>
+__device__ __forceinline__ float term4(float acc, const float4 q, const float4 x) {
+    if (IP) {
+        acc = fmaf(q.x, x.x, acc); acc = fmaf(q.y, x.y, acc);
+        acc = fmaf(q.z, x.z, acc); acc = fmaf(q.w, x.w, acc);
+    } else {
+        float t;
+        t = q.x - x.x; acc = fmaf(t, t, acc);
+        t = q.y - x.y; acc = fmaf(t, t, acc);
+        t = q.z - x.z; acc = fmaf(t, t, acc);
+        t = q.w - x.w; acc = fmaf(t, t, acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int o = 16 >> s;
+        const int n = 16 >> s;
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (i < n / 2) {
+                const float send = upper ? v[i] : v[i + n / 2];
+                const float keep = upper ? v[i + n / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(VS_FULL, send, o);
+            }
+        }
+    }
+    return v[0] + __shfl_xor_sync(VS_FULL, v[0], 1);
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+
+__device__ __noinline__ int compact_slow_sel(float* keys, uint32_t* pos, int n, int k, float margin, int limit,
+                                             float* thr, int* overflow) {
+    return warp_compact(keys, pos, n, k, margin, limit, thr, overflow);
+}
+
+// selected payload positions of every list, ascending, at sel_off[l]
+__global__ void k_list_sel_positions(const int64_t* __restrict__ list_off, int nlist,
+                                     const uint32_t* __restrict__ pbits, const int64_t* __restrict__ sel_off,
+                                     uint32_t* __restrict__ spos) {
+    const int lane = threadIdx.x & 31;
+    for (int l = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < nlist; l += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = list_off[l], b = list_off[l + 1];
+        int64_t out = sel_off[l];
+        for (int64_t r0 = a; r0 < b; r0 += 32 * 32) {
+            const int64_t r = r0 + lane * 32;
+            uint32_t bits = 0u;
+            if (r < b) {
+                const int sh = (int)(r & 31);
+                const uint32_t lo = pbits[r >> 5];
+                const uint32_t hi = sh ? pbits[(r >> 5) + 1] : 0u;
+                bits = __funnelshift_r(lo, hi, sh);
+                const int64_t nb = b - r;
+                if (nb < 32) bits &= (1u << nb) - 1u;
+            }
+            const int c = __popc(bits);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(VS_FULL, incl, o);
+                if (lane >= o) incl += t;
+            }
+            int64_t w = out + incl - c;
+            while (bits) {
+                const int bb = __ffs(bits) - 1;
+                bits &= bits - 1;
+                spos[w++] = (uint32_t)(r + bb);
+            }
+            out += __shfl_sync(VS_FULL, incl, 31);
+        }
+    }
+}
+
+__global__ void k_make_recs(const int4* __restrict__ units, const int32_t* __restrict__ n_units, int64_t max_units,
+                            const int32_t* __restrict__ pair_codes, const int32_t* __restrict__ lsel,
+                            const int64_t* __restrict__ sel_off, const uint32_t* __restrict__ spos,
+                            UnitRec* __restrict__ recs) {
+    const int nu = *n_units;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < max_units && u < nu;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int4 un = units[u];
+        UnitRec r;
+        r.list = un.x;
+        r.np = un.z;
+        r.first_pair = un.y;
+        r.nsel = lsel[un.x];
+        r.sel_off = (uint32_t)sel_off[un.x];
+        r.pad0 = r.pad1 = r.pad2 = 0u;
+#pragma unroll
+        for (int s = 0; s < QT; ++s) r.code[s] = s < un.z ? pair_codes[un.y + s] : 0;
+#pragma unroll
+        for (int i = 0; i < RPOS; ++i) r.pos[i] = i < r.nsel ? spos[r.sel_off + i] : 0u;
+        recs[u] = r;
+    }
+}
+
+struct SelSmem {
+    UnitRec rec[2];
+};
+}  // namespace
+
+struct IvfSelParams {
+    const float* Q;
+    int64_t nq;
+    int d, dp;
+    const void* payload;
+    int nprobe;
+    const UnitRec* recs;
+    const int32_t* n_units;
+    const uint32_t* spos;
+    const float* margin;
+    int ip, k;
+    CandBuf cb;
+    unsigned long long* visited;
+};
+
+template <typename T, bool IP>
+__global__ void __launch_bounds__(NT, 4) k_ivf_scan_sel(IvfSelParams p) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SelSmem& S = *reinterpret_cast<SelSmem*>(smraw);
+    T* xs = reinterpret_cast<T*>(smraw + ((sizeof(SelSmem) + 127) & ~size_t(127)));   // [RS][dp]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = p.d, dp = p.dp, nt = dp / 128;
+    const T* payload = reinterpret_cast<const T*>(p.payload);
+    const int C = p.cb.C;
+    const int n_units = *p.n_units;
+    const int row_bytes = d * (int)sizeof(T);
+    const bool v16 = (row_bytes & 15) == 0;
+    const int piece = v16 ? 16 : 8;
+    const int pieces = row_bytes / piece;
+    unsigned long long visited = 0;
+    for (int i = tid; i < RS * dp; i += NT) xs[i] = T(0.f);   // zero tail [d, dp) of every staged row
+    int u = blockIdx.x;
+    if (u < n_units && tid < 32) reinterpret_cast<uint32_t*>(&S.rec[0])[tid] = reinterpret_cast<const uint32_t*>(p.recs + u)[tid];
+    __syncthreads();
+    int cur = 0;
+    for (; u < n_units; u += gridDim.x, cur ^= 1) {
+        const UnitRec& R = S.rec[cur];
+        const int np = R.np, nsel = R.nsel;
+        const int64_t l_unused = R.list;
+        (void)l_unused;
+        // rows of the first chunk (positions in the record) ...
+        const int nr0 = min(RS, nsel);
+        for (int i = tid; i < nr0 * pieces; i += NT) {
+            const int r = i / pieces, pc = i - r * pieces;
+            const char* src = reinterpret_cast<const char*>(payload + (int64_t)R.pos[r] * d) + pc * piece;
+            char* dst = reinterpret_cast<char*>(xs + r * dp) + pc * piece;
+            if (v16) cp_async16(dst, src);
+            else cp_async8(dst, src);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        // ... and this warp's two queries, in the same round trip
+        int qidx[2], sub[2], cnt[2] = {0, 0}, ovf[2] = {0, 0};
+        float tau[2];
+        bool live[2];
+        float4 qv[2][TMAX];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int slot = warp + h * NW;
+            live[h] = slot < np;
+            const int code = live[h] ? R.code[slot] : 0;
+            qidx[h] = code / p.nprobe;
+            sub[h] = code % p.nprobe;
+            tau[h] = __int_as_float(0x7f800000);
+            const float* qg = p.Q + (int64_t)qidx[h] * d;
+#pragma unroll
+            for (int t = 0; t < TMAX; ++t) {
+                const int e = lane * 4 + 128 * t;
+                qv[h][t] = (live[h] && e < d) ? __ldg(reinterpret_cast<const float4*>(qg + e))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        // the next unit's record, consumed after this unit
+        const int un = u + gridDim.x;
+        uint32_t nrec = 0u;
+        if (warp == 0 && un < n_units) nrec = reinterpret_cast<const uint32_t*>(p.recs + un)[lane];
+        if (tid == 0) visited += (unsigned long long)nsel * np;
+        for (int c0 = 0; c0 < nsel; c0 += RS) {
+            const int nr = min(RS, nsel - c0);
+            if (c0 > 0) {
+                // later chunks (lists with more than RS selected rows)
+                __syncthreads();   // the previous chunk's rows are consumed
+                for (int i = tid; i < nr * pieces; i += NT) {
+                    const int r = i / pieces, pc = i - r * pieces;
+                    const int rr = c0 + r;
+                    const uint32_t pos = rr < RPOS ? R.pos[rr] : p.spos[R.sel_off + rr];
+                    const char* src = reinterpret_cast<const char*>(payload + (int64_t)pos * d) + pc * piece;
+                    char* dst = reinterpret_cast<char*>(xs + r * dp) + pc * piece;
+                    if (v16) cp_async16(dst, src);
+                    else cp_async8(dst, src);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            if (live[0]) {
+                float acc[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+#pragma unroll
+                for (int r = 0; r < RS; ++r) {
+                    if (r < nr) {
+                        const T* xr = xs + r * dp + lane * 4;
+#pragma unroll
+                        for (int t = 0; t < TMAX; ++t) {
+                            if (t < nt) {
+                                const float4 x = V4<T>::lds(xr + 128 * t);
+                                acc[r] = term4<IP>(acc[r], qv[0][t], x);
+                                acc[RS + r] = term4<IP>(acc[RS + r], qv[1][t], x);
+                            }
+                        }
+                    }
+                }
+                const float tot = transpose_reduce16(acc, lane);   // (lane >> 1) = h * RS + r
+                const float key = IP ? -tot : tot;
+                const int myh = (lane >> 1) / RS, myr = (lane >> 1) % RS;
+                const int rr = c0 + myr;
+                const uint32_t mypos = (myr < nr) ? (rr < RPOS ? R.pos[rr] : p.spos[R.sel_off + rr]) : 0u;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!live[h]) continue;
+                    const int q = qidx[h];
+                    const int64_t cbase = ((int64_t)q * p.cb.n_sub + sub[h]) * C;
+                    float* ckey = p.cb.key + cbase;
+                    uint32_t* cpos = p.cb.pos + cbase;
+                    bool adm = (lane & 1) == 0 && myh == h && myr < nr && key <= tau[h];
+                    unsigned b = __ballot_sync(VS_FULL, adm);
+                    if (b && cnt[h] + __popc(b) > C) {
+                        float nthr;
+                        int lov = 0;
+                        cnt[h] = compact_slow_sel(ckey, cpos, cnt[h], p.k, p.margin[q], C - 32, &nthr, &lov);
+                        tau[h] = nthr;
+                        ovf[h] |= lov;
+                        adm = adm && key <= tau[h];
+                        b = __ballot_sync(VS_FULL, adm);
+                    }
+                    if (adm) {
+                        const int slot = cnt[h] + __popc(b & lanemask_lt());
+                        ckey[slot] = key;
+                        cpos[slot] = mypos;
+                    }
+                    cnt[h] += __popc(b);
+                }
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!live[h]) continue;
+                p.cb.cnt[(int64_t)qidx[h] * p.cb.n_sub + sub[h]] = cnt[h];
+                if (ovf[h]) p.cb.overflow[qidx[h]] = 1;
+            }
+        }
+        if (warp == 0) reinterpret_cast<uint32_t*>(&S.rec[cur ^ 1])[lane] = nrec;
+        __syncthreads();   // next record visible; staged rows free
+    }
+    if (tid == 0 && visited) atomicAdd(p.visited, visited);
+}
+
+// setup (per search) + the scan; counts / sel_off / spos / recs are scratch
+// sized by the caller (ivf_sel_scratch)
+size_t ivf_sel_temp_bytes(int nlist) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, nlist + 1);
+    return b + 256;
+}
+
+__global__ void k_widen_counts(const int32_t* __restrict__ c, int n, int64_t* __restrict__ w) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) w[i] = i < n ? c[i] : 0;
+}
+
+template <typename T>
+cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
+    if (a.nq == 0) return cudaSuccess;
+    cudaError_t e;
+    // per-list selected counts -> offsets -> positions
+    const int lb = std::max(1, std::min((a.nlist * 32 + 255) / 256, 4096));
+    k_list_selected<<<lb, 256, 0, s>>>(a.list_off, a.nlist, a.pbits, a.lsel);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_widen_counts<<<(a.nlist + 256) / 256, 256, 0, s>>>(a.lsel, a.nlist, a.lsel64);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    size_t tb = a.tmp_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(a.tmp, tb, a.lsel64, a.sel_off, a.nlist + 1, s)) != cudaSuccess) return e;
+    k_list_sel_positions<<<lb, 256, 0, s>>>(a.list_off, a.nlist, a.pbits, a.sel_off, a.spos);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    UnitRec* recs = reinterpret_cast<UnitRec*>(a.recs);
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>((a.max_units + 255) / 256, 8192));
+    k_make_recs<<<rb, 256, 0, s>>>(a.units, a.n_units, a.max_units, a.pair_codes, a.lsel, a.sel_off, a.spos, recs);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    IvfSelParams p;
+    p.Q = a.Q;
+    p.nq = a.nq;
+    p.d = a.d;
+    p.dp = (a.d + 127) / 128 * 128;
+    p.payload = a.payload;
+    p.nprobe = a.nprobe;
+    p.recs = recs;
+    p.n_units = a.n_units;
+    p.spos = a.spos;
+    p.margin = a.margin;
+    p.ip = a.ip;
+    p.k = a.k;
+    p.cb = a.cb;
+    p.visited = a.visited;
+    const size_t smem = ((sizeof(SelSmem) + 127) & ~size_t(127)) + (size_t)RS * p.dp * sizeof(T);
+    auto kern = a.ip ? k_ivf_scan_sel<T, true> : k_ivf_scan_sel<T, false>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return e;
+    int per_sm = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem)) != cudaSuccess) return e;
+    const int64_t grid = std::min<int64_t>((int64_t)a.sm_count * std::max(per_sm, 1), a.max_units);
+    kern<<<(unsigned)std::max<int64_t>(grid, 1), NT, smem, s>>>(p);
+    return cudaGetLastError();
+}
+template cudaError_t launch_ivf_scan_sel<float>(const IvfSelLaunch&, cudaStream_t);
+template cudaError_t launch_ivf_scan_sel<__nv_bfloat16>(const IvfSelLaunch&, cudaStream_t);
+
+}  // namespace vs

@@ -148,6 +148,41 @@ size_t ivf_lmajor_smem(int dp, int dtype_bytes);
 template <typename T>
 cudaError_t launch_ivf_scan_lmajor(const IvfLmParams& p, int sm_count, cudaStream_t s);
 
+// ---- phase A: filtered IVF list scan over pre-selected rows (vs_ivf_sel.cu) --------------
+struct IvfSelLaunch {
+    const float* Q;
+    int64_t nq;
+    int d;
+    const void* payload;
+    const int64_t* list_off;
+    int nlist;
+    const uint32_t* pbits;      // permuted filter bitmap (required)
+    int nprobe;
+    const int32_t* pair_codes;  // from launch_ivf_group (unit_pairs = kIvfLmQT)
+    const int4* units;
+    const int32_t* n_units;
+    int64_t max_units;
+    const float* margin;
+    int ip, k;
+    CandBuf cb;                 // n_sub = nprobe
+    unsigned long long* visited;
+    // scratch: lsel [nlist], lsel64 / sel_off [nlist + 1], spos [n_total], recs [max_units] x 128 B
+    int32_t* lsel;
+    int64_t* lsel64;
+    int64_t* sel_off;
+    uint32_t* spos;
+    void* recs;
+    void* tmp;
+    size_t tmp_bytes;           // >= ivf_sel_temp_bytes(nlist)
+    int sm_count;
+};
+constexpr size_t kIvfSelRecBytes = 128;
+size_t ivf_sel_temp_bytes(int nlist);
+template <typename T>
+cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s);
+__global__ void k_list_selected(const int64_t* __restrict__ list_off, int nlist, const uint32_t* __restrict__ pbits,
+                                int32_t* __restrict__ sel);
+
 // ---- phase B: exact float64 re-rank + tie-rule top-k ------------------------------------
 // numpy's pairwise-summation plan for one row length d (<= 2048): leaves left
 // to right, internal nodes in post-order (slot nleaf + j = slot a_j + slot b_j),

@@ -58,7 +58,6 @@ class DeviceGroup:
         self.members = [N.Context.borrowed(N.load().vs_group_ctx(h, i), d, owner=self)
                         for i, d in enumerate(self.devices)]
         self._cols = weakref.WeakKeyDictionary()   # column -> (shard DeviceColumns, row_lo)
-        self._ivfs = weakref.WeakKeyDictionary()   # IvfIndex -> member index parts
 
     def __len__(self):
         return len(self.devices)
@@ -133,7 +132,8 @@ class DeviceGroup:
     # ---- IVF over list shards -------------------------------------------------------------------
     def shard_ivf(self, index):
         """Per-member index parts: same centroids, the LPT-owned lists' rows."""
-        hit = self._ivfs.get(index)
+        key = ("group", id(self))            # cached on the index (its _dev dict)
+        hit = index._dev.get(key)
         if hit is not None:
             return hit
         from .distributed import lpt_assign
@@ -158,7 +158,7 @@ class DeviceGroup:
                                            N.ptr(pay), N.DTYPE_F32, N.METRIC_CODE[index.metric], None, None,
                                            C.byref(h)), "ivf_create")
             parts.append(N.DeviceIvf(m, h))
-        self._ivfs[index] = parts
+        index._dev[key] = parts
         return parts
 
     def ivf_search_raw(self, index, queries, k: int, nprobe: int, row_filter=None):
