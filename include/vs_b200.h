@@ -130,6 +130,10 @@ int vs_column_wrap(vs_ctx* ctx, void* dev_ptr, int64_t n, int32_t d,
 int vs_column_wrap_host(vs_ctx* ctx, void* host_ptr, int64_t n, int32_t d,
                         int32_t dtype, vs_column** out);
 int vs_column_free(vs_column* col);
+/* the rows of a borrowed column (vs_column_wrap / _wrap_host) changed: drop
+ * the cached row norms and max norm (recomputed by the next search; stale
+ * norms would make the approximate keys and margins wrong) */
+int vs_column_invalidate(vs_column* col);
 int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype);
 
 /* ---- exhaustive search (enn_search, vecindex.py:109-132) -----------------

@@ -50,6 +50,7 @@ SIGNATURES = {
     "vs_column_wrap": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
     "vs_column_wrap_host": (C.c_int, [_vp, _vp, _i64, _i32, _i32, C.POINTER(_vp)]),
     "vs_column_free": (C.c_int, [_vp]),
+    "vs_column_invalidate": (C.c_int, [_vp]),
     "vs_column_info": (C.c_int, [_vp, _vp, _vp, _vp]),
     "vs_enn_search": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _i64, _i32, _i32, _i64,
                                 _vp, _vp, _vp, C.POINTER(_i64)]),
@@ -266,6 +267,16 @@ class DeviceColumn:
         self.ctx = ctx
         self.n, self.d, self.dtype = int(n), int(d), int(dtype)
         self._keepalive = keepalive if borrow else None
+        self._version = getattr(keepalive, "_version", None)
+
+    def refresh(self) -> None:
+        """A borrowed torch tensor modified in place since the last search
+        (torch bumps `_version`) gets its cached row norms invalidated."""
+        t = self._keepalive
+        v = getattr(t, "_version", None)
+        if v is not None and v != self._version:
+            check(load().vs_column_invalidate(self.handle), "column_invalidate")
+            self._version = v
 
     def __del__(self):
         try:

@@ -79,9 +79,10 @@ int flush_out(vs_ctx* ctx, std::vector<OutBuf>& pending) {
     return VS_OK;
 }
 
-int ensure_norms(vs_column* col) {
+// row norms of a column, computed on the CALLING context's stream (a column may
+// be searched through contexts other than the one that created it)
+int ensure_norms(vs_column* col, vs_ctx* ctx) {
     if (col->norms_ready) return VS_OK;
-    vs_ctx* ctx = col->ctx;
     if (!col->norms) {
         CK(cudaMalloc(&col->norms, std::max<int64_t>(col->n, 1) * sizeof(float)));
         CK(cudaMalloc(&col->max_norm_bits, sizeof(unsigned)));
@@ -231,8 +232,12 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
             const int n_sub = (int)(n_split * 2);
             int64_t C = pow2ceil(std::max<int64_t>(2 * job.k, job.k + 32)) << (ctx->opt_slack + cshift);
             const int64_t rows_per_sub = (rps + 1) / 2;
-            exhaustive = C >= pow2ceil(rows_per_sub + 64);
-            if (exhaustive) C = pow2ceil(rows_per_sub + 64);
+            // buffers that hold every row they see cannot overflow: used whenever
+            // they fit in 256 MiB (small batches, e.g. the coarse quantizer of a
+            // few queries, whose centroid keys crowd inside the margin band)
+            const int64_t cap = pow2ceil(rows_per_sub + 64);
+            exhaustive = C >= cap || (int64_t)job.nq * n_sub * cap * 8 <= (int64_t(256) << 20);
+            if (exhaustive) C = cap;
             vs::CandBuf cb;
             cb.n_sub = n_sub;
             cb.C = (int)C;
@@ -676,6 +681,12 @@ int vs_column_free(vs_column* col) {
     return VS_OK;
 }
 
+int vs_column_invalidate(vs_column* col) {
+    if (!col) return set_err(VS_ERR_PARAMETER, "null column");
+    col->norms_ready = false;   // recomputed (on the caller's stream) by the next search
+    return VS_OK;
+}
+
 int vs_column_info(const vs_column* col, int64_t* n, int32_t* d, int32_t* dtype) {
     if (!col) return set_err(VS_ERR_PARAMETER, "null column");
     if (n) *n = col->n;
@@ -917,7 +928,7 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     }
     if (out_visited) *out_visited = nq * nsel;
     if (nq == 0) return VS_OK;
-    CKS(ensure_norms(col));
+    CKS(ensure_norms(col, ctx));
     float* margin = nullptr;
     CKS(arena_alloc(ctx, (size_t)nq, &margin));
     if (!q_ready) {
@@ -1051,7 +1062,7 @@ int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries
         pe.active = true;
         return VS_OK;
     }
-    CKS(ensure_norms(col));
+    CKS(ensure_norms(col, ctx));
     job.xnorm = col->norms;
     job.xmax = col->max_norm_bits;
     float* margin = nullptr;
@@ -1770,6 +1781,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
             a.list_off = v->list_off;
             a.nlist = v->nlist;
             a.pbits = job.pbits;
+            a.pnorm = v->pnorms;
             a.nprobe = job.nprobe;
             a.pair_codes = gr.pair_codes;
             a.units = gr.units;
@@ -2061,7 +2073,7 @@ extern "C" int vs_ivf_assign(vs_ctx* ctx, const vs_ivf* ivf, const vs_column* da
     DevGuard g(ctx->device);
     CK(ctx->arena.reset());
     if (data->n == 0) return VS_OK;
-    CKS(ensure_norms(const_cast<vs_column*>(data)));
+    CKS(ensure_norms(const_cast<vs_column*>(data), ctx));
     return vs::ivf_assign_gpu(ctx, ivf, data, out_lists);
 }
 
@@ -2073,7 +2085,7 @@ extern "C" int vs_ivf_build(vs_ctx* ctx, const vs_column* data, int32_t nlist, c
         return set_err(VS_ERR_PARAMETER, "nlist must be in [1, %lld], got %d", (long long)data->n, nlist);
     DevGuard g(ctx->device);
     CK(ctx->arena.reset());
-    CKS(ensure_norms(const_cast<vs_column*>(data)));
+    CKS(ensure_norms(const_cast<vs_column*>(data), ctx));
     return vs::ivf_build_gpu(ctx, data, nlist, init_rows, seed, metric, max_iters, out);
 }
 

@@ -16,10 +16,11 @@
 //      at the top of a unit the row positions and the queries are known: the
 //      selected rows (cp.async, 16 bytes, coalesced) and the unit's queries
 //      (into registers) are requested together and arrive in one round trip;
-//   3. scoring and candidate appends are those of the list-major kernel: two
+//   3. scoring and candidate appends follow the list-major kernel: two
 //      queries per warp held in registers, staged rows from shared memory,
-//      fp32 direct form (error bound eps_simt), one butterfly transpose-
-//      reduction per chunk, per-pair candidate buffers.
+//      fp32 (error bound eps_simt), one butterfly transpose-
+//      reduction per chunk, per-pair candidate buffers; the
+//      key is the dot form ||x||^2 - 2 q.x (one FFMA per element and query).
 // Reference: IvfIndex.search, vecindex.py:230-258, with the filtered
 // extension rows = rows[mask[rows]].
 #include <cub/cub.cuh>
@@ -62,21 +63,6 @@ struct V4<__nv_bfloat16> {
         return make_float4(a.x, a.y, b.x, b.y);
     }
 };
-
-template <bool IP>
-__device__ __forceinline__ float term4(float acc, const float4 q, const float4 x) {
-    if (IP) {
-        acc = fmaf(q.x, x.x, acc); acc = fmaf(q.y, x.y, acc);
-        acc = fmaf(q.z, x.z, acc); acc = fmaf(q.w, x.w, acc);
-    } else {
-        float t;
-        t = q.x - x.x; acc = fmaf(t, t, acc);
-        t = q.y - x.y; acc = fmaf(t, t, acc);
-        t = q.z - x.z; acc = fmaf(t, t, acc);
-        t = q.w - x.w; acc = fmaf(t, t, acc);
-    }
-    return acc;
-}
 
 __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 #pragma unroll
@@ -186,6 +172,7 @@ struct IvfSelParams {
     const UnitRec* recs;
     const int32_t* n_units;
     const uint32_t* spos;
+    const float* pnorm;
     const float* margin;
     int ip, k;
     CandBuf cb;
@@ -272,28 +259,36 @@ __global__ void __launch_bounds__(NT, 4) k_ivf_scan_sel(IvfSelParams p) {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncthreads();
             if (live[0]) {
+                // dot form (one FFMA per element and query): every t step updates
+                // 2 x RS independent accumulators; rows past nr hold stale data
+                // and are scored but never appended
                 float acc[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) acc[i] = 0.f;
 #pragma unroll
-                for (int r = 0; r < RS; ++r) {
-                    if (r < nr) {
-                        const T* xr = xs + r * dp + lane * 4;
+                for (int t = 0; t < TMAX; ++t) {
+                    if (t < nt) {
 #pragma unroll
-                        for (int t = 0; t < TMAX; ++t) {
-                            if (t < nt) {
-                                const float4 x = V4<T>::lds(xr + 128 * t);
-                                acc[r] = term4<IP>(acc[r], qv[0][t], x);
-                                acc[RS + r] = term4<IP>(acc[RS + r], qv[1][t], x);
-                            }
+                        for (int r = 0; r < RS; ++r) {
+                            const float4 x = V4<T>::lds(xs + r * dp + lane * 4 + 128 * t);
+                            acc[r] = fmaf(qv[0][t].x, x.x, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].x, x.x, acc[RS + r]);
+                            acc[r] = fmaf(qv[0][t].y, x.y, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].y, x.y, acc[RS + r]);
+                            acc[r] = fmaf(qv[0][t].z, x.z, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].z, x.z, acc[RS + r]);
+                            acc[r] = fmaf(qv[0][t].w, x.w, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].w, x.w, acc[RS + r]);
                         }
                     }
                 }
-                const float tot = transpose_reduce16(acc, lane);   // (lane >> 1) = h * RS + r
-                const float key = IP ? -tot : tot;
+                const float dot = transpose_reduce16(acc, lane);   // (lane >> 1) = h * RS + r
                 const int myh = (lane >> 1) / RS, myr = (lane >> 1) % RS;
                 const int rr = c0 + myr;
                 const uint32_t mypos = (myr < nr) ? (rr < RPOS ? R.pos[rr] : p.spos[R.sel_off + rr]) : 0u;
+                // key: -q.x, or ||x||^2 - 2 q.x (the query's ||q||^2 is common to
+                // all its keys; the margin eps_simt covers this form too)
+                const float key = IP ? -dot : fmaf(-2.f, dot, myr < nr ? p.pnorm[mypos] : 0.f);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if (!live[h]) continue;
@@ -375,6 +370,7 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
     p.recs = recs;
     p.n_units = a.n_units;
     p.spos = a.spos;
+    p.pnorm = a.pnorm;
     p.margin = a.margin;
     p.ip = a.ip;
     p.k = a.k;

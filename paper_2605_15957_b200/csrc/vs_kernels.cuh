@@ -157,6 +157,7 @@ struct IvfSelLaunch {
     const int64_t* list_off;
     int nlist;
     const uint32_t* pbits;      // permuted filter bitmap (required)
+    const float* pnorm;         // ||x||^2 per payload row
     int nprobe;
     const int32_t* pair_codes;  // from launch_ivf_group (unit_pairs = kIvfLmQT)
     const int4* units;

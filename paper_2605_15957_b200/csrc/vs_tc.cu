@@ -921,8 +921,17 @@ __global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict_
 // margin = 2 x E, with E the rigorous error of the approximate key:
 //   L2: key = fl(||x||^2_fp32 - 2 acc)   E = 2 E_dot + E_norm + E_round
 //   IP: key = -acc                        E = E_dot
-//   E_dot = ||q~|| Dx + ||dq|| X~ + ||dq|| Dx + 2^-14 ||q~|| X~   (last term:
-//           tensor-core fp32 accumulation, generously bounded)
+//   E_dot = ||q~|| Dx + ||dq|| X~ + ||dq|| Dx + E_acc
+//   E_acc = max(2^-14, (ceil(d/16) + 4) 2^-20) ||q~|| X~: the tensor core's fp32
+//           accumulation, whose rounding NVIDIA does not document. bf16 x bf16
+//           products are exact in fp32; each of the ceil(d/16) K=16 MMA steps
+//           adds one accumulator rounding, and the 16-term sum inside one step
+//           at most log2(16) = 4 more. Any order of summation then errs by at
+//           most (steps) x (per-rounding error) x sum|q~_i x~_i| <= ... x
+//           ||q~|| X~ (Cauchy-Schwarz). 2^-20 per rounding allows a 20-bit
+//           accumulator (16x round-to-nearest fp32's 2^-24, 8x truncation's
+//           2^-23); for d <= 1024 the 2^-14 floor dominates.
+//           tests/test_gpu_tc.py::test_adversarial_cancellation exercises it.
 //   E_norm = (d + 2) 2^-24 X^2,  E_round = 2^-23 (X^2 + 2 ||q~|| X~)
 __global__ void k_tc_margins(const float2* __restrict__ qerr, int64_t nq, int d, const unsigned* __restrict__ xmax,
                              const unsigned* __restrict__ xmax2, int ip, float* __restrict__ margin) {
@@ -932,7 +941,8 @@ __global__ void k_tc_margins(const float2* __restrict__ qerr, int64_t nq, int d,
     const float Xt = sqrtf(__uint_as_float(xmax2[0])) * 1.0001f;   // max ||x~||
     const float Dx = sqrtf(__uint_as_float(xmax2[1])) * 1.0001f;   // max ||dx||
     const float X2 = __uint_as_float(*xmax) * 1.0002f;             // max ||x||^2 (fp32)
-    const float edot = qe.x * Dx + qe.y * Xt + qe.y * Dx + 6.103515625e-05f * qe.x * Xt;
+    const float acc_u = fmaxf(6.103515625e-05f, (float)((d + 15) / 16 + 4) * 9.5367431640625e-07f);
+    const float edot = qe.x * Dx + qe.y * Xt + qe.y * Dx + acc_u * qe.x * Xt;
     float e;
     if (ip) {
         e = edot;

@@ -136,6 +136,14 @@ class EmbeddingColumn:
         obj._host_stream = t
         return obj
 
+    def invalidate(self) -> None:
+        """The borrowed rows (from_device / host_resident) were changed in place
+        by means torch cannot see (e.g. raw pointers): drop the device-side
+        cached row norms so the next search recomputes them."""
+        from . import _native as N
+        for dc in self._device.values():
+            N.check(N.load().vs_column_invalidate(dc.handle), "column_invalidate")
+
     @property
     def values(self) -> np.ndarray:
         if self._values is None and self._host_stream is not None:

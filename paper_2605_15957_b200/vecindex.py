@@ -148,9 +148,13 @@ def _dims(col):
 
 
 def device_column(col, ctx: N.Context) -> N.DeviceColumn:
-    """The (cached) device copy of an embedding column."""
+    """The (cached) device copy of an embedding column. A borrowed device (or
+    pinned host) tensor that was modified in place since its last use gets its
+    cached norms dropped (EmbeddingColumn.invalidate() does it explicitly)."""
     if isinstance(col, EmbeddingColumn):
         dc = col._device.get(ctx.device)
+        if dc is not None:
+            dc.refresh()
         if dc is None:
             if col._host_stream is not None:
                 t = col._host_stream

@@ -212,3 +212,29 @@ def test_exact_scores_across_dims(dim):
     for metric in ("squared_l2", "inner_product"):
         nt = vs.enn_search(q, data, vs.SearchParams(k=25), metric=metric)
         assert_same(nt, O.enn_search(q, data, 25, metric))
+
+
+def test_borrowed_column_mutation_invalidates_norms():
+    """A from_device column modified in place between searches: the cached row
+    norms must not survive (torch's version counter, or invalidate())."""
+    import torch
+    rng = np.random.default_rng(12)
+    data = rng.standard_normal((20000, 64)).astype(np.float32)
+    t = torch.from_numpy(data).cuda()
+    col = vs.EmbeddingColumn.from_device(t)
+    q = rng.standard_normal((300, 64)).astype(np.float32)
+    vs.enn_search(q, col, vs.SearchParams(k=10))                 # norms cached
+    t[::3] *= 3.0                                                # in place: _version bumps
+    got = vs.enn_search(q, col, vs.SearchParams(k=10))
+    ref = O.enn_search(q, t.cpu().numpy(), 10)
+    assert np.array_equal(got.data_row, ref.data_row)
+    assert np.array_equal(got.distance, ref.distance)
+    # a write torch's version counter does not see: through a second view
+    # object's storage (untracked), then the explicit invalidate()
+    alias = torch.empty(0, device=t.device).set_(t.untyped_storage(), 0, t.shape, t.stride())
+    alias[:500] = 0.0
+    col.invalidate()
+    got = vs.enn_search(q, col, vs.SearchParams(k=10))
+    ref = O.enn_search(q, t.cpu().numpy(), 10)
+    assert np.array_equal(got.data_row, ref.data_row)
+    assert np.array_equal(got.distance, ref.distance)

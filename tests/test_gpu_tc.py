@@ -115,3 +115,27 @@ def test_large_host_query_batch_async_upload(kernel, pinned, force_retry):
     ref = O.enn_filtered(q[idx], data, mask, k)
     assert np.array_equal(nt.data_row.reshape(nq, k)[idx].reshape(-1), ref.data_row)
     assert np.array_equal(nt.distance.reshape(nq, k)[idx].reshape(-1), ref.distance)
+
+
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+def test_adversarial_cancellation(tc_kernel, metric):
+    """Rows whose dot products with the query cancel massively inside the fp32
+    accumulation (a +8 half and a -8 half: partial sums reach 8 d/2 before
+    falling back to ~0) and differ only by small perturbations that are added
+    while the accumulator is large. The tensor-core keys then carry their
+    largest accumulation error; the margin (E_acc, vs_tc.cu k_tc_margins)
+    must still keep every true neighbour, so ids and distances equal the
+    oracle's."""
+    rng = np.random.default_rng(99)
+    d, n = 2048, 3000
+    base = np.concatenate([np.full(d // 2, 8.0), np.full(d // 2, -8.0)]).astype(np.float32)
+    data = np.tile(base, (n, 1))
+    cols = rng.integers(0, d // 2, (n, 6))
+    vals = (rng.integers(-64, 65, (n, 6)) * 2.0 ** -10).astype(np.float32)    # bf16-exact
+    np.put_along_axis(data, cols, np.take_along_axis(data, cols, 1) + vals, 1)
+    data[::7] = rng.standard_normal((len(data[::7]), d)).astype(np.float32)   # ordinary rows too
+    q = np.concatenate([np.ones((4, d)), rng.standard_normal((4, d))]).astype(np.float32)
+    q[:4, : d // 2] += (rng.integers(-4, 5, (4, d // 2)) * 2.0 ** -8)
+    nt = vs.enn_search(q, data, vs.SearchParams(k=25), metric=metric)
+    assert tc_kernel.stats()[N.STAT_LAST_ENN_KERNEL] == 2
+    assert_same(nt, O.enn_search(q, data, 25, metric))
