@@ -431,6 +431,40 @@ class ExactWorkload:
         n_sel = self.n_sel_total if self.sharded else self.n_sel
         assert int(cc.min()) == min(self.k, n_sel), "short result rows"
         assert bool((dd[:, 1:] >= dd[:, :-1]).all()), "distances not sorted"
+        if self.world == 1:
+            self._check_oracle()
+
+    def _check_oracle(self):
+        """Two sampled queries (first and last of the batch) bit-exact against
+        the oracle over the host copy of the selected rows (checker only,
+        outside the timed region; oracle.enn_pruned = enn_search's arithmetic)."""
+        import torch
+
+        from oracle import sqlvs_oracle as O
+        qi = np.array([0, self.nq - 1])
+        if self.cfg.get("host"):
+            mask = np.unpackbits(self.bits.cpu().numpy().view(np.uint8), bitorder="little")[:self.host_data.shape[0]]
+            rows = np.flatnonzero(mask)
+            xs = self.host_data.numpy()[rows]
+        elif self.replicas:
+            emb, mask, _ = self.host_sample
+            rows = np.flatnonzero(mask)
+            xs = emb[rows]
+        else:
+            m = torch.from_numpy(np.unpackbits(self.bits.cpu().numpy().view(np.uint8), bitorder="little")
+                                 [:self.col.count].astype(bool)).to(self.dev)
+            r = torch.nonzero(m).flatten()
+            xs = self.col._dev_tensor[r].float().cpu().numpy()
+            rows = r.cpu().numpy()
+        q = self.queries[torch.from_numpy(qi).to(self.dev)].cpu().numpy()
+        ref = O.enn_pruned(q, xs, self.k, "squared_l2", row_ids=rows + self.lo)
+        ids, dd, cc = (t.cpu().numpy() for t in self.out_dev)
+        for j, i in enumerate(qi):
+            want_i, want_d = ref.per_query(j)
+            c = int(cc[i])
+            if not (np.array_equal(ids[i, :c], want_i) and np.array_equal(dd[i, :c], want_d)):
+                raise SystemExit(f"PARITY FAILURE: query {i} differs from the oracle")
+        log(f"check: queries {qi.tolist()} bit-exact vs the oracle")
 
     def io_bytes(self):
         h2d = self.q_host.numel() * 4 + self.bits_host.numel() * 4
@@ -444,6 +478,7 @@ class ExactWorkload:
         return "weak" if (self.replicas or self.cfg.get("host")) else "strong"
 
     def roofline(self, kt, steps, ctx, N):
+        self.kernel_name = {1: "simt_fp32", 2: "tcgen05_bf16", 3: "wide"}.get(ctx.stats()[N.STAT_LAST_ENN_KERNEL], "?")
         if self.cfg.get("host"):
             # streamed variant: the bound is the PCIe transfer of the selected rows
             byts = float(self.n_sel) * self.d * 4
@@ -459,9 +494,8 @@ class ExactWorkload:
         flops = 2.0 * self.nq * self.n_sel * self.d
         achieved = flops / (scan_ns / max(scan_n, 1) / 1e9) / 1e12 if scan_n else None
         peak = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
-        kern = {1: "simt_fp32", 2: "tcgen05_bf16"}.get(ctx.stats()[N.STAT_LAST_ENN_KERNEL], "?")
+        kern = self.kernel_name
         traffic = _traffic(f"cfg{self.cfg['id']}:{kern}")
-        self.kernel_name = kern
         return {"bound": "tensor", "kernel": f"enn_scan ({kern})",
                 "achieved": round(achieved, 2) if achieved else None, "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4) if achieved else None,
@@ -668,6 +702,22 @@ class IvfWorkload:
     def check(self):
         ids, dd, cc = self.out_dev
         assert bool(((dd[:, 1:] >= dd[:, :-1]) | dd[:, 1:].isnan()).all()), "distances not sorted"
+        if self.world > 1:
+            return
+        # two sampled queries (their probed lists were gathered at setup) bit-exact
+        # against the oracle's IVF search (checker only, outside the timed region)
+        from oracle import sqlvs_oracle as O
+        qi = [0, len(self.cpu_q) - 1]
+        res = O.ivf_search(self.cpu_q[qi], self.index.centroids, self.index.partitions, lambda c: self.cpu_lists[c],
+                           self.nprobe, self.k, mask=self.mask_host)
+        ids, dd, cc = (t.cpu().numpy() for t in self.out_dev)
+        for j, i in enumerate(qi):
+            want_i, want_d = res.per_query(j)
+            c = int(cc[i])
+            if not (np.array_equal(res.probes[j], self.cpu_probes[i]) and np.array_equal(ids[i, :c], want_i)
+                    and np.array_equal(dd[i, :c], want_d)):
+                raise SystemExit(f"PARITY FAILURE: query {i} differs from the oracle")
+        log(f"check: queries {qi} (probes, ids, distances) bit-exact vs the oracle")
 
     def io_bytes(self):
         h2d = self.q_host.numel() * 4 + (self.bits_host.numel() * 4 if self.bits_host is not None else 0)
