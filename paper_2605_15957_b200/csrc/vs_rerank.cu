@@ -68,55 +68,25 @@ struct Small : LeafPlan {
 };
 
 // k-th smallest (1 <= k <= count) orderable key among the keys `foreach`
-// visits: a range-adaptive radix select. The first pass bins the keys' actual
-// range [lo, hi] into <= HBINS bins (not the top 11 bits of the 32-bit key,
-// which put keys of similar magnitude into one or two bins); every later pass
-// refines the selected bin the same way, so concentrated keys need 1-2 passes
-// instead of 3. Histogram increments are warp-aggregated (__match_any_sync):
-// near-tied keys do not serialise on one shared-memory address.
+// visits: a 3-pass radix select (11 + 11 + 10 bits) over a shared-memory
+// histogram, instead of a 32-step bisection over the keys.
 template <class ForEach>
 __device__ uint32_t block_radix_kth(ForEach foreach, unsigned k, unsigned* hist, Small& sm) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    uint32_t lo = 0xffffffffu, hi = 0u;
-    foreach([&](uint32_t u) {
-        lo = min(lo, u);
-        hi = max(hi, u);
-    });
-    lo = __reduce_min_sync(VS_FULL, lo);
-    hi = __reduce_max_sync(VS_FULL, hi);
-    if (lane == 0) {
-        hist[w] = lo;
-        hist[NWARP + w] = hi;
-    }
-    __syncthreads();
-    uint32_t base = hist[0], top = hist[NWARP];
-    for (int i = 1; i < NWARP; ++i) {
-        base = min(base, hist[i]);
-        top = max(top, hist[NWARP + i]);
-    }
-    uint32_t range = top - base;    // keys live in [base, base + range]
-    __syncthreads();
+    uint32_t prefix = 0u, pmask = 0u;
 #pragma unroll 1
-    while (range > 0) {
-        const int shift = max(0, 32 - __clz(range) - 11);
-        const int nb = (int)(range >> shift) + 1;   // <= HBINS
+    for (int pass = 0; pass < 3; ++pass) {
+        const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+        const int nb = pass == 2 ? 1024 : 2048;
         for (int i = tid; i < nb; i += NT) hist[i] = 0u;
         __syncthreads();
         foreach([&](uint32_t u) {
-            if (u >= base && u - base <= range) {
-                const uint32_t bin = (u - base) >> shift;
-                const unsigned am = __activemask();
-                const unsigned grp = __match_any_sync(am, bin);
-                if (lane == __ffs(grp) - 1) atomicAdd(&hist[bin], (unsigned)__popc(grp));
-            }
+            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & (uint32_t)(nb - 1)], 1u);
         });
         __syncthreads();
-        const int per = (nb + NT - 1) / NT;
+        const int per = nb / NT;
         unsigned loc = 0;
-        for (int b = 0; b < per; ++b) {
-            const int bi = tid * per + b;
-            loc += bi < nb ? hist[bi] : 0u;
-        }
+        for (int b = 0; b < per; ++b) loc += hist[tid * per + b];
         unsigned incl = loc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -130,10 +100,9 @@ __device__ uint32_t block_radix_kth(ForEach foreach, unsigned k, unsigned* hist,
         if (excl < k && k <= excl + loc) {
             unsigned c = excl;
             for (int b = 0; b < per; ++b) {
-                const int bi = tid * per + b;
-                const unsigned h = bi < nb ? hist[bi] : 0u;
+                const unsigned h = hist[tid * per + b];
                 if (c + h >= k) {
-                    sm.sel_bin = bi;
+                    sm.sel_bin = tid * per + b;
                     sm.sel_below = c;
                     break;
                 }
@@ -142,12 +111,11 @@ __device__ uint32_t block_radix_kth(ForEach foreach, unsigned k, unsigned* hist,
         }
         __syncthreads();
         k -= sm.sel_below;
-        const uint32_t off = (uint32_t)sm.sel_bin << shift;
-        base += off;
-        range = min(range - off, shift ? (1u << shift) - 1u : 0u);
+        prefix |= (uint32_t)sm.sel_bin << shift;
+        pmask |= (uint32_t)(nb - 1) << shift;
         __syncthreads();
     }
-    return base;
+    return prefix;
 }
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
@@ -698,103 +666,40 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
         }
         __syncthreads();
     }
-    // 0. live candidates -> shared memory. The buffers' counts are prefix-summed
-    //    (in `hist`, free until the select), so flat slot f maps to (buffer,
-    //    entry) by a binary search and every thread keeps several independent
-    //    key loads in flight: one round trip for the keys and one for the live
-    //    ones' positions, instead of two per buffer and warp.
+    // 0. live candidates -> shared memory (one warp per buffer, coalesced)
     if (tid == 0) sm.counter = 0;
-    if (nsub <= HBINS) {
-        unsigned* cpre = hist;   // inclusive prefix of the counts
-        {
-            const int per = (nsub + NT - 1) / NT;
-            unsigned loc = 0;
-            for (int b = 0; b < per; ++b) {
-                const int si = tid * per + b;
-                loc += si < nsub ? (unsigned)cnts[si] : 0u;
-            }
-            unsigned incl = loc;
+    __syncthreads();
+    for (int s = w; s < nsub; s += NWARP) {
+        const int cs = cnts[s];
+        const float* bk = ckey + (int64_t)s * C;
+        const uint32_t* bp = cpos + (int64_t)s * C;
+        for (int j0 = 0; j0 < cs; j0 += 128) {
+            // four independent key loads in flight, then the positions of the live ones
+            float kk[4];
+            uint32_t pp[4];
+            bool live[4];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned t = __shfl_up_sync(VS_FULL, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (lane == 31) sm.wtot[w] = incl;
-            __syncthreads();
-            unsigned run = incl - loc;
-            for (int i = 0; i < w; ++i) run += sm.wtot[i];
-            for (int b = 0; b < per; ++b) {
-                const int si = tid * per + b;
-                if (si < nsub) {
-                    run += (unsigned)cnts[si];
-                    cpre[si] = run;
-                }
-            }
-            __syncthreads();
-        }
-        const int64_t totf = tot;
-        constexpr int G = 4;
-        for (int64_t f0 = 0; f0 < totf; f0 += (int64_t)G * NT) {
-            float kk[G];
-            int64_t slot_i[G];
-            bool live[G];
-            uint32_t pp[G];
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const int64_t f = f0 + h * NT + tid;
-                slot_i[h] = -1;
-                kk[h] = 0.f;
-                if (f < totf) {
-                    int a = 0, b = nsub - 1;   // first buffer whose inclusive prefix exceeds f
-                    while (a < b) {
-                        const int m = (a + b) >> 1;
-                        if ((int64_t)cpre[m] > f) b = m;
-                        else a = m + 1;
-                    }
-                    const int64_t j = f - (a ? (int64_t)cpre[a - 1] : 0);
-                    slot_i[h] = (int64_t)a * C + j;
-                    kk[h] = ckey[slot_i[h]];
-                }
+            for (int h = 0; h < 4; ++h) {
+                const int j = j0 + 32 * h + lane;
+                kk[h] = j < cs ? bk[j] : 0.f;
             }
 #pragma unroll
-            for (int h = 0; h < G; ++h) {
-                live[h] = slot_i[h] >= 0 && f2o(kk[h]) <= pre;
-                pp[h] = live[h] ? cpos[slot_i[h]] : 0u;
+            for (int h = 0; h < 4; ++h) {
+                const int j = j0 + 32 * h + lane;
+                live[h] = j < cs && f2o(kk[h]) <= pre;
+                pp[h] = live[h] ? bp[j] : 0u;
             }
 #pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const unsigned bl = __ballot_sync(VS_FULL, live[h]);
-                if (!bl) continue;
+            for (int h = 0; h < 4; ++h) {
+                const unsigned b = __ballot_sync(VS_FULL, live[h]);
+                if (!b) continue;
                 int base = 0;
-                if (lane == 0) base = atomicAdd(&sm.counter, __popc(bl));
+                if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
                 base = __shfl_sync(VS_FULL, base, 0);
-                const int slot = base + __popc(bl & lanemask_lt());
+                const int slot = base + __popc(b & lanemask_lt());
                 if (live[h] && slot < LCAP) {
                     lkey[slot] = kk[h];
                     lpos[slot] = pp[h];
-                }
-            }
-        }
-    } else {
-        __syncthreads();
-        for (int s = w; s < nsub; s += NWARP) {
-            const int cs = cnts[s];
-            const float* bk = ckey + (int64_t)s * C;
-            const uint32_t* bp = cpos + (int64_t)s * C;
-            for (int j0 = 0; j0 < cs; j0 += 32) {
-                const int j = j0 + lane;
-                const float kv = j < cs ? bk[j] : 0.f;
-                const bool lv = j < cs && f2o(kv) <= pre;
-                const uint32_t pv = lv ? bp[j] : 0u;
-                const unsigned bl = __ballot_sync(VS_FULL, lv);
-                if (!bl) continue;
-                int base = 0;
-                if (lane == 0) base = atomicAdd(&sm.counter, __popc(bl));
-                base = __shfl_sync(VS_FULL, base, 0);
-                const int slot = base + __popc(bl & lanemask_lt());
-                if (lv && slot < LCAP) {
-                    lkey[slot] = kv;
-                    lpos[slot] = pv;
                 }
             }
         }
