@@ -61,7 +61,8 @@ enum vs_option {
     VS_OPT_FORCE_RETRY = 4,  /* test hook: treat every query as overflowed once    */
     VS_OPT_TIMING = 5,       /* 1: record CUDA events around every kernel class    */
     VS_OPT_STREAM_CHUNK = 6, /* host-resident search: selected rows per chunk (0 auto) */
-    VS_OPT_IVF_CHUNK_ROWS = 7 /* tensor-core IVF scan: rows per list chunk (0: 131072) */
+    VS_OPT_IVF_CHUNK_ROWS = 7, /* tensor-core IVF scan: rows per list chunk (0: 131072) */
+    VS_OPT_COARSE = 8        /* IVF coarse quantizer: 0 auto, 1 candidate buffers, 2 dense keys */
 };
 
 /* kernel classes reported by vs_ctx_kernel_times (CUDA-event durations on the

@@ -26,6 +26,7 @@ DTYPE_F32, DTYPE_BF16 = 0, 1
 OPT_ENN_KERNEL, OPT_IVF_KERNEL, OPT_CAND_SLACK, OPT_FORCE_RETRY, OPT_TIMING = 1, 2, 3, 4, 5
 OPT_STREAM_CHUNK = 6
 OPT_IVF_CHUNK_ROWS = 7
+OPT_COARSE = 8
 KERNEL_CLASSES = ("select", "enn_scan", "rerank", "coarse", "ivf_scan", "ivf_rerank", "merge", "stage",
                   "coarse_rerank")
 STAT_LAUNCHES, STAT_OVERFLOW_QUERIES, STAT_SURVIVORS, STAT_LAST_ENN_KERNEL = 0, 1, 2, 3

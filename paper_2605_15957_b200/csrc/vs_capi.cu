@@ -559,6 +559,7 @@ int vs_ctx_set_option(vs_ctx* ctx, int32_t key, int64_t value) {
         case VS_OPT_CAND_SLACK: ctx->opt_slack = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8)); break;
         case VS_OPT_FORCE_RETRY: ctx->opt_force_retry = (int)value; break;
         case VS_OPT_TIMING: ctx->opt_timing = (int)value; break;
+        case VS_OPT_COARSE: ctx->opt_coarse = (int)value; break;
         default: return set_err(VS_ERR_PARAMETER, "unknown option %d", key);
     }
     return VS_OK;
@@ -1939,6 +1940,71 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     return VS_OK;
 }
 
+// IVF coarse quantizer on dense keys: the tensor cores write every (query,
+// centroid) key of a query chunk (tc_dense_keys, MODE 3), one CTA per query
+// selects the margin band around its nprobe-th key (launch_dense_select) into
+// a single candidate buffer, and phase B scores that band exactly (k_rerank:
+// tie-rule top-nprobe, bit-identical probes). Replaces candidate buffers fed
+// by the GEMM epilogue, which made the coarse GEMM epilogue-bound and left
+// ~2,300 candidates per query for phase B to sort through.
+int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
+    const int64_t ncols = cj.nsel;
+    const int64_t qc = std::max<int64_t>(256, std::min<int64_t>(cj.nq, ((int64_t)1 << 28) / std::max<int64_t>(ncols, 1)));
+    float* keys = nullptr;
+    float* tm = nullptr;
+    CKS(arena_alloc(ctx, (size_t)std::min(qc, cj.nq) * ncols, &keys));
+    CKS(arena_alloc(ctx, (size_t)cj.nq, &tm));
+    const int C = (int)pow2ceil(std::max<int64_t>(4 * (int64_t)cj.k, cj.k + 256));
+    for (int64_t q0 = 0; q0 < cj.nq; q0 += qc) {
+        const int64_t n = std::min(qc, cj.nq - q0);
+        EnnJob sub = cj;
+        sub.q = cj.q + q0 * cj.d;
+        sub.nq = n;
+        if (sub.out_ids32) sub.out_ids32 += q0 * cj.k;
+        if (sub.out_ids) sub.out_ids += q0 * cj.k;
+        if (sub.out_dist) sub.out_dist += q0 * cj.k;
+        if (sub.out_count) sub.out_count += q0;
+        if (cj.narrow)
+            CKS(vs::bn128::tc_dense_keys(ctx, sub.q, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip,
+                                         keys, tm + q0));
+        else
+            CKS(vs::tc_dense_keys(ctx, sub.q, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip, keys,
+                                  tm + q0));
+        vs::CandBuf cb;
+        cb.n_sub = 1;
+        cb.C = C;
+        CKS(arena_alloc(ctx, (size_t)n * C, &cb.key));
+        CKS(arena_alloc(ctx, (size_t)n * C, &cb.pos));
+        CKS(arena_alloc(ctx, (size_t)n, &cb.cnt));
+        CKS(arena_alloc(ctx, (size_t)n, &cb.overflow));
+        CK(cudaMemsetAsync(cb.overflow, 0, n * sizeof(int), ctx->stream));
+        {
+            KTimer kt(ctx, cj.cls_rerank);
+            CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cb, ctx->stream));
+        }
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+        PhaseA st;
+        st.sp.Q = sub.q;
+        st.sp.nq = n;
+        st.sp.d = cj.d;
+        st.sp.X = cj.rows;
+        st.sp.sel = nullptr;
+        st.sp.nsel = ncols;
+        st.sp.xnorm = cj.xnorm;
+        st.sp.margin = tm + q0;
+        st.sp.ip = cj.ip;
+        st.sp.k = cj.k;
+        st.sp.cb = cb;
+        st.sp.tau_g = nullptr;
+        st.sp.verify = 0;
+        st.exhaustive = false;
+        ctx->stats[VS_STAT_LAST_ENN_KERNEL] = 2;
+        (void)simt_margin;
+        CKS(enn_phase_b(ctx, sub, st, 0, false, PhaseBHooks{}));
+    }
+    return VS_OK;
+}
+
 }  // namespace
 
 // IVF search; probes_in (nullable, [nq][nprobe]) skips the coarse quantizer
@@ -1994,7 +2060,14 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     cj.cls_scan = VS_K_COARSE;
     cj.cls_rerank = VS_K_COARSE_RERANK;
     cj.narrow = !getenv("VS_COARSE_WIDE");
-    CKS(run_enn(ctx, cj, cm, 0, false));
+    // VS_OPT_COARSE: 0 auto (dense keys when the tensor cores pay off), 1 candidate
+    // buffers, 2 dense keys whenever the tensor cores apply
+    const bool dense_ok = nprobe <= kTopkCap && ctx->opt_enn_kernel != 1 && vs::tc_supported(d, VS_DTYPE_F32, 0);
+    if (dense_ok && (ctx->opt_coarse == 2 || (ctx->opt_coarse == 0 && vs::tc_profitable(nq, ivf->nlist, d)))) {
+        CKS(coarse_dense(ctx, cj, cm));
+    } else {
+        CKS(run_enn(ctx, cj, cm, 0, false));
+    }
     }
     if (probe_only) {
         CKS(flush_out(ctx, pending));

@@ -129,6 +129,7 @@ struct vs_ctx {
     int opt_slack = 0;
     int opt_force_retry = 0;
     int opt_timing = 0;
+    int opt_coarse = 0;              // IVF coarse quantizer: 0 auto, 1 candidate buffers, 2 dense keys
     int64_t opt_stream_chunk = 0;    // host-resident search: selected rows per chunk (0 = auto)
     int64_t opt_ivf_chunk_rows = 0;  // tensor-core IVF scan: rows per list chunk (0 = 131072)
     int sm_reserve = 0;              // SMs left free by persistent kernels (streamed gathers)

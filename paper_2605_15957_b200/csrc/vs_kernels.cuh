@@ -238,6 +238,11 @@ struct RerankParams {
 template <typename T>
 cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s);
 
+// dense keys [nq][ncols] -> one margin-band buffer per query (cb.n_sub = 1):
+// every column with key <= k-th key + margin (overflow flagged past cb.C)
+cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
+                                const CandBuf& cb, cudaStream_t s);
+
 // [G][nq][k] sorted shard key lists -> [nq] k-th smallest of their union
 cudaError_t launch_union_kth(const float* keys, int G, int64_t nq, int k, float* out, cudaStream_t s);
 

@@ -965,6 +965,78 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
     }
 }
 
+// IVF coarse quantizer with dense keys (tc_dense_keys): per query, the k-th
+// smallest key K* and every column with key <= K* + margin land in a single
+// candidate buffer (the margin band: exact by construction);
+// k_rerank then scores them exactly. Rows of up to kDenseCache keys are cached
+// in shared memory for the select passes.
+constexpr int kDenseCache = 16384;
+__global__ void __launch_bounds__(NT) k_dense_select(const float* __restrict__ keys, int64_t ncols, int k,
+                                                     const float* __restrict__ margin, CandBuf cb) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Small& sm = *reinterpret_cast<Small*>(smraw);
+    unsigned* hist = reinterpret_cast<unsigned*>(smraw + ((sizeof(Small) + 127) & ~size_t(127)));
+    float* kc = reinterpret_cast<float*>(hist + HBINS);
+    const int tid = threadIdx.x;
+    const int64_t q = blockIdx.x;
+    const float* row = keys + q * ncols;
+    const bool cached = ncols <= kDenseCache;
+    if (cached) {
+        if ((ncols & 3) == 0) {
+            for (int64_t i = tid; i < ncols / 4; i += NT)
+                reinterpret_cast<float4*>(kc)[i] = __ldcs(reinterpret_cast<const float4*>(row) + i);
+        } else {
+            for (int64_t i = tid; i < ncols; i += NT) kc[i] = __ldcs(row + i);
+        }
+    }
+    __syncthreads();
+    const float* src = cached ? kc : row;
+    const unsigned kk = (unsigned)min((int64_t)k, ncols);
+    const uint32_t kth = block_radix_kth(
+        [&](auto fn) {
+            for (int64_t i = tid; i < ncols; i += NT) fn(f2o(src[i]));
+        },
+        kk, hist, sm);
+    const uint32_t thr = f2o(__fadd_ru(o2f(kth), margin[q]));
+    if (tid == 0) sm.counter = 0;
+    __syncthreads();
+    const int C = cb.C;
+    float* bk = cb.key + q * (int64_t)C;
+    uint32_t* bp = cb.pos + q * (int64_t)C;
+    const int lane = tid & 31;
+    for (int64_t i0 = 0; i0 < ncols; i0 += NT) {
+        const int64_t i = i0 + tid;
+        const float kv = i < ncols ? src[i] : 0.f;
+        const bool live = i < ncols && f2o(kv) <= thr;
+        const unsigned b = __ballot_sync(VS_FULL, live);
+        if (!b) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
+        base = __shfl_sync(VS_FULL, base, 0);
+        const int slot = base + __popc(b & lanemask_lt());
+        if (live && slot < C) {
+            bk[slot] = kv;
+            bp[slot] = (uint32_t)i;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        cb.cnt[q] = min(sm.counter, C);
+        if (sm.counter > C) cb.overflow[q] = 1;
+    }
+}
+
+cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
+                                const CandBuf& cb, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    const size_t smem = ((sizeof(Small) + 127) & ~size_t(127)) + (size_t)HBINS * 4 +
+                        (ncols <= kDenseCache ? (size_t)ncols * 4 : 0);
+    cudaError_t e = cudaFuncSetAttribute(k_dense_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_dense_select<<<(unsigned)nq, NT, smem, s>>>(keys, ncols, k, margin, cb);
+    return cudaGetLastError();
+}
+
 // k-th smallest of the union of G sorted key lists per query (distributed
 // protocol: the exact global k-th approximate key from every shard's local
 // top-k keys): [G][nq][k] -> [nq]

@@ -116,6 +116,8 @@ struct Params {
     int lim0;                       // first compaction point (0: 2k + 64)
     int dense_direct;               // epilogue: dense chunks append per lane (else cooperatively)
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
+    float* keys_out;                // MODE 3: dense approximate keys [nq][keys_ld]
+    int64_t keys_ld;
 };
 
 // one work item: A tile rows [a_row, a_row + QTILE), B tiles of BN rows from
@@ -547,6 +549,70 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 else mbar_arrive(&S.tempty[acc]);
             }
             if (q < p.nq) atomicMin(&p.argmin_out[q], ((unsigned long long)best_o << 32) | best_i);
+        }
+    } else if (warp >= EPI_WARP0 && MODE == 3) {
+        // ===== epilogue (dense keys): TMEM -> approximate keys -> global =====
+        // (IVF coarse quantizer: every (query, centroid) key is stored and a
+        // per-query select follows, instead of candidate buffers)
+        const int et = threadIdx.x - EPI_WARP0 * 32;
+        const int row = et & (BM - 1);
+        const int half = et >> 7;
+        const int quad = warp & 3;
+        float* xw = xn_w[warp - EPI_WARP0];
+        uint32_t tcount = 0;
+        for (int64_t it = unit; it < nitems; it += nunits) {
+            const Item item = decode_item<MODE, QTILE>(p, it);
+            const int64_t q = item.a_row + (int64_t)rank * BM + row;
+            float* krow = p.keys_out + (q < p.nq ? q : 0) * p.keys_ld;
+            for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
+                const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
+                const int64_t r0 = item.b_row0 + t * BN;
+                const int ncols = (int)min((int64_t)BN, p.nsel - r0);
+                if (!IP) {
+                    for (int c = lane * 4; c < BN / 2; c += 128) {
+                        const int64_t i = r0 + half * (BN / 2) + c;
+                        float4 v;
+                        v.x = i + 0 < p.nsel ? __ldg(p.xn + i + 0) : 0.f;
+                        v.y = i + 1 < p.nsel ? __ldg(p.xn + i + 1) : 0.f;
+                        v.z = i + 2 < p.nsel ? __ldg(p.xn + i + 2) : 0.f;
+                        v.w = i + 3 < p.nsel ? __ldg(p.xn + i + 3) : 0.f;
+                        *reinterpret_cast<float4*>(xw + c) = v;
+                    }
+                }
+                __syncwarp();
+                mbar_wait(&S.tfull[acc], aph);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * BN + half * (BN / 2);
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 64; ++ch) {
+                    uint32_t r[32];
+                    TMEM_LD32(taddr + ch * 32, r);
+                    tmem_wait_ld();
+                    const int cb0 = half * (BN / 2) + ch * 32;
+                    float kv[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float a = __uint_as_float(r[j]);
+                        kv[j] = IP ? -a : fmaf(-2.f, a, xw[ch * 32 + j]);
+                    }
+                    if (q < p.nq) {
+                        float* dst = krow + r0 + cb0;
+                        if (cb0 + 32 <= ncols && ((p.keys_ld | r0) & 3) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                __stcs(reinterpret_cast<float4*>(dst + j), make_float4(kv[j], kv[j + 1], kv[j + 2], kv[j + 3]));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (cb0 + j < ncols) dst[j] = kv[j];
+                        }
+                    }
+                }
+                tc_fence_before();
+                if (PAIR) mbar_arrive_leader(&S.tempty[acc]);
+                else mbar_arrive(&S.tempty[acc]);
+                __syncwarp();
+            }
         }
     } else if (warp >= EPI_WARP0) {
         // ===== epilogue: TMEM -> keys -> candidate buffers =====
@@ -1243,6 +1309,85 @@ int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* 
     const int dp = (d + 7) / 8 * 8;
     const unsigned blocks = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 148 * 64);
     tc::k_stage_rows<float><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, out, nullptr, junk);
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    return VS_OK;
+}
+
+// Dense approximate keys of every (query, column) pair on the tensor cores
+// (MODE 3): keys[q][c] = ||c||^2 - 2 q~.c~ (or -q~.c~), margin[q] = 2 x their
+// rigorous error bound (k_tc_margins). The IVF coarse quantizer's phase A:
+// its columns (the centroids) are few enough that the whole key matrix of a
+// query chunk is cheaper to write and select from than candidate buffers.
+int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X, int64_t ncols,
+                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin) {
+    using namespace vs_internal;
+    if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cudaStream_t st = ctx->stream;
+    const int dp = (d + 7) / 8 * 8;
+    __nv_bfloat16 *qa = nullptr, *xb = nullptr;
+    float* xn = nullptr;
+    float2* qerr = nullptr;
+    unsigned* xmax2 = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq * dp, &qa));
+    CKS(arena_alloc(ctx, (size_t)ncols * dp, &xb));
+    CKS(arena_alloc(ctx, (size_t)ncols, &xn));
+    CKS(arena_alloc(ctx, (size_t)nq, &qerr));
+    CKS(arena_alloc(ctx, 2, &xmax2));
+    {
+        KTimer kt(ctx, VS_K_STAGE);
+        CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));
+        const unsigned blocks = (unsigned)std::min<int64_t>((ncols * 32 + 255) / 256, 148 * 64);
+        tc::k_stage_rows<float><<<blocks, 256, 0, st>>>(X, nullptr, ncols, d, dp, xnorm, xb, ip ? nullptr : xn, xmax2);
+        CK(cudaGetLastError());
+        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+            Q, nq, d, dp, qa, qerr);
+        CK(cudaGetLastError());
+        tc::k_tc_margins<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qerr, nq, d, xmax, xmax2, ip, margin);
+        CK(cudaGetLastError());
+        ctx->stats[VS_STAT_LAUNCHES] += 3;
+    }
+    const bool pair = use_pair(nq);
+    const int qtile_rows = pair ? 2 * tc::BM : tc::BM;
+    const int qtiles = (int)((nq + qtile_rows - 1) / qtile_rows);
+    const int64_t ntiles = (ncols + tc::BN - 1) / tc::BN;
+    const int sms = pair ? ctx->sm_count / 2 : ctx->sm_count;
+    // splits: >= 2 waves of work items, the shortest makespan (no buffers to size)
+    int best_s = 1;
+    double best_cost = 1e30;
+    for (int s = 1; s <= std::min<int64_t>(ntiles, 64); ++s) {
+        const int64_t per = (ntiles + s - 1) / s;
+        const int64_t items = (int64_t)qtiles * ((ntiles + per - 1) / per);
+        const double cost = std::ceil((double)items / sms) * per + 0.5 * per / 8.0;
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best_s = s;
+        }
+    }
+    const int64_t per = (ntiles + best_s - 1) / best_s;
+    const int nsplit = (int)((ntiles + per - 1) / per);
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, qa, nq, d, dp, tc::BM) || !make_map(&mb, xb, ncols, d, dp, pair ? tc::BN / 2 : tc::BN))
+        return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    tc::Params pr{};
+    pr.nq = nq;
+    pr.d = d;
+    pr.kblocks = (d + tc::BK - 1) / tc::BK;
+    pr.nsel = ncols;
+    pr.qtiles = qtiles;
+    pr.nsplit = nsplit;
+    pr.tiles_per_split = per;
+    pr.ntiles = ntiles;
+    pr.xn = xn;
+    pr.ip = ip;
+    pr.keys_out = keys;
+    pr.keys_ld = ncols;
+    const int64_t items = (int64_t)qtiles * nsplit;
+    const unsigned units = (unsigned)std::min<int64_t>(items, sms);
+    const unsigned grid = pair ? 2 * units : units;
+    KTimer kt(ctx, VS_K_COARSE);
+    if (ip) CK((pair ? launch_tc<true, 3, true>(ma, mb, pr, grid, st) : launch_tc<true, 3, false>(ma, mb, pr, grid, st)));
+    else CK((pair ? launch_tc<false, 3, true>(ma, mb, pr, grid, st) : launch_tc<false, 3, false>(ma, mb, pr, grid, st)));
     CK(cudaGetLastError());
     ctx->stats[VS_STAT_LAUNCHES] += 1;
     return VS_OK;

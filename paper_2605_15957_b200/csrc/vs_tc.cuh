@@ -15,6 +15,8 @@ namespace vs {
 namespace bn128 {
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift,
                 CandBuf* cb, bool* exhaustive, int timer_class);
+int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X, int64_t ncols,
+                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin);
 }
 inline namespace bn256 {
 
@@ -35,6 +37,10 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
                    const float* cnorm, int64_t ncols, unsigned long long* out, __nv_bfloat16* xb,
                    unsigned* junk);
 int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out, unsigned* junk);
+// dense approximate keys [nq][ncols] of float32 rows X on the tensor cores
+// (MODE 3; the IVF coarse quantizer) and their per-query margins
+int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X, int64_t ncols,
+                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin);
 
 // IVF list-major phase A on the tensor cores (bf16 list-contiguous payload):
 // pairs already grouped by list into units of <= 128 pairs

@@ -99,3 +99,31 @@ def test_list_sharding_plus_merge_equals_unsharded():
     mask = np.arange(12)[None, :] < oc[:, None]
     assert np.array_equal(oi[mask], whole.data_row)
     assert np.array_equal(od[mask], whole.distance)
+
+
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+@pytest.mark.parametrize("coarse", [1, 2])
+def test_coarse_quantizer_modes_equal_oracle(metric, coarse):
+    """The coarse quantizer with candidate buffers (VS_OPT_COARSE=1) and with
+    dense tensor-core keys + per-query margin-band select (2): identical
+    probes (the reference's select_top over float64 centroid distances)."""
+    rng = np.random.default_rng(17 + coarse)
+    n, d, nlist = 40000, 128, 2048
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    cen = data[np.sort(rng.choice(n, nlist, replace=False))].copy()
+    cen[7] = cen[3]                                     # tied centroids: the lower list id wins
+    assign = np.argmin(O.pairwise_sq_l2_fast(data, cen), axis=1)
+    parts = [np.flatnonzero(assign == c).astype(np.int64) for c in range(nlist)]
+    payload = [data[p] for p in parts]
+    q = rng.standard_normal((400, d)).astype(np.float32)
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_COARSE, coarse)
+    try:
+        idx = vs.IvfIndex(nlist, d, n, metric, "owning", cen, parts, payload)
+        got = idx.search(q, vs.SearchParams(k=10, nprobe=40))
+    finally:
+        ctx.set_option(N.OPT_COARSE, 0)
+    ref = O.ivf_search(q, cen, parts, lambda c: payload[c], 40, 10, metric)
+    assert np.array_equal(got.probes, ref.probes)
+    assert np.array_equal(got.data_row, ref.data_row)
+    assert np.array_equal(got.distance, ref.distance)
