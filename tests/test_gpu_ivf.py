@@ -6,6 +6,7 @@ import pytest
 
 import paper_2605_15957_b200 as vs
 from oracle import sqlvs_oracle as O
+from paper_2605_15957_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
 
