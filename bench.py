@@ -216,11 +216,30 @@ def _device_slice_bf16(n, d, lo, hi, dev):
 _SAMPLE = {}
 
 
+def _ref_sqlvs():
+    """The unmodified reference package shipped as oracle/_ref/sqlvs (copied by
+    oracle/build_ref.py in the build container), or None."""
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "sqlvs" / "vecindex.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import sqlvs.table
+    import sqlvs.vecindex
+    return sqlvs
+
+
 def _cpu_worker(qi):
-    from oracle import sqlvs_oracle as O
     s = _SAMPLE
     # reference pipeline: the filtered side is gathered once (relops.py:112-113),
-    # then enn_search scores it exhaustively in float64 (vecindex.py:109-132)
+    # then enn_search scores it exhaustively in float64 (vecindex.py:109-132):
+    # the reference's own code when shipped (oracle/_ref), else the oracle port
+    ref = s.get("ref")
+    if ref is not None:
+        ref.vecindex.enn_search(ref.table.EmbeddingColumn(s["q"][qi:qi + 1]), s["ref_col"],
+                                ref.vecindex.SearchParams(k=s["k"]))
+        return qi
+    from oracle import sqlvs_oracle as O
     O.enn_search(s["q"][qi:qi + 1], s["xs"], s["k"], row_ids=s["rows"])
     return qi
 
@@ -240,7 +259,7 @@ def cpu_sample(cfg, rows=262_144, seed=42):
     return x, mask, q
 
 
-def time_cpu_reference(cfg, budget_s=15.0, processes=1):
+def time_cpu_reference(cfg, budget_s=15.0, processes=1, use_reference=False):
     """Reference search (oracle port) q/s on the sample, extrapolated to the
     full collection. processes > 1: query-sharded worker processes."""
     import multiprocessing as mp
@@ -250,6 +269,9 @@ def time_cpu_reference(cfg, budget_s=15.0, processes=1):
         _SAMPLE.update(xs=np.ascontiguousarray(x[rows_sel]), rows=rows_sel, q=q, k=cfg["k"],
                        n_rows=x.shape[0], n_sel=int(mask.sum()))
         del x
+        ref = _ref_sqlvs() if use_reference else None
+        if ref is not None:
+            _SAMPLE.update(ref=ref, ref_col=ref.table.EmbeddingColumn(_SAMPLE["xs"]))
     q = _SAMPLE["q"]
     rows = _SAMPLE["n_rows"]
     done = 0
@@ -964,17 +986,20 @@ def run_reference(args, cfg):
     vals = []
     sample = ""
     for i in range(args.warmup + args.steps):
-        qps, sample, _ = time_cpu_reference(cfg, budget_s=args.ref_budget, processes=procs)
+        qps, sample, _ = time_cpu_reference(cfg, budget_s=args.ref_budget, processes=procs, use_reference=True)
         if i >= args.warmup:
             vals.append(qps)
     v = statistics.median(vals)
+    kind = "reference" if _SAMPLE.get("ref") is not None else "port"
+    sample += ("; the unmodified reference sqlvs.vecindex.enn_search (oracle/_ref)" if kind == "reference"
+               else "; the oracle port of enn_search (oracle/_ref absent)")
     print(json.dumps({
         "impl": "reference", "metric": "filtered top-k queries/sec", "value": round(v, 6),
         "unit": "queries/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (Vec-H mixture law, host sample)",
         "config": {"workload": cfg["name"]},
-        "cpu_baseline": {"value": round(v, 6), "unit": "queries/s", "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": round(v, 6), "unit": "queries/s", "cores": procs, "kind": kind,
                          "sample": sample + f"; {procs} query-sharded processes"},
         "e2e": {"value": round(v, 6), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -992,8 +1017,13 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=8.0)
     ap.add_argument("--cand-slack", type=int, default=0, help="VS_OPT_CAND_SLACK (candidate buffer x2^s)")
+    ap.add_argument("--n-rows", type=int, default=0,
+                    help="code-path runs only (e.g. the N>1 path on one GPU): a smaller collection; "
+                         "never used for reported numbers")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.n_rows:
+        cfg.update(n=args.n_rows, name=cfg["name"] + f" [CODE-PATH RUN: {args.n_rows} rows]")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -1979,7 +1979,7 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
         CKS(arena_alloc(ctx, (size_t)n, &cb.overflow));
         CK(cudaMemsetAsync(cb.overflow, 0, n * sizeof(int), ctx->stream));
         {
-            KTimer kt(ctx, cj.cls_rerank);
+            KTimer kt(ctx, cj.cls_scan);   // candidate generation: part of the coarse phase A
             CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cb, ctx->stream));
         }
         ctx->stats[VS_STAT_LAUNCHES] += 1;

@@ -969,51 +969,128 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
 // smallest key K* and every column with key <= K* + margin land in a single
 // candidate buffer (the margin band: exact by construction);
 // k_rerank then scores them exactly. Rows of up to kDenseCache keys are cached
-// in shared memory for the select passes.
+// in shared memory. The k-th key comes from a range-adaptive radix select:
+// the first pass bins the row's actual key range [min, max] into 2048 bins
+// (a query's centroid keys share one or two exponents, so the top bits of the
+// raw key would put all 16k keys into a handful of bins and serialise the
+// histogram atomics), each later pass splits the chosen bin the same way.
 constexpr int kDenseCache = 16384;
-__global__ void __launch_bounds__(NT) k_dense_select(const float* __restrict__ keys, int64_t ncols, int k,
-                                                     const float* __restrict__ margin, CandBuf cb) {
+constexpr int DS_NT = 512;
+__global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict__ keys, int64_t ncols, int k,
+                                                        const float* __restrict__ margin, CandBuf cb) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    Small& sm = *reinterpret_cast<Small*>(smraw);
-    unsigned* hist = reinterpret_cast<unsigned*>(smraw + ((sizeof(Small) + 127) & ~size_t(127)));
+    unsigned* hist = reinterpret_cast<unsigned*>(smraw);          // [HBINS]
     float* kc = reinterpret_cast<float*>(hist + HBINS);
-    const int tid = threadIdx.x;
+    __shared__ unsigned red_lo[DS_NT / 32], red_hi[DS_NT / 32], wtot[DS_NT / 32];
+    __shared__ int sel_bin, counter;
+    __shared__ unsigned sel_below;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    constexpr int NWD = DS_NT / 32;
     const int64_t q = blockIdx.x;
     const float* row = keys + q * ncols;
     const bool cached = ncols <= kDenseCache;
+    uint32_t lo = 0xffffffffu, hi = 0u;
     if (cached) {
         if ((ncols & 3) == 0) {
-            for (int64_t i = tid; i < ncols / 4; i += NT)
-                reinterpret_cast<float4*>(kc)[i] = __ldcs(reinterpret_cast<const float4*>(row) + i);
+            for (int64_t i = tid; i < ncols / 4; i += DS_NT) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
+                reinterpret_cast<float4*>(kc)[i] = v;
+                lo = min(min(lo, f2o(v.x)), min(f2o(v.y), min(f2o(v.z), f2o(v.w))));
+                hi = max(max(hi, f2o(v.x)), max(f2o(v.y), max(f2o(v.z), f2o(v.w))));
+            }
         } else {
-            for (int64_t i = tid; i < ncols; i += NT) kc[i] = __ldcs(row + i);
+            for (int64_t i = tid; i < ncols; i += DS_NT) {
+                const float v = __ldcs(row + i);
+                kc[i] = v;
+                lo = min(lo, f2o(v));
+                hi = max(hi, f2o(v));
+            }
+        }
+    } else {
+        for (int64_t i = tid; i < ncols; i += DS_NT) {
+            const uint32_t u = f2o(row[i]);
+            lo = min(lo, u);
+            hi = max(hi, u);
         }
     }
+    lo = __reduce_min_sync(VS_FULL, lo);
+    hi = __reduce_max_sync(VS_FULL, hi);
+    if (lane == 0) {
+        red_lo[w] = lo;
+        red_hi[w] = hi;
+    }
     __syncthreads();
+    uint32_t base = red_lo[0], top = red_hi[0];
+    for (int i = 1; i < NWD; ++i) {
+        base = min(base, red_lo[i]);
+        top = max(top, red_hi[i]);
+    }
     const float* src = cached ? kc : row;
-    const unsigned kk = (unsigned)min((int64_t)k, ncols);
-    const uint32_t kth = block_radix_kth(
-        [&](auto fn) {
-            for (int64_t i = tid; i < ncols; i += NT) fn(f2o(src[i]));
-        },
-        kk, hist, sm);
-    const uint32_t thr = f2o(__fadd_ru(o2f(kth), margin[q]));
-    if (tid == 0) sm.counter = 0;
+    unsigned kk = (unsigned)min((int64_t)k, ncols);
+    uint32_t range = top - base;   // keys live in [base, base + range]
+#pragma unroll 1
+    while (range > 0) {
+        const int shift = max(0, 32 - __clz(range) - 11);
+        const int nb = (int)(range >> shift) + 1;   // <= HBINS
+        for (int i = tid; i < nb; i += DS_NT) hist[i] = 0u;
+        __syncthreads();
+        for (int64_t i = tid; i < ncols; i += DS_NT) {
+            const uint32_t u = f2o(src[i]);
+            if (u >= base && u - base <= range) atomicAdd(&hist[(u - base) >> shift], 1u);
+        }
+        __syncthreads();
+        const int per = (nb + DS_NT - 1) / DS_NT;
+        unsigned loc = 0;
+        for (int b = 0; b < per; ++b) {
+            const int bi = tid * per + b;
+            loc += bi < nb ? hist[bi] : 0u;
+        }
+        unsigned incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(VS_FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wtot[w] = incl;
+        __syncthreads();
+        unsigned excl = incl - loc;
+        for (int i = 0; i < w; ++i) excl += wtot[i];
+        if (excl < kk && kk <= excl + loc) {
+            unsigned c = excl;
+            for (int b = 0; b < per; ++b) {
+                const int bi = tid * per + b;
+                const unsigned h = bi < nb ? hist[bi] : 0u;
+                if (c + h >= kk) {
+                    sel_bin = bi;
+                    sel_below = c;
+                    break;
+                }
+                c += h;
+            }
+        }
+        __syncthreads();
+        kk -= sel_below;
+        const uint32_t off = (uint32_t)sel_bin << shift;
+        base += off;
+        range = min(range - off, shift ? (1u << shift) - 1u : 0u);
+        __syncthreads();
+    }
+    const uint32_t thr = f2o(__fadd_ru(o2f(base), margin[q]));
+    if (tid == 0) counter = 0;
     __syncthreads();
     const int C = cb.C;
     float* bk = cb.key + q * (int64_t)C;
     uint32_t* bp = cb.pos + q * (int64_t)C;
-    const int lane = tid & 31;
-    for (int64_t i0 = 0; i0 < ncols; i0 += NT) {
+    for (int64_t i0 = 0; i0 < ncols; i0 += DS_NT) {
         const int64_t i = i0 + tid;
         const float kv = i < ncols ? src[i] : 0.f;
         const bool live = i < ncols && f2o(kv) <= thr;
         const unsigned b = __ballot_sync(VS_FULL, live);
         if (!b) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
-        base = __shfl_sync(VS_FULL, base, 0);
-        const int slot = base + __popc(b & lanemask_lt());
+        int bs = 0;
+        if (lane == 0) bs = atomicAdd(&counter, __popc(b));
+        bs = __shfl_sync(VS_FULL, bs, 0);
+        const int slot = bs + __popc(b & lanemask_lt());
         if (live && slot < C) {
             bk[slot] = kv;
             bp[slot] = (uint32_t)i;
@@ -1021,19 +1098,18 @@ __global__ void __launch_bounds__(NT) k_dense_select(const float* __restrict__ k
     }
     __syncthreads();
     if (tid == 0) {
-        cb.cnt[q] = min(sm.counter, C);
-        if (sm.counter > C) cb.overflow[q] = 1;
+        cb.cnt[q] = min(counter, C);
+        if (counter > C) cb.overflow[q] = 1;
     }
 }
 
 cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
                                 const CandBuf& cb, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    const size_t smem = ((sizeof(Small) + 127) & ~size_t(127)) + (size_t)HBINS * 4 +
-                        (ncols <= kDenseCache ? (size_t)ncols * 4 : 0);
+    const size_t smem = (size_t)HBINS * 4 + (ncols <= kDenseCache ? (size_t)ncols * 4 : 0);
     cudaError_t e = cudaFuncSetAttribute(k_dense_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_dense_select<<<(unsigned)nq, NT, smem, s>>>(keys, ncols, k, margin, cb);
+    k_dense_select<<<(unsigned)nq, DS_NT, smem, s>>>(keys, ncols, k, margin, cb);
     return cudaGetLastError();
 }
 
