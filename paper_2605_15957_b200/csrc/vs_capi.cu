@@ -1983,6 +1983,14 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
             CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cb, ctx->stream));
         }
         ctx->stats[VS_STAT_LAUNCHES] += 1;
+        // the bf16 band (~2x nprobe centroids) -> fp32 keys with the SIMT margin:
+        // phase B re-scores ~nprobe centroids in float64 instead of the band
+        const bool refine = cj.ip == 0 && simt_margin != nullptr;
+        if (refine) {
+            KTimer kt(ctx, cj.cls_rerank);
+            CK(vs::launch_refine32(cb, n, sub.q, cj.d, (const float*)cj.rows, ctx->stream));
+            ctx->stats[VS_STAT_LAUNCHES] += 1;
+        }
         PhaseA st;
         st.sp.Q = sub.q;
         st.sp.nq = n;
@@ -1991,7 +1999,7 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
         st.sp.sel = nullptr;
         st.sp.nsel = ncols;
         st.sp.xnorm = cj.xnorm;
-        st.sp.margin = tm + q0;
+        st.sp.margin = refine ? simt_margin + q0 : tm + q0;
         st.sp.ip = cj.ip;
         st.sp.k = cj.k;
         st.sp.cb = cb;
@@ -1999,7 +2007,6 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
         st.sp.verify = 0;
         st.exhaustive = false;
         ctx->stats[VS_STAT_LAST_ENN_KERNEL] = 2;
-        (void)simt_margin;
         CKS(enn_phase_b(ctx, sub, st, 0, false, PhaseBHooks{}));
     }
     return VS_OK;

@@ -242,6 +242,9 @@ cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s);
 // every column with key <= k-th key + margin (overflow flagged past cb.C)
 cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
                                 const CandBuf& cb, cudaStream_t s);
+// rewrite each buffer entry's key as the fp32 squared distance (q - x)^2
+// (squared-L2 bands only; margin eps_simt applies)
+cudaError_t launch_refine32(const CandBuf& cb, int64_t nq, const float* Q, int d, const float* X, cudaStream_t s);
 
 // [G][nq][k] sorted shard key lists -> [nq] k-th smallest of their union
 cudaError_t launch_union_kth(const float* keys, int G, int64_t nq, int k, float* out, cudaStream_t s);

@@ -980,7 +980,7 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
                                                         const float* __restrict__ margin, CandBuf cb) {
     extern __shared__ __align__(16) unsigned char smraw[];
     unsigned* hist = reinterpret_cast<unsigned*>(smraw);          // [HBINS]
-    float* kc = reinterpret_cast<float*>(hist + HBINS);
+    uint32_t* kc = reinterpret_cast<uint32_t*>(hist + HBINS);      // orderable keys (cached rows)
     __shared__ unsigned red_lo[DS_NT / 32], red_hi[DS_NT / 32], wtot[DS_NT / 32];
     __shared__ int sel_bin, counter;
     __shared__ unsigned sel_below;
@@ -988,27 +988,23 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
     constexpr int NWD = DS_NT / 32;
     const int64_t q = blockIdx.x;
     const float* row = keys + q * ncols;
+    const int n = (int)ncols;
     const bool cached = ncols <= kDenseCache;
+    const bool vec = cached && (n & 3) == 0;
+    // keys as orderable uint32 (converted once), and their range
     uint32_t lo = 0xffffffffu, hi = 0u;
-    if (cached) {
-        if ((ncols & 3) == 0) {
-            for (int64_t i = tid; i < ncols / 4; i += DS_NT) {
-                const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
-                reinterpret_cast<float4*>(kc)[i] = v;
-                lo = min(min(lo, f2o(v.x)), min(f2o(v.y), min(f2o(v.z), f2o(v.w))));
-                hi = max(max(hi, f2o(v.x)), max(f2o(v.y), max(f2o(v.z), f2o(v.w))));
-            }
-        } else {
-            for (int64_t i = tid; i < ncols; i += DS_NT) {
-                const float v = __ldcs(row + i);
-                kc[i] = v;
-                lo = min(lo, f2o(v));
-                hi = max(hi, f2o(v));
-            }
+    if (vec) {
+        for (int i = tid; i < n / 4; i += DS_NT) {
+            const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
+            const uint4 u = make_uint4(f2o(v.x), f2o(v.y), f2o(v.z), f2o(v.w));
+            reinterpret_cast<uint4*>(kc)[i] = u;
+            lo = min(lo, min(min(u.x, u.y), min(u.z, u.w)));
+            hi = max(hi, max(max(u.x, u.y), max(u.z, u.w)));
         }
     } else {
-        for (int64_t i = tid; i < ncols; i += DS_NT) {
-            const uint32_t u = f2o(row[i]);
+        for (int i = tid; i < n; i += DS_NT) {
+            const uint32_t u = f2o(__ldcs(row + i));
+            if (cached) kc[i] = u;
             lo = min(lo, u);
             hi = max(hi, u);
         }
@@ -1021,12 +1017,13 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
     }
     __syncthreads();
     uint32_t base = red_lo[0], top = red_hi[0];
+#pragma unroll
     for (int i = 1; i < NWD; ++i) {
         base = min(base, red_lo[i]);
         top = max(top, red_hi[i]);
     }
-    const float* src = cached ? kc : row;
-    unsigned kk = (unsigned)min((int64_t)k, ncols);
+    auto key_at = [&](int i) -> uint32_t { return cached ? kc[i] : f2o(row[i]); };
+    unsigned kk = (unsigned)min(k, n);
     uint32_t range = top - base;   // keys live in [base, base + range]
 #pragma unroll 1
     while (range > 0) {
@@ -1034,9 +1031,20 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
         const int nb = (int)(range >> shift) + 1;   // <= HBINS
         for (int i = tid; i < nb; i += DS_NT) hist[i] = 0u;
         __syncthreads();
-        for (int64_t i = tid; i < ncols; i += DS_NT) {
-            const uint32_t u = f2o(src[i]);
-            if (u >= base && u - base <= range) atomicAdd(&hist[(u - base) >> shift], 1u);
+        if (vec) {
+            for (int i = tid; i < n / 4; i += DS_NT) {
+                const uint4 u = reinterpret_cast<const uint4*>(kc)[i];
+                uint32_t t;
+                t = u.x - base; if (u.x >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
+                t = u.y - base; if (u.y >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
+                t = u.z - base; if (u.z >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
+                t = u.w - base; if (u.w >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
+            }
+        } else {
+            for (int i = tid; i < n; i += DS_NT) {
+                const uint32_t u = key_at(i), t = u - base;
+                if (u >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
+            }
         }
         __syncthreads();
         const int per = (nb + DS_NT - 1) / DS_NT;
@@ -1081,10 +1089,10 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
     const int C = cb.C;
     float* bk = cb.key + q * (int64_t)C;
     uint32_t* bp = cb.pos + q * (int64_t)C;
-    for (int64_t i0 = 0; i0 < ncols; i0 += DS_NT) {
-        const int64_t i = i0 + tid;
-        const float kv = i < ncols ? src[i] : 0.f;
-        const bool live = i < ncols && f2o(kv) <= thr;
+    for (int i0 = 0; i0 < n; i0 += DS_NT) {
+        const int i = i0 + tid;
+        const uint32_t u = i < n ? key_at(i) : 0xffffffffu;
+        const bool live = i < n && u <= thr;
         const unsigned b = __ballot_sync(VS_FULL, live);
         if (!b) continue;
         int bs = 0;
@@ -1092,7 +1100,7 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
         bs = __shfl_sync(VS_FULL, bs, 0);
         const int slot = bs + __popc(b & lanemask_lt());
         if (live && slot < C) {
-            bk[slot] = kv;
+            bk[slot] = o2f(u);
             bp[slot] = (uint32_t)i;
         }
     }
@@ -1101,6 +1109,56 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
         cb.cnt[q] = min(counter, C);
         if (counter > C) cb.overflow[q] = 1;
     }
+}
+
+// fp32 refinement of a margin band (IVF coarse quantizer): every buffer entry's
+// key becomes the fp32 squared distance sum (q - x)^2, whose error is within
+// the SIMT margin eps_simt (vs_capi.cu) - ~10x tighter than the bf16 band.
+// The band contains the exact top-k (ties included), so the k-th fp32 key K32
+// of the band + that margin again keeps every exact top-k row: phase B then
+// scores ~k rows in float64 instead of the whole bf16 band.
+__global__ void __launch_bounds__(256) k_refine32(CandBuf cb, const float* __restrict__ Q, int d,
+                                                  const float* __restrict__ X) {
+    extern __shared__ __align__(16) float qsh[];
+    const int64_t q = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) qsh[i] = Q[q * d + i];
+    __syncthreads();
+    const int cnt = cb.cnt[q];
+    float* bk = cb.key + q * (int64_t)cb.C;
+    const uint32_t* bp = cb.pos + q * (int64_t)cb.C;
+    const bool v4 = (d & 3) == 0;
+    for (int i = w; i < cnt; i += (int)(blockDim.x >> 5)) {
+        const float* x = X + (int64_t)bp[i] * d;
+        float acc = 0.f;
+        if (v4) {
+            for (int e = lane * 4; e < d; e += 128) {
+                const float4 xv = __ldg(reinterpret_cast<const float4*>(x + e));
+                const float4 qv = *reinterpret_cast<const float4*>(qsh + e);
+                float t;
+                t = qv.x - xv.x; acc = fmaf(t, t, acc);
+                t = qv.y - xv.y; acc = fmaf(t, t, acc);
+                t = qv.z - xv.z; acc = fmaf(t, t, acc);
+                t = qv.w - xv.w; acc = fmaf(t, t, acc);
+            }
+        } else {
+            for (int e = lane; e < d; e += 32) {
+                const float t = qsh[e] - __ldg(x + e);
+                acc = fmaf(t, t, acc);
+            }
+        }
+        acc = warp_sumf(acc);
+        if (lane == 0) bk[i] = acc;
+    }
+}
+
+cudaError_t launch_refine32(const CandBuf& cb, int64_t nq, const float* Q, int d, const float* X, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    const size_t smem = (size_t)d * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_refine32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_refine32<<<(unsigned)nq, 256, smem, s>>>(cb, Q, d, X);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
