@@ -976,76 +976,52 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
 // histogram atomics), each later pass splits the chosen bin the same way.
 constexpr int kDenseCache = 16384;
 constexpr int DS_NT = 512;
-__global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict__ keys, int64_t ncols, int k,
-                                                        const float* __restrict__ margin, CandBuf cb) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    unsigned* hist = reinterpret_cast<unsigned*>(smraw);          // [HBINS]
-    uint32_t* kc = reinterpret_cast<uint32_t*>(hist + HBINS);      // orderable keys (cached rows)
-    __shared__ unsigned red_lo[DS_NT / 32], red_hi[DS_NT / 32], wtot[DS_NT / 32];
-    __shared__ int sel_bin, counter;
-    __shared__ unsigned sel_below;
+constexpr int DS_KPT = kDenseCache / DS_NT;     // keys per thread of a cached row
+constexpr int DS_CAND = 2048;                   // band candidates held in shared memory
+
+struct DsShared {
+    unsigned red_lo[DS_NT / 32], red_hi[DS_NT / 32], wtot[DS_NT / 32];
+    int sel_bin, counter, ovf;
+    unsigned sel_below;
+};
+
+// kk-th smallest (1 <= kk <= count) of the orderable keys `foreach` visits, by a
+// range-adaptive radix select: each pass bins the current key range into <=
+// HBINS bins and narrows to the bin holding the kk-th key
+template <class ForEach>
+__device__ uint32_t ds_radix_kth(ForEach foreach, unsigned kk, unsigned* hist, DsShared& S) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     constexpr int NWD = DS_NT / 32;
-    const int64_t q = blockIdx.x;
-    const float* row = keys + q * ncols;
-    const int n = (int)ncols;
-    const bool cached = ncols <= kDenseCache;
-    const bool vec = cached && (n & 3) == 0;
-    // keys as orderable uint32 (converted once), and their range
     uint32_t lo = 0xffffffffu, hi = 0u;
-    if (vec) {
-        for (int i = tid; i < n / 4; i += DS_NT) {
-            const float4 v = __ldcs(reinterpret_cast<const float4*>(row) + i);
-            const uint4 u = make_uint4(f2o(v.x), f2o(v.y), f2o(v.z), f2o(v.w));
-            reinterpret_cast<uint4*>(kc)[i] = u;
-            lo = min(lo, min(min(u.x, u.y), min(u.z, u.w)));
-            hi = max(hi, max(max(u.x, u.y), max(u.z, u.w)));
-        }
-    } else {
-        for (int i = tid; i < n; i += DS_NT) {
-            const uint32_t u = f2o(__ldcs(row + i));
-            if (cached) kc[i] = u;
-            lo = min(lo, u);
-            hi = max(hi, u);
-        }
-    }
+    foreach([&](uint32_t u) {
+        lo = min(lo, u);
+        hi = max(hi, u);
+    });
     lo = __reduce_min_sync(VS_FULL, lo);
     hi = __reduce_max_sync(VS_FULL, hi);
     if (lane == 0) {
-        red_lo[w] = lo;
-        red_hi[w] = hi;
+        S.red_lo[w] = lo;
+        S.red_hi[w] = hi;
     }
     __syncthreads();
-    uint32_t base = red_lo[0], top = red_hi[0];
+    uint32_t base = S.red_lo[0], top = S.red_hi[0];
 #pragma unroll
     for (int i = 1; i < NWD; ++i) {
-        base = min(base, red_lo[i]);
-        top = max(top, red_hi[i]);
+        base = min(base, S.red_lo[i]);
+        top = max(top, S.red_hi[i]);
     }
-    auto key_at = [&](int i) -> uint32_t { return cached ? kc[i] : f2o(row[i]); };
-    unsigned kk = (unsigned)min(k, n);
-    uint32_t range = top - base;   // keys live in [base, base + range]
+    uint32_t range = top - base;
+    __syncthreads();
 #pragma unroll 1
     while (range > 0) {
         const int shift = max(0, 32 - __clz(range) - 11);
-        const int nb = (int)(range >> shift) + 1;   // <= HBINS
+        const int nb = (int)(range >> shift) + 1;
         for (int i = tid; i < nb; i += DS_NT) hist[i] = 0u;
         __syncthreads();
-        if (vec) {
-            for (int i = tid; i < n / 4; i += DS_NT) {
-                const uint4 u = reinterpret_cast<const uint4*>(kc)[i];
-                uint32_t t;
-                t = u.x - base; if (u.x >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
-                t = u.y - base; if (u.y >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
-                t = u.z - base; if (u.z >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
-                t = u.w - base; if (u.w >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
-            }
-        } else {
-            for (int i = tid; i < n; i += DS_NT) {
-                const uint32_t u = key_at(i), t = u - base;
-                if (u >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
-            }
-        }
+        foreach([&](uint32_t u) {
+            const uint32_t t = u - base;
+            if (u >= base && t <= range) atomicAdd(&hist[t >> shift], 1u);
+        });
         __syncthreads();
         const int per = (nb + DS_NT - 1) / DS_NT;
         unsigned loc = 0;
@@ -1059,56 +1035,175 @@ __global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict_
             const unsigned t = __shfl_up_sync(VS_FULL, incl, o);
             if (lane >= o) incl += t;
         }
-        if (lane == 31) wtot[w] = incl;
+        if (lane == 31) S.wtot[w] = incl;
         __syncthreads();
         unsigned excl = incl - loc;
-        for (int i = 0; i < w; ++i) excl += wtot[i];
+        for (int i = 0; i < w; ++i) excl += S.wtot[i];
         if (excl < kk && kk <= excl + loc) {
             unsigned c = excl;
             for (int b = 0; b < per; ++b) {
                 const int bi = tid * per + b;
                 const unsigned h = bi < nb ? hist[bi] : 0u;
                 if (c + h >= kk) {
-                    sel_bin = bi;
-                    sel_below = c;
+                    S.sel_bin = bi;
+                    S.sel_below = c;
                     break;
                 }
                 c += h;
             }
         }
         __syncthreads();
-        kk -= sel_below;
-        const uint32_t off = (uint32_t)sel_bin << shift;
+        kk -= S.sel_below;
+        const uint32_t off = (uint32_t)S.sel_bin << shift;
         base += off;
         range = min(range - off, shift ? (1u << shift) - 1u : 0u);
         __syncthreads();
     }
-    const uint32_t thr = f2o(__fadd_ru(o2f(base), margin[q]));
-    if (tid == 0) counter = 0;
-    __syncthreads();
+    return base;
+}
+
+// IVF coarse quantizer with dense keys (tc_dense_keys): per query, the kk-th
+// smallest key K* and every column with key <= K* + margin land in a single
+// candidate buffer (the margin band: exact by construction).
+// A cached row (<= 16384 keys) is selected without touching every key more
+// than twice: each of the 512 threads holds 32 keys in registers; the kk-th
+// smallest of the 512 per-thread minima is an upper bound U >= K* (kk keys
+// lie at or below it) and in expectation barely above K*, so the keys <= U +
+// margin (a few more than the band) are compacted into shared memory and the
+// exact K* and band are taken there. Longer rows, or an unlucky U, fall back
+// to a range-adaptive radix select over the whole row.
+__global__ void __launch_bounds__(DS_NT) k_dense_select(const float* __restrict__ keys, int64_t ncols, int k,
+                                                        const float* __restrict__ margin, CandBuf cb) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    unsigned* hist = reinterpret_cast<unsigned*>(smraw);           // [HBINS]
+    uint32_t* cand = hist + HBINS;                                 // [DS_CAND] band candidates (orderable)
+    uint32_t* cpos = cand + DS_CAND;                               // [DS_CAND] their columns
+    uint32_t* tmin = cpos + DS_CAND;                               // [DS_NT]
+    __shared__ DsShared S;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t q = blockIdx.x;
+    const float* row = keys + q * ncols;
+    const int n = (int)ncols;
+    const unsigned kk = (unsigned)min(k, n);
+    const float mq = margin[q];
     const int C = cb.C;
     float* bk = cb.key + q * (int64_t)C;
     uint32_t* bp = cb.pos + q * (int64_t)C;
-    for (int i0 = 0; i0 < n; i0 += DS_NT) {
-        const int i = i0 + tid;
-        const uint32_t u = i < n ? key_at(i) : 0xffffffffu;
-        const bool live = i < n && u <= thr;
-        const unsigned b = __ballot_sync(VS_FULL, live);
-        if (!b) continue;
-        int bs = 0;
-        if (lane == 0) bs = atomicAdd(&counter, __popc(b));
-        bs = __shfl_sync(VS_FULL, bs, 0);
-        const int slot = bs + __popc(b & lanemask_lt());
-        if (live && slot < C) {
-            bk[slot] = o2f(u);
-            bp[slot] = (uint32_t)i;
+    if (tid == 0) {
+        S.counter = 0;
+        S.ovf = 0;
+    }
+    // thread t holds columns t + 512 j (j < 32)
+    uint32_t kr[DS_KPT];
+    const bool small = n <= kDenseCache && kk <= DS_NT;
+    uint32_t mn = 0xffffffffu;
+    if (small) {
+#pragma unroll
+        for (int j = 0; j < DS_KPT; ++j) {
+            const int i = tid + j * DS_NT;
+            kr[j] = i < n ? f2o(__ldcs(row + i)) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < DS_KPT; ++j) mn = min(mn, kr[j]);
+        tmin[tid] = mn;
+    }
+    __syncthreads();
+    uint32_t thr;   // final band: keys <= thr
+    bool done = false;
+    if (small) {
+        // U = kk-th smallest per-thread minimum (>= K*); candidates <= U + margin
+        const uint32_t U = ds_radix_kth(
+            [&](auto fn) {
+                if (tid < DS_NT) fn(tmin[tid]);
+            },
+            kk, hist, S);
+        const uint32_t thr_u = f2o(__fadd_ru(o2f(U), mq));
+#pragma unroll
+        for (int j = 0; j < DS_KPT; ++j) {
+            const bool live = kr[j] <= thr_u;
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            if (!b) continue;
+            int bs = 0;
+            if (lane == 0) bs = atomicAdd(&S.counter, __popc(b));
+            bs = __shfl_sync(VS_FULL, bs, 0);
+            const int slot = bs + __popc(b & lanemask_lt());
+            if (live && slot < DS_CAND) {
+                cand[slot] = kr[j];
+                cpos[slot] = (uint32_t)(tid + j * DS_NT);
+            }
+        }
+        __syncthreads();
+        const int nc = S.counter;
+        if (nc <= DS_CAND) {   // block-uniform
+            const uint32_t kth = ds_radix_kth(
+                [&](auto fn) {
+                    for (int i = tid; i < nc; i += DS_NT) fn(cand[i]);
+                },
+                kk, hist, S);
+            thr = f2o(__fadd_ru(o2f(kth), mq));
+            if (tid == 0) S.counter = 0;
+            __syncthreads();
+            for (int i0 = 0; i0 < nc; i0 += DS_NT) {
+                const int i = i0 + tid;
+                const bool live = i < nc && cand[i] <= thr;
+                const unsigned b = __ballot_sync(VS_FULL, live);
+                if (!b) continue;
+                int bs = 0;
+                if (lane == 0) bs = atomicAdd(&S.counter, __popc(b));
+                bs = __shfl_sync(VS_FULL, bs, 0);
+                const int slot = bs + __popc(b & lanemask_lt());
+                if (live && slot < C) {
+                    bk[slot] = o2f(cand[i]);
+                    bp[slot] = cpos[i];
+                }
+            }
+            done = true;
+        }
+        __syncthreads();
+        if (tid == 0 && !done) S.counter = 0;
+        __syncthreads();
+    }
+    if (!done) {
+        // whole-row radix select
+        const uint32_t kth = ds_radix_kth(
+            [&](auto fn) {
+                for (int i = tid; i < n; i += DS_NT) fn(f2o(row[i]));
+            },
+            kk, hist, S);
+        thr = f2o(__fadd_ru(o2f(kth), mq));
+        if (tid == 0) S.counter = 0;
+        __syncthreads();
+        for (int i0 = 0; i0 < n; i0 += DS_NT) {
+            const int i = i0 + tid;
+            const uint32_t u = i < n ? f2o(row[i]) : 0xffffffffu;
+            const bool live = i < n && u <= thr;
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            if (!b) continue;
+            int bs = 0;
+            if (lane == 0) bs = atomicAdd(&S.counter, __popc(b));
+            bs = __shfl_sync(VS_FULL, bs, 0);
+            const int slot = bs + __popc(b & lanemask_lt());
+            if (live && slot < C) {
+                bk[slot] = o2f(u);
+                bp[slot] = (uint32_t)i;
+            }
         }
     }
     __syncthreads();
     if (tid == 0) {
-        cb.cnt[q] = min(counter, C);
-        if (counter > C) cb.overflow[q] = 1;
+        cb.cnt[q] = min(S.counter, C);
+        if (S.counter > C) cb.overflow[q] = 1;
     }
+}
+
+cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
+                                const CandBuf& cb, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    const size_t smem = (size_t)HBINS * 4 + (size_t)DS_CAND * 8 + (size_t)DS_NT * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_dense_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_dense_select<<<(unsigned)nq, DS_NT, smem, s>>>(keys, ncols, k, margin, cb);
+    return cudaGetLastError();
 }
 
 // fp32 refinement of a margin band (IVF coarse quantizer): every buffer entry's
@@ -1161,15 +1256,6 @@ cudaError_t launch_refine32(const CandBuf& cb, int64_t nq, const float* Q, int d
     return cudaGetLastError();
 }
 
-cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
-                                const CandBuf& cb, cudaStream_t s) {
-    if (nq == 0) return cudaSuccess;
-    const size_t smem = (size_t)HBINS * 4 + (ncols <= kDenseCache ? (size_t)ncols * 4 : 0);
-    cudaError_t e = cudaFuncSetAttribute(k_dense_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_dense_select<<<(unsigned)nq, DS_NT, smem, s>>>(keys, ncols, k, margin, cb);
-    return cudaGetLastError();
-}
 
 // k-th smallest of the union of G sorted key lists per query (distributed
 // protocol: the exact global k-th approximate key from every shard's local
