@@ -324,6 +324,7 @@ int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bo
     rp.margin = sp.margin;
     rp.tau_g = sp.tau_g;
     rp.verify = sp.verify;
+    rp.band_ready = sp.band_ready;
     rp.rows = job.rows;
     rp.row_map = job.sel;
     rp.id_map = job.id_map;
@@ -1772,7 +1773,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         if (lmajor && job.pbits && sel_env && v->n_total < (int64_t)UINT32_MAX) {
             // filtered: pre-selected rows per list, one round trip per unit (vs_ivf_sel.cu)
             IvfGroups gr;
-            CKS(ivf_group(ctx, job, vs::kIvfLmQT, &gr));
+            CKS(ivf_group(ctx, job, vs::kSelUnitPairs, &gr));
             CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
             vs::IvfSelLaunch a;
             a.Q = job.q;
@@ -1797,9 +1798,6 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
             CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.lsel64));
             CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.sel_off));
             CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(v->n_total, 1), &a.spos));
-            char* recs = nullptr;
-            CKS(arena_alloc(ctx, (size_t)gr.max_units * vs::kIvfSelRecBytes, &recs));
-            a.recs = recs;
             a.tmp_bytes = vs::ivf_sel_temp_bytes(v->nlist);
             char* tmp = nullptr;
             CKS(arena_alloc(ctx, a.tmp_bytes, &tmp));
@@ -1950,11 +1948,19 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
 int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
     const int64_t ncols = cj.nsel;
     const int64_t qc = std::max<int64_t>(256, std::min<int64_t>(cj.nq, ((int64_t)1 << 28) / std::max<int64_t>(ncols, 1)));
+    // per-chunk minima let the select read ~4 % of the keys (k_coarse_select)
+    const bool chunked = vs::coarse_select_ok(ncols, cj.k) && !getenv("VS_COARSE_FULLSELECT");
+    const int64_t nch = (ncols + 31) / 32;
     float* keys = nullptr;
+    float* mins = nullptr;
     float* tm = nullptr;
     CKS(arena_alloc(ctx, (size_t)std::min(qc, cj.nq) * ncols, &keys));
+    if (chunked) CKS(arena_alloc(ctx, (size_t)std::min(qc, cj.nq) * nch, &mins));
     CKS(arena_alloc(ctx, (size_t)cj.nq, &tm));
     const int C = (int)pow2ceil(std::max<int64_t>(4 * (int64_t)cj.k, cj.k + 256));
+    // fp16 operands: the tensor-core band is already about as tight as the fp32
+    // SIMT margin, so the fp32 refinement pass would not shrink it
+    const bool f16 = vs::use_f16(VS_DTYPE_F32, cj.xmax);
     for (int64_t q0 = 0; q0 < cj.nq; q0 += qc) {
         const int64_t n = std::min(qc, cj.nq - q0);
         EnnJob sub = cj;
@@ -1966,10 +1972,10 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
         if (sub.out_count) sub.out_count += q0;
         if (cj.narrow)
             CKS(vs::bn128::tc_dense_keys(ctx, sub.q, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip,
-                                         keys, tm + q0));
+                                         keys, tm + q0, mins));
         else
             CKS(vs::tc_dense_keys(ctx, sub.q, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip, keys,
-                                  tm + q0));
+                                  tm + q0, mins));
         vs::CandBuf cb;
         cb.n_sub = 1;
         cb.C = C;
@@ -1980,12 +1986,13 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
         CK(cudaMemsetAsync(cb.overflow, 0, n * sizeof(int), ctx->stream));
         {
             KTimer kt(ctx, cj.cls_scan);   // candidate generation: part of the coarse phase A
-            CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cb, ctx->stream));
+            if (chunked) CK(vs::launch_coarse_select(keys, mins, n, ncols, cj.k, tm + q0, cb, ctx->stream));
+            else CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cb, ctx->stream));
         }
         ctx->stats[VS_STAT_LAUNCHES] += 1;
         // the bf16 band (~2x nprobe centroids) -> fp32 keys with the SIMT margin:
         // phase B re-scores ~nprobe centroids in float64 instead of the band
-        const bool refine = cj.ip == 0 && simt_margin != nullptr;
+        const bool refine = !f16 && cj.ip == 0 && simt_margin != nullptr;
         if (refine) {
             KTimer kt(ctx, cj.cls_rerank);
             CK(vs::launch_refine32(cb, n, sub.q, cj.d, (const float*)cj.rows, ctx->stream));
@@ -2005,6 +2012,7 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
         st.sp.cb = cb;
         st.sp.tau_g = nullptr;
         st.sp.verify = 0;
+        st.sp.band_ready = refine ? 0 : 1;   // the select wrote exactly the band of the k-th key
         st.exhaustive = false;
         ctx->stats[VS_STAT_LAST_ENN_KERNEL] = 2;
         CKS(enn_phase_b(ctx, sub, st, 0, false, PhaseBHooks{}));

@@ -62,6 +62,7 @@ struct EnnScanParams {
     CandBuf cb;
     unsigned* tau_g = nullptr;  // tensor-core path: per-query global admission bound
     int verify = 0;             // phase A kept local top-k only: phase B must verify
+    int band_ready = 0;         // one buffer per query holding exactly the margin band (RerankParams)
     cudaEvent_t q_ready = nullptr;  // nullable: queries still in flight (host->device on a copy
                                     // stream); phase A stages the rows first, then waits
 };
@@ -159,7 +160,7 @@ struct IvfSelLaunch {
     const uint32_t* pbits;      // permuted filter bitmap (required)
     const float* pnorm;         // ||x||^2 per payload row
     int nprobe;
-    const int32_t* pair_codes;  // from launch_ivf_group (unit_pairs = kIvfLmQT)
+    const int32_t* pair_codes;  // from launch_ivf_group (unit_pairs = kSelUnitPairs)
     const int4* units;
     const int32_t* n_units;
     int64_t max_units;
@@ -167,17 +168,16 @@ struct IvfSelLaunch {
     int ip, k;
     CandBuf cb;                 // n_sub = nprobe
     unsigned long long* visited;
-    // scratch: lsel [nlist], lsel64 / sel_off [nlist + 1], spos [n_total], recs [max_units] x 128 B
+    // scratch: lsel [nlist], lsel64 / sel_off [nlist + 1], spos [n_total]
     int32_t* lsel;
     int64_t* lsel64;
     int64_t* sel_off;
     uint32_t* spos;
-    void* recs;
     void* tmp;
     size_t tmp_bytes;           // >= ivf_sel_temp_bytes(nlist)
     int sm_count;
 };
-constexpr size_t kIvfSelRecBytes = 128;
+constexpr int kSelUnitPairs = 64;   // filtered scan: a unit is a whole list (its pairs split past 64)
 size_t ivf_sel_temp_bytes(int nlist);
 template <typename T>
 cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s);
@@ -232,6 +232,8 @@ struct RerankParams {
                                       //      exact key (distance, or -score) above this bound
     float* out_kth = nullptr;         // [nq][k] write this shard's k smallest approximate keys
                                       //      (ascending, +inf padded) and stop
+    int band_ready = 0;         // the single buffer per query already holds exactly the
+                                //      margin band of its k-th key: every entry survives
     int ubytes;                 // filled by launch_rerank: shared-memory union size
     int reg_path;               // filled by launch_rerank: register-resident scorer
 };
@@ -242,6 +244,11 @@ cudaError_t launch_rerank(const RerankParams& p, cudaStream_t s);
 // every column with key <= k-th key + margin (overflow flagged past cb.C)
 cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, int k, const float* margin,
                                 const CandBuf& cb, cudaStream_t s);
+// the same band from per-32-column key minima (MODE 3 `mins`): reads only
+// the chunks that can hold band keys; coarse_select_ok() says when it applies
+bool coarse_select_ok(int64_t ncols, int k);
+cudaError_t launch_coarse_select(const float* keys, const float* mins, int64_t nq, int64_t ncols, int k,
+                                 const float* margin, const CandBuf& cb, cudaStream_t s);
 // rewrite each buffer entry's key as the fp32 squared distance (q - x)^2
 // (squared-L2 bands only; margin eps_simt applies)
 cudaError_t launch_refine32(const CandBuf& cb, int64_t nq, const float* Q, int d, const float* X, cudaStream_t s);

@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
         // 1. k-th smallest approximate key  2. survivors (shared-memory path)
         uint32_t thr_o = 0xffffffffu;
         uint32_t kth = 0xffffffffu;
-        if (nl >= p.k && (nl > p.k || p.out_kth)) {
+        if (!p.band_ready && nl >= p.k && (nl > p.k || p.out_kth)) {
             kth = block_radix_kth(
                 [&](auto fn) {
                     for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
@@ -826,21 +826,49 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
 #pragma unroll
             for (int m = 0; m < 16; ++m) x[m] = m < M ? Pair2<T>::ld(xg + 8 * m) : make_float2(0.f, 0.f);
         };
-        // two rows per iteration (rows i and i + NWARP of this warp). The next
-        // pair's row indices (dependent loads of the survivor list and the
-        // selection) are fetched while this pair's row loads are in flight,
-        // and the next pair's rows are prefetched into L2.
+        // two rows per iteration (rows i and i + NWARP of this warp). Survivor
+        // rows are random 4 KB gathers from HBM, so the warp keeps RR_PD
+        // iterations (2 x RR_PD rows) of L2 prefetches ahead of its loads; the
+        // row indices (a dependent load through the selection) are resolved
+        // once into the union region, free between the survivor selection and
+        // the top-k (measured, config 2: one iteration of lead left every
+        // iteration waiting on HBM).
         auto prefetch_row = [&](int64_t r) {
             const char* base = reinterpret_cast<const char*>(rows + r * (int64_t)d);
             for (int o = lane * 128; o < row_bytes; o += 32 * 128)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
         };
+        constexpr int RR_PD = 4;
+        int64_t* ridx = reinterpret_cast<int64_t*>(u);
+        uint32_t* rps = reinterpret_cast<uint32_t*>(u + (size_t)ns * 8);
+        const bool staged = ns * 12 <= (int64_t)p.ubytes;   // block-uniform
+        if (staged) {
+            for (int64_t j = tid; j < ns; j += NT) {
+                uint32_t ps;
+                ridx[j] = row_of(j, ps);
+                rps[j] = ps;
+            }
+            __syncthreads();
+        }
+        auto row_at = [&](int64_t j, uint32_t& ps) -> int64_t {
+            if (staged) {
+                ps = rps[j];
+                return ridx[j];
+            }
+            return row_of(j, ps);
+        };
+        auto prefetch_iter = [&](int64_t j) {
+            uint32_t ps;
+            if (j < ns) prefetch_row(row_at(j, ps));
+            if (j + NWARP < ns) prefetch_row(row_at(j + NWARP, ps));
+        };
+        for (int pd = 1; pd <= RR_PD; ++pd) prefetch_iter(w + pd * 2 * NWARP);
         int64_t i = w;
         uint32_t psa = 0, psb = 0;
         int64_t ra = 0, rb = 0;
         if (i < ns) {
-            ra = row_of(i, psa);
-            rb = (i + NWARP < ns) ? row_of(i + NWARP, psb) : ra;
+            ra = row_at(i, psa);
+            rb = (i + NWARP < ns) ? row_at(i + NWARP, psb) : ra;
         }
         for (; i < ns; i += 2 * NWARP) {
             const int64_t i2 = i + NWARP;
@@ -848,15 +876,14 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
             float2 xa[16], xb[16];
             fetch(xa, ra);
             fetch(xb, rb);
-            // next pair: indices now (overlapping the loads above), rows -> L2
+            // RR_PD iterations ahead -> L2; the next pair's indices
+            prefetch_iter(i + (RR_PD + 1) * 2 * NWARP);
             const int64_t in = i + 2 * NWARP, in2 = in + NWARP;
             uint32_t psa_n = 0, psb_n = 0;
             int64_t ra_n = 0, rb_n = 0;
             if (in < ns) {
-                ra_n = row_of(in, psa_n);
-                rb_n = (in2 < ns) ? row_of(in2, psb_n) : ra_n;
-                prefetch_row(ra_n);
-                if (in2 < ns) prefetch_row(rb_n);
+                ra_n = row_at(in, psa_n);
+                rb_n = (in2 < ns) ? row_at(in2, psb_n) : ra_n;
             }
             double sa, sb;
             warp_np_score_reg2<IP, T>(qpd, xa, xb, M, qtail, rows + ra * (int64_t)d + offL + 8 * M,
@@ -1203,6 +1230,193 @@ cudaError_t launch_dense_select(const float* keys, int64_t nq, int64_t ncols, in
     cudaError_t e = cudaFuncSetAttribute(k_dense_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_dense_select<<<(unsigned)nq, DS_NT, smem, s>>>(keys, ncols, k, margin, cb);
+    return cudaGetLastError();
+}
+
+// IVF coarse quantizer, dense keys with per-chunk minima (MODE 3 epilogue:
+// mins[q][c] = min key of columns 32c..32c+31). One warp per query:
+//   1. U = kk-th smallest chunk minimum: kk columns have key <= U, so the
+//      kk-th smallest key K* <= U;
+//   2. only chunks whose minimum is <= U + margin can hold a key <= U + margin
+//      (typically ~kk of the 512 chunks of 16,384 centroids): their keys are
+//      read (one coalesced 128-byte load per chunk) and those <= U + margin
+//      kept in shared memory;
+//   3. K* = kk-th smallest of those, band = keys <= K* + margin (<= U + margin,
+//      so all of them were kept): the same margin band as k_dense_select
+//      (exact by construction), from ~4 % of the key bytes.
+// A candidate overflow falls back to a bitwise search over the whole row.
+namespace {
+constexpr int CS_WARPS = 4;
+constexpr int CS_MAXCH = 1024;   // chunks per row (ncols <= 32768)
+constexpr int CS_CAND = 512;     // keys <= U + margin held per query
+
+// kk-th smallest (1-based, kk <= n) of the orderable values v[0..n), one warp;
+// bits above the highest bit where lo and hi differ are common to every value
+__device__ __forceinline__ uint32_t warp_kth(const uint32_t* v, int n, unsigned kk, uint32_t lo, uint32_t hi,
+                                             int lane) {
+    const uint32_t diff = lo ^ hi;
+    if (!diff) return lo;
+    const int top = 31 - __clz(diff);
+    uint32_t res = lo & ~((top == 31 ? 0u : (2u << top)) - 1u);
+#pragma unroll 1
+    for (int b = top; b >= 0; --b) {
+        const uint32_t t = res | (1u << b);
+        unsigned c = 0;
+        for (int i = lane; i < n; i += 32) c += v[i] < t ? 1u : 0u;
+        c = __reduce_add_sync(VS_FULL, c);
+        if (c < kk) res = t;
+    }
+    return res;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(CS_WARPS * 32) k_coarse_select(const float* __restrict__ keys,
+                                                                 const float* __restrict__ mins, int64_t nq,
+                                                                 int64_t ncols, int k,
+                                                                 const float* __restrict__ margin, CandBuf cb) {
+    __shared__ uint32_t s_min[CS_WARPS][CS_MAXCH];
+    __shared__ uint16_t s_ch[CS_WARPS][CS_MAXCH];
+    __shared__ uint32_t s_ck[CS_WARPS][CS_CAND];
+    __shared__ uint32_t s_cp[CS_WARPS][CS_CAND];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * CS_WARPS + w;
+    if (q >= nq) return;   // warp-uniform; no block barriers below
+    const int n = (int)ncols;
+    const int nch = (n + 31) >> 5;
+    const unsigned kk = (unsigned)min(k, n);
+    const float* row = keys + q * ncols;
+    const float* mrow = mins + q * (int64_t)nch;
+    const float mq = margin[q];
+    uint32_t* vm = s_min[w];
+    uint16_t* ch = s_ch[w];
+    uint32_t* ck = s_ck[w];
+    uint32_t* cp = s_cp[w];
+    // 1. chunk minima
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = lane; i < nch; i += 32) {
+        const uint32_t u = f2o(__ldcs(mrow + i));
+        vm[i] = u;
+        lo = min(lo, u);
+        hi = max(hi, u);
+    }
+    lo = __reduce_min_sync(VS_FULL, lo);
+    hi = __reduce_max_sync(VS_FULL, hi);
+    __syncwarp();
+    const uint32_t U = warp_kth(vm, nch, kk, lo, hi, lane);
+    const uint32_t thr_u = f2o(__fadd_ru(o2f(U), mq));
+    // 2. chunks that can hold a key <= U + margin
+    int nc = 0;
+    for (int i0 = 0; i0 < nch; i0 += 32) {
+        const int i = i0 + lane;
+        const bool live = i < nch && vm[i] <= thr_u;
+        const unsigned b = __ballot_sync(VS_FULL, live);
+        if (live) ch[nc + __popc(b & lanemask_lt())] = (uint16_t)i;
+        nc += __popc(b);
+    }
+    __syncwarp();
+    // 3. their keys <= U + margin (four chunk loads in flight)
+    int ncand = 0;
+    bool ovf = false;
+    uint32_t clo = 0xffffffffu, chi = 0u;
+    for (int j0 = 0; j0 < nc && !ovf; j0 += 4) {
+        uint32_t u[4];
+        int col[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            col[h] = j0 + h < nc ? (int)ch[j0 + h] * 32 + lane : n;
+            u[h] = col[h] < n ? f2o(__ldcs(row + col[h])) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const bool live = col[h] < n && u[h] <= thr_u;
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            if (ncand + __popc(b) > CS_CAND) {
+                ovf = true;
+                break;
+            }
+            if (live) {
+                const int slot = ncand + __popc(b & lanemask_lt());
+                ck[slot] = u[h];
+                cp[slot] = (uint32_t)col[h];
+                clo = min(clo, u[h]);
+                chi = max(chi, u[h]);
+            }
+            ncand += __popc(b);
+        }
+    }
+    float* bk = cb.key + q * (int64_t)cb.C;
+    uint32_t* bp = cb.pos + q * (int64_t)cb.C;
+    int cnt = 0;
+    if (!ovf) {
+        __syncwarp();
+        clo = __reduce_min_sync(VS_FULL, clo);
+        chi = __reduce_max_sync(VS_FULL, chi);
+        const uint32_t kth = warp_kth(ck, ncand, kk, clo, chi, lane);
+        const uint32_t thr = f2o(__fadd_ru(o2f(kth), mq));
+        for (int i0 = 0; i0 < ncand; i0 += 32) {
+            const int i = i0 + lane;
+            const bool live = i < ncand && ck[i] <= thr;
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            const int slot = cnt + __popc(b & lanemask_lt());
+            if (live && slot < cb.C) {
+                bk[slot] = o2f(ck[i]);
+                bp[slot] = cp[i];
+            }
+            cnt += __popc(b);
+        }
+    } else {
+        // rare: more than CS_CAND keys within the margin of U; the whole row
+        // from global memory (bitwise search for K*, then the band)
+        uint32_t glo = 0xffffffffu, ghi = 0u;
+        for (int i = lane; i < n; i += 32) {
+            const uint32_t u = f2o(row[i]);
+            glo = min(glo, u);
+            ghi = max(ghi, u);
+        }
+        glo = __reduce_min_sync(VS_FULL, glo);
+        ghi = __reduce_max_sync(VS_FULL, ghi);
+        uint32_t res = glo;
+        if (glo != ghi) {
+            const int top = 31 - __clz(glo ^ ghi);
+            res = glo & ~((top == 31 ? 0u : (2u << top)) - 1u);
+            for (int b = top; b >= 0; --b) {
+                const uint32_t t = res | (1u << b);
+                unsigned c = 0;
+                for (int i = lane; i < n; i += 32) c += f2o(row[i]) < t ? 1u : 0u;
+                c = __reduce_add_sync(VS_FULL, c);
+                if (c < kk) res = t;
+            }
+        }
+        const uint32_t thr = f2o(__fadd_ru(o2f(res), mq));
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int i = i0 + lane;
+            const uint32_t u = i < n ? f2o(row[i]) : 0xffffffffu;
+            const bool live = i < n && u <= thr;
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            const int slot = cnt + __popc(b & lanemask_lt());
+            if (live && slot < cb.C) {
+                bk[slot] = o2f(u);
+                bp[slot] = (uint32_t)i;
+            }
+            cnt += __popc(b);
+        }
+    }
+    if (lane == 0) {
+        cb.cnt[q] = min(cnt, cb.C);
+        if (cnt > cb.C) cb.overflow[q] = 1;
+    }
+}
+
+bool coarse_select_ok(int64_t ncols, int k) {
+    const int64_t nch = (ncols + 31) / 32;
+    return nch <= CS_MAXCH && k >= 1 && k <= nch && k <= CS_CAND / 4;
+}
+
+cudaError_t launch_coarse_select(const float* keys, const float* mins, int64_t nq, int64_t ncols, int k,
+                                 const float* margin, const CandBuf& cb, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    k_coarse_select<<<(unsigned)((nq + CS_WARPS - 1) / CS_WARPS), CS_WARPS * 32, 0, s>>>(keys, mins, nq, ncols, k,
+                                                                                        margin, cb);
     return cudaGetLastError();
 }
 

@@ -118,6 +118,11 @@ struct Params {
     const int64_t* pair_base;       // MODE 2 with chunks: first flat buffer of each pair (nullable)
     float* keys_out;                // MODE 3: dense approximate keys [nq][keys_ld]
     int64_t keys_ld;
+    // MODE 0/3 operand type: 0 bf16, 1 fp16 (power-of-two scaled, see k_stage_queries)
+    int f16;
+    const float* kinv;              // nullable: [nq] 2^-(query scale + row scale) of the fp16 operands
+    float* mins_out;                // MODE 3, nullable: min key of every 32-column chunk [nq][mins_ld]
+    int64_t mins_ld;
 };
 
 // one work item: A tile rows [a_row, a_row + QTILE), B tiles of BN rows from
@@ -271,6 +276,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 // instruction descriptor: kind::f16, A/B = BF16, D = F32, K-major both, M=128, N=256
 __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+// the same with A/B = F16 (a_format = b_format = 0)
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 1) {
         // ===== MMA issuer (single thread; rank 0 of a pair) =====
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN);
+            const uint32_t idesc = p.f16 ? idesc_f16(PAIR ? 2 * BM : BM, BN) : idesc_bf16(PAIR ? 2 * BM : BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t tcount = 0;
@@ -564,6 +573,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const Item item = decode_item<MODE, QTILE>(p, it);
             const int64_t q = item.a_row + (int64_t)rank * BM + row;
             float* krow = p.keys_out + (q < p.nq ? q : 0) * p.keys_ld;
+            // key = ||x||^2 - 2 q.x (or -q.x) with q.x = acc x 2^-(scales): exact factor
+            const float ks = (p.kinv && q < p.nq) ? __ldg(p.kinv + q) : 1.f;
+            const float cmul = IP ? -ks : -2.f * ks;
             for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
                 const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                 const int64_t r0 = item.b_row0 + t * BN;
@@ -593,7 +605,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float a = __uint_as_float(r[j]);
-                        kv[j] = IP ? -a : fmaf(-2.f, a, xw[ch * 32 + j]);
+                        kv[j] = IP ? a * cmul : fmaf(cmul, a, xw[ch * 32 + j]);
+                    }
+                    if (q < p.nq && p.mins_out && cb0 < ncols) {
+                        float mn = __int_as_float(0x7f800000);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (cb0 + j < ncols) mn = fminf(mn, kv[j]);
+                        p.mins_out[q * p.mins_ld + ((r0 + cb0) >> 5)] = mn;
                     }
                     if (q < p.nq) {
                         float* dst = krow + r0 + cb0;
@@ -686,6 +705,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             float* ckey = p.cb.key + cbase;
             uint32_t* cpos = p.cb.pos + cbase;
             const float qmargin = qv ? p.margin[q] : 0.f;
+            const float ks = (MODE != 2 && p.kinv && qv) ? __ldg(p.kinv + q) : 1.f;
+            const float cmul = IP ? -ks : -2.f * ks;   // exact: a power of two
             int cnt = 0;
             int ovf = 0;
             // geometric compaction schedule, checked once per tile before any TMEM
@@ -779,7 +800,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float a = __uint_as_float(cur[j]);
-                        kk[j] = IP ? -a : fmaf(-2.f, a, xv[j]);
+                        kk[j] = IP ? a * cmul : fmaf(cmul, a, xv[j]);
                         mask |= (kk[j] <= tau ? 1u : 0u) << j;
                     }
                     mask &= valid;
@@ -894,22 +915,77 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // (Cauchy-Schwarz on the error vectors), which is ~1.7x tighter than the
 // worst-case 2^-8 ||q|| ||x|| bound and still rigorous.
 
-// queries fp32 -> bf16 (round to nearest even), row stride dp; warp per query
-__global__ void k_stage_queries(const float* __restrict__ q, int64_t nq, int d, int dp,
-                                __nv_bfloat16* __restrict__ out, float2* __restrict__ qerr) {
+// 16-bit operand types: bf16 (8-bit significand) or fp16 (11-bit: 8x smaller
+// rounding error, hence an ~6x narrower margin band and fewer phase-B
+// survivors). fp16's range is small, so fp16 operands are scaled by powers of
+// two: every row by 2^ex with 2^ex max||x|| < 2^14 (column-wide), every query
+// by its own 2^eq with 2^eq ||q|| < 2^14. Both scalings are exact, elements
+// stay below 2^14 < 65504, and the epilogue multiplies the accumulator by
+// 2^-(eq+ex) (exact). Rounding errors are tracked in unscaled units.
+template <typename O> struct Op16;
+template <> struct Op16<__nv_bfloat16> {
+    static __device__ __forceinline__ uint32_t pack(float a, float b, float2& back) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        back = __bfloat1622float2(h);
+        return *reinterpret_cast<const uint32_t*>(&h);
+    }
+    static __device__ __forceinline__ __nv_bfloat16 one(float v, float& back) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        back = __bfloat162float(h);
+        return h;
+    }
+};
+template <> struct Op16<__half> {
+    static __device__ __forceinline__ uint32_t pack(float a, float b, float2& back) {
+        const __half2 h = __floats2half2_rn(a, b);
+        back = __half22float2(h);
+        return *reinterpret_cast<const uint32_t*>(&h);
+    }
+    static __device__ __forceinline__ __half one(float v, float& back) {
+        const __half h = __float2half_rn(v);
+        back = __half2float(h);
+        return h;
+    }
+};
+// 2^e with 2^e sqrt(norm2) < 2^14 (1 for a zero or non-finite norm)
+__device__ __forceinline__ float pow2_scale(float norm2) {
+    const float n = sqrtf(norm2);
+    if (!(n > 0.f) || !isfinite(n)) return 1.f;
+    int e;
+    frexpf(n * 1.001f, &e);   // n * 1.001 < 2^e
+    return ldexpf(1.f, max(-120, min(120, 14 - e)));
+}
+
+// queries fp32 -> 16-bit (round to nearest even), row stride dp; warp per query.
+// fp16 (xs != nullptr): the query's own power-of-two scale, and kinv[q] =
+// 2^-(eq + ex) with ex the rows' scale (from their max norm xs).
+template <typename O>
+__global__ void k_stage_queries(const float* __restrict__ q, int64_t nq, int d, int dp, O* __restrict__ out,
+                                float2* __restrict__ qerr, const unsigned* __restrict__ xs,
+                                float* __restrict__ kinv) {
     const int lane = threadIdx.x & 31;
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const float sx = xs ? pow2_scale(__uint_as_float(*xs)) : 1.f;
     for (; w < nq; w += nw) {
+        const float* src = q + w * (int64_t)d;
+        float sq = 1.f;
+        if (xs) {
+            float n2 = 0.f;
+            for (int c = lane; c < d; c += 32) n2 = fmaf(src[c], src[c], n2);
+            sq = pow2_scale(warp_sumf(n2));
+            if (lane == 0) kinv[w] = 1.f / (sq * sx);
+        }
+        const float iq = 1.f / sq;
         float sn = 0.f, se = 0.f;
         for (int c = lane; c < dp; c += 32) {
-            const float v = c < d ? q[w * (int64_t)d + c] : 0.f;
-            const __nv_bfloat16 b = __float2bfloat16_rn(v);
-            const float vb = __bfloat162float(b);
+            const float v = c < d ? src[c] : 0.f;
+            float vb;
+            out[w * (int64_t)dp + c] = Op16<O>::one(v * sq, vb);
+            vb *= iq;
             const float e = vb - v;  // exact in fp32 (Sterbenz-free: |e| << |v|, same binade)
             sn = fmaf(vb, vb, sn);
             se = fmaf(e, e, se);
-            out[w * (int64_t)dp + c] = b;
         }
         sn = warp_sumf(sn);
         se = warp_sumf(se);
@@ -932,44 +1008,47 @@ __global__ void k_stage_pair_queries(const float* __restrict__ q, const int32_t*
     }
 }
 
-template <typename T>
+template <typename T, typename O>
 __global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict__ sel, int64_t nsel, int d,
-                             int dp, const float* __restrict__ norms, __nv_bfloat16* __restrict__ out,
-                             float* __restrict__ xn, unsigned* __restrict__ xmax2) {
+                             int dp, const float* __restrict__ norms, O* __restrict__ out,
+                             float* __restrict__ xn, unsigned* __restrict__ xmax2,
+                             const unsigned* __restrict__ xs = nullptr) {
     const int lane = threadIdx.x & 31;
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // fp16 operands: the column-wide power-of-two scale (k_stage_queries)
+    const float sx = xs ? pow2_scale(__uint_as_float(*xs)) : 1.f;
+    const float ix = 1.f / sx;
     float mb = 0.f, me = 0.f;
     for (; w < nsel; w += nw) {
         const int64_t r = sel ? sel[w] : w;
         const T* src = x + r * (int64_t)d;
-        __nv_bfloat16* dst = out + w * (int64_t)dp;
+        O* dst = out + w * (int64_t)dp;
         float sn = 0.f, se = 0.f;
         if (sizeof(T) == 4 && (d % 4) == 0 && (dp % 4) == 0) {
             for (int c = lane * 4; c < dp; c += 128) {
                 const float4 v = (c < d) ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) + c)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-                const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-                const __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
-                const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+                float2 fa, fb;
+                uint2 u;
+                u.x = Op16<O>::pack(v.x * sx, v.y * sx, fa);
+                u.y = Op16<O>::pack(v.z * sx, v.w * sx, fb);
+                fa.x *= ix; fa.y *= ix; fb.x *= ix; fb.y *= ix;
                 const float e0 = fa.x - v.x, e1 = fa.y - v.y, e2 = fb.x - v.z, e3 = fb.y - v.w;
                 sn = fmaf(fa.x, fa.x, sn); sn = fmaf(fa.y, fa.y, sn);
                 sn = fmaf(fb.x, fb.x, sn); sn = fmaf(fb.y, fb.y, sn);
                 se = fmaf(e0, e0, se); se = fmaf(e1, e1, se); se = fmaf(e2, e2, se); se = fmaf(e3, e3, se);
-                uint2 u;
-                u.x = *reinterpret_cast<const uint32_t*>(&a);
-                u.y = *reinterpret_cast<const uint32_t*>(&b);
                 *reinterpret_cast<uint2*>(dst + c) = u;
             }
         } else {
             for (int c = lane; c < dp; c += 32) {
                 const float v = c < d ? ld_elem(src + c) : 0.f;
-                const __nv_bfloat16 b = __float2bfloat16_rn(v);
-                const float vb = __bfloat162float(b);
+                float vb;
+                dst[c] = Op16<O>::one(v * sx, vb);
+                vb *= ix;
                 const float e = vb - v;
                 sn = fmaf(vb, vb, sn);
                 se = fmaf(e, e, se);
-                dst[c] = b;
             }
         }
         sn = warp_sumf(sn);
@@ -1038,12 +1117,12 @@ bool get_encode() {
     return true;
 }
 
-bool make_map(CUtensorMap* map, const void* gaddr, int64_t rows, int d, int dp, int box_rows) {
+bool make_map(CUtensorMap* map, const void* gaddr, int64_t rows, int d, int dp, int box_rows, bool f16 = false) {
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)std::max<int64_t>(rows, 1)};
     cuuint64_t strides[1] = {(cuuint64_t)dp * 2};
     cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(gaddr), dims, strides, box,
+    CUresult r = g_encode(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(gaddr), dims, strides, box,
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -1093,6 +1172,13 @@ bool tc_supported(int d, int dtype, int ip) {
     return d >= 8 && get_encode();
 }
 
+// fp16 operands for float32 rows whose max norm is known (the power-of-two
+// scaling needs it); VS_TC_BF16=1 keeps bf16 (A/B runs)
+bool use_f16(int dtype, const unsigned* xmax) {
+    static const bool bf16_env = getenv("VS_TC_BF16") != nullptr && getenv("VS_TC_BF16")[0] == '1';
+    return dtype == VS_DTYPE_F32 && xmax != nullptr && !bf16_env;
+}
+
 bool tc_profitable(int64_t nq, int64_t nsel, int d) {
     return nq >= 64 && (double)nq * (double)nsel * (double)d >= 4.0e9;
 }
@@ -1116,6 +1202,10 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     float2* qerr = nullptr;
     unsigned* tau_g = nullptr;
     unsigned* xmax2 = nullptr;
+    float* kinv = nullptr;
+    // float32 rows: fp16 operands (8x smaller rounding error than bf16, same
+    // tensor throughput); bf16-stored rows stay their own exact operand
+    const bool f16 = use_f16(dtype, xmax);
     CKS(arena_alloc(ctx, (size_t)nq * dp, &qa));
     CKS(arena_alloc(ctx, (size_t)nsel * dp, &xb));
     CKS(arena_alloc(ctx, (size_t)nsel, &xn));
@@ -1123,22 +1213,30 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     CKS(arena_alloc(ctx, (size_t)nq, &qerr));
     CKS(arena_alloc(ctx, (size_t)nq, &tau_g));
     CKS(arena_alloc(ctx, 2, &xmax2));
+    if (f16) CKS(arena_alloc(ctx, (size_t)nq, &kinv));
     {
         KTimer kt(ctx, VS_K_STAGE);
         CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));
         // rows first: they do not need the queries, whose host->device copy may
         // still be in flight on the copy stream (sp.q_ready)
         const unsigned blocks = (unsigned)std::min<int64_t>((nsel * 32 + 255) / 256, 148 * 64);
-        if (dtype == VS_DTYPE_F32)
-            tc::k_stage_rows<float><<<blocks, 256, 0, st>>>((const float*)sp.X, sp.sel, nsel, d, dp, sp.xnorm, xb,
-                                                            sp.ip ? nullptr : xn, xmax2);
+        if (f16)
+            tc::k_stage_rows<float, __half><<<blocks, 256, 0, st>>>((const float*)sp.X, sp.sel, nsel, d, dp,
+                                                                    sp.xnorm, (__half*)xb, sp.ip ? nullptr : xn,
+                                                                    xmax2, xmax);
+        else if (dtype == VS_DTYPE_F32)
+            tc::k_stage_rows<float, __nv_bfloat16><<<blocks, 256, 0, st>>>((const float*)sp.X, sp.sel, nsel, d, dp,
+                                                                           sp.xnorm, xb, sp.ip ? nullptr : xn, xmax2);
         else
-            tc::k_stage_rows<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)sp.X, sp.sel, nsel, d,
-                                                                    dp, sp.xnorm, xb, sp.ip ? nullptr : xn, xmax2);
+            tc::k_stage_rows<__nv_bfloat16, __nv_bfloat16><<<blocks, 256, 0, st>>>(
+                (const __nv_bfloat16*)sp.X, sp.sel, nsel, d, dp, sp.xnorm, xb, sp.ip ? nullptr : xn, xmax2);
         CK(cudaGetLastError());
         if (sp.q_ready) CK(cudaStreamWaitEvent(st, sp.q_ready, 0));
-        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-            sp.Q, nq, d, dp, qa, qerr);
+        const unsigned qblocks = (unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16);
+        if (f16)
+            tc::k_stage_queries<__half><<<qblocks, 256, 0, st>>>(sp.Q, nq, d, dp, (__half*)qa, qerr, xmax, kinv);
+        else
+            tc::k_stage_queries<__nv_bfloat16><<<qblocks, 256, 0, st>>>(sp.Q, nq, d, dp, qa, qerr, nullptr, nullptr);
         CK(cudaGetLastError());
         tc::k_tc_margins<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qerr, nq, d, xmax, xmax2, sp.ip, margin);
         CK(cudaGetLastError());
@@ -1191,9 +1289,11 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     CK(cudaMemsetAsync(c.overflow, 0, nq * sizeof(int), st));
 
     CUtensorMap ma, mb;
-    if (!make_map(&ma, qa, nq, d, dp, tc::BM) || !make_map(&mb, xb, nsel, d, dp, pair ? tc::BN / 2 : tc::BN))
+    if (!make_map(&ma, qa, nq, d, dp, tc::BM, f16) || !make_map(&mb, xb, nsel, d, dp, pair ? tc::BN / 2 : tc::BN, f16))
         return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    tc::Params pr;
+    tc::Params pr{};
+    pr.f16 = f16 ? 1 : 0;
+    pr.kinv = kinv;
     pr.nq = nq;
     pr.d = d;
     pr.kblocks = (d + tc::BK - 1) / tc::BK;
@@ -1275,11 +1375,11 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
         const int64_t m = std::min(chunk, n - r0);
         const unsigned blocks = (unsigned)std::min<int64_t>((m * 32 + 255) / 256, 148 * 64);
         if (dtype == VS_DTYPE_F32)
-            tc::k_stage_rows<float><<<blocks, 256, 0, st>>>((const float*)x + r0 * (int64_t)d, nullptr, m, d, dp,
-                                                            nullptr, xb, nullptr, junk);
+            tc::k_stage_rows<float, __nv_bfloat16><<<blocks, 256, 0, st>>>((const float*)x + r0 * (int64_t)d, nullptr,
+                                                                           m, d, dp, nullptr, xb, nullptr, junk);
         else
-            tc::k_stage_rows<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)x + r0 * (int64_t)d,
-                                                                    nullptr, m, d, dp, nullptr, xb, nullptr, junk);
+            tc::k_stage_rows<__nv_bfloat16, __nv_bfloat16><<<blocks, 256, 0, st>>>(
+                (const __nv_bfloat16*)x + r0 * (int64_t)d, nullptr, m, d, dp, nullptr, xb, nullptr, junk);
         CK(cudaGetLastError());
         CUtensorMap ma;
         if (!make_map(&ma, xb, m, d, dp, tc::BM)) return set_err(VS_ERR_CUDA, "tensor map (rows)");
@@ -1308,7 +1408,8 @@ int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* 
     using namespace vs_internal;
     const int dp = (d + 7) / 8 * 8;
     const unsigned blocks = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 148 * 64);
-    tc::k_stage_rows<float><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, out, nullptr, junk);
+    tc::k_stage_rows<float, __nv_bfloat16><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, out, nullptr,
+                                                                            junk);
     CK(cudaGetLastError());
     ctx->stats[VS_STAT_LAUNCHES] += 1;
     return VS_OK;
@@ -1320,7 +1421,7 @@ int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* 
 // its columns (the centroids) are few enough that the whole key matrix of a
 // query chunk is cheaper to write and select from than candidate buffers.
 int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X, int64_t ncols,
-                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin) {
+                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin, float* mins) {
     using namespace vs_internal;
     if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cudaStream_t st = ctx->stream;
@@ -1329,19 +1430,30 @@ int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X
     float* xn = nullptr;
     float2* qerr = nullptr;
     unsigned* xmax2 = nullptr;
+    float* kinv = nullptr;
+    const bool f16 = use_f16(VS_DTYPE_F32, xmax);
     CKS(arena_alloc(ctx, (size_t)nq * dp, &qa));
     CKS(arena_alloc(ctx, (size_t)ncols * dp, &xb));
     CKS(arena_alloc(ctx, (size_t)ncols, &xn));
     CKS(arena_alloc(ctx, (size_t)nq, &qerr));
     CKS(arena_alloc(ctx, 2, &xmax2));
+    if (f16) CKS(arena_alloc(ctx, (size_t)nq, &kinv));
     {
         KTimer kt(ctx, VS_K_STAGE);
         CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));
         const unsigned blocks = (unsigned)std::min<int64_t>((ncols * 32 + 255) / 256, 148 * 64);
-        tc::k_stage_rows<float><<<blocks, 256, 0, st>>>(X, nullptr, ncols, d, dp, xnorm, xb, ip ? nullptr : xn, xmax2);
-        CK(cudaGetLastError());
-        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-            Q, nq, d, dp, qa, qerr);
+        const unsigned qblocks = (unsigned)std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16);
+        if (f16) {
+            tc::k_stage_rows<float, __half><<<blocks, 256, 0, st>>>(X, nullptr, ncols, d, dp, xnorm, (__half*)xb,
+                                                                    ip ? nullptr : xn, xmax2, xmax);
+            CK(cudaGetLastError());
+            tc::k_stage_queries<__half><<<qblocks, 256, 0, st>>>(Q, nq, d, dp, (__half*)qa, qerr, xmax, kinv);
+        } else {
+            tc::k_stage_rows<float, __nv_bfloat16><<<blocks, 256, 0, st>>>(X, nullptr, ncols, d, dp, xnorm, xb,
+                                                                           ip ? nullptr : xn, xmax2);
+            CK(cudaGetLastError());
+            tc::k_stage_queries<__nv_bfloat16><<<qblocks, 256, 0, st>>>(Q, nq, d, dp, qa, qerr, nullptr, nullptr);
+        }
         CK(cudaGetLastError());
         tc::k_tc_margins<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(qerr, nq, d, xmax, xmax2, ip, margin);
         CK(cudaGetLastError());
@@ -1367,9 +1479,11 @@ int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X
     const int64_t per = (ntiles + best_s - 1) / best_s;
     const int nsplit = (int)((ntiles + per - 1) / per);
     CUtensorMap ma, mb;
-    if (!make_map(&ma, qa, nq, d, dp, tc::BM) || !make_map(&mb, xb, ncols, d, dp, pair ? tc::BN / 2 : tc::BN))
+    if (!make_map(&ma, qa, nq, d, dp, tc::BM, f16) || !make_map(&mb, xb, ncols, d, dp, pair ? tc::BN / 2 : tc::BN, f16))
         return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     tc::Params pr{};
+    pr.f16 = f16 ? 1 : 0;
+    pr.kinv = kinv;
     pr.nq = nq;
     pr.d = d;
     pr.kblocks = (d + tc::BK - 1) / tc::BK;
@@ -1382,6 +1496,8 @@ int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X
     pr.ip = ip;
     pr.keys_out = keys;
     pr.keys_ld = ncols;
+    pr.mins_out = mins;
+    pr.mins_ld = (ncols + 31) / 32;
     const int64_t items = (int64_t)qtiles * nsplit;
     const unsigned units = (unsigned)std::min<int64_t>(items, sms);
     const unsigned grid = pair ? 2 * units : units;
@@ -1419,8 +1535,8 @@ int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
         tc::k_stage_pair_queries<<<(unsigned)std::min<int64_t>((a.npairs * 32 + 255) / 256, 148 * 32), 256, 0, st>>>(
             a.Q, a.pair_codes, a.npairs, a.nprobe, d, dp, qp);
         CK(cudaGetLastError());
-        tc::k_stage_queries<<<(unsigned)std::min<int64_t>((a.nq * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-            a.Q, a.nq, d, dp, qa, qerr);
+        tc::k_stage_queries<__nv_bfloat16><<<(unsigned)std::min<int64_t>((a.nq * 32 + 255) / 256, 148 * 16), 256, 0,
+                                             st>>>(a.Q, a.nq, d, dp, qa, qerr, nullptr, nullptr);
         CK(cudaGetLastError());
         // bf16-stored rows are their own tensor-core operand: ||x~|| = ||x||, dx = 0
         CK(cudaMemsetAsync(xmax2, 0, 2 * sizeof(unsigned), st));

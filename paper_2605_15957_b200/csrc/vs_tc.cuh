@@ -16,12 +16,15 @@ namespace bn128 {
 int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax, int cshift,
                 CandBuf* cb, bool* exhaustive, int timer_class);
 int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X, int64_t ncols,
-                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin);
+                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin,
+                  float* mins = nullptr);
 }
 inline namespace bn256 {
 
 // whether the tensor-core phase A handles this shape / dtype / metric
 bool tc_supported(int d, int dtype, int ip);
+// whether phase A stages fp16 operands (float32 rows with a known max norm)
+bool use_f16(int dtype, const unsigned* xmax);
 // heuristic: enough work to amortise the bf16 staging pass
 bool tc_profitable(int64_t nq, int64_t nsel, int d);
 // runs phase A on the tensor cores; fills `cb` (allocated by the callee from
@@ -40,7 +43,8 @@ int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* 
 // dense approximate keys [nq][ncols] of float32 rows X on the tensor cores
 // (MODE 3; the IVF coarse quantizer) and their per-query margins
 int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X, int64_t ncols,
-                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin);
+                  const float* xnorm, const unsigned* xmax, int ip, float* keys, float* margin,
+                  float* mins = nullptr);
 
 // IVF list-major phase A on the tensor cores (bf16 list-contiguous payload):
 // pairs already grouped by list into units of <= 128 pairs

@@ -128,3 +128,36 @@ def test_coarse_quantizer_modes_equal_oracle(metric, coarse):
     assert np.array_equal(got.probes, ref.probes)
     assert np.array_equal(got.data_row, ref.data_row)
     assert np.array_equal(got.distance, ref.distance)
+
+
+@pytest.mark.parametrize("full_select", [False, True])
+@pytest.mark.parametrize("dups", [0, 700])
+def test_coarse_dense_select_variants(monkeypatch, full_select, dups):
+    """Dense coarse keys: the chunk-minima select (k_coarse_select) and the
+    whole-row select give the reference's probes; 700 identical centroids put
+    more keys inside the margin than the chunk select holds (its whole-row
+    fallback) and than the band buffer holds (overflow re-run)."""
+    if full_select:
+        monkeypatch.setenv("VS_COARSE_FULLSELECT", "1")
+    rng = np.random.default_rng(5 + dups)
+    n, d, nlist = 30000, 64, 3000
+    data = rng.standard_normal((n, d)).astype(np.float32)
+    cen = data[np.sort(rng.choice(n, nlist, replace=False))].copy()
+    if dups:
+        cen[100:100 + dups] = cen[99]
+    assign = np.argmin(O.pairwise_sq_l2_fast(data, cen), axis=1)
+    parts = [np.flatnonzero(assign == c).astype(np.int64) for c in range(nlist)]
+    payload = [data[p] for p in parts]
+    q = rng.standard_normal((300, d)).astype(np.float32)
+    q[:20] = cen[99] + 1e-3 * rng.standard_normal((20, d)).astype(np.float32)
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_COARSE, 2)
+    try:
+        idx = vs.IvfIndex(nlist, d, n, "squared_l2", "owning", cen, parts, payload)
+        got = idx.search(q, vs.SearchParams(k=5, nprobe=48))
+    finally:
+        ctx.set_option(N.OPT_COARSE, 0)
+    ref = O.ivf_search(q, cen, parts, lambda c: payload[c], 48, 5)
+    assert np.array_equal(got.probes, ref.probes)
+    assert np.array_equal(got.data_row, ref.data_row)
+    assert np.array_equal(got.distance, ref.distance)

@@ -139,3 +139,22 @@ def test_adversarial_cancellation(tc_kernel, metric):
     nt = vs.enn_search(q, data, vs.SearchParams(k=25), metric=metric)
     assert tc_kernel.stats()[N.STAT_LAST_ENN_KERNEL] == 2
     assert_same(nt, O.enn_search(q, data, 25, metric))
+
+
+@pytest.mark.parametrize("scale", [1e-15, 1e-6, 3e4, 1e12])
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+def test_tc_fp16_operand_scaling(tc_kernel, scale, metric):
+    """float32 rows run as power-of-two-scaled fp16 operands: magnitudes far
+    outside fp16's range (overflow above 65504, subnormals below 6e-5) must
+    still give the reference's exact answer, and mixed query magnitudes each
+    get their own scale."""
+    rng = np.random.default_rng(int(np.log10(scale)) + 50)
+    data = (rng.standard_normal((6000, 96)) * scale).astype(np.float32)
+    q = (rng.standard_normal((140, 96)) * scale).astype(np.float32)
+    q[::7] *= np.float32(1e3)
+    q[3] = 0.0
+    data[5] = 0.0
+    mask = rng.random(6000) < 0.5
+    nt = vs.enn_search(q, data, vs.SearchParams(k=12), metric=metric, row_filter=mask)
+    assert N.Context.get().stats()[N.STAT_LAST_ENN_KERNEL] == 2
+    assert_same(nt, O.enn_filtered(q, data, mask, 12, metric))
