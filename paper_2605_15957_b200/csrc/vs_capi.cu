@@ -336,6 +336,7 @@ int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bo
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_pos));
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_key));
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_id));
+    CKS(arena_alloc(ctx, (size_t)job.nq, &rp.s_count));
     rp.out_ids = job.out_ids;
     rp.out_dist = job.out_dist;
     rp.out_ids32 = job.out_ids32;
@@ -1773,7 +1774,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         if (lmajor && job.pbits && sel_env && v->n_total < (int64_t)UINT32_MAX) {
             // filtered: pre-selected rows per list, one round trip per unit (vs_ivf_sel.cu)
             IvfGroups gr;
-            CKS(ivf_group(ctx, job, vs::kSelUnitPairs, &gr));
+            CKS(ivf_group(ctx, job, vs::kIvfLmQT, &gr));
             CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
             vs::IvfSelLaunch a;
             a.Q = job.q;
@@ -1798,6 +1799,9 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
             CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.lsel64));
             CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.sel_off));
             CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(v->n_total, 1), &a.spos));
+            char* recs = nullptr;
+            CKS(arena_alloc(ctx, (size_t)gr.max_units * vs::kIvfSelRecBytes, &recs));
+            a.recs = recs;
             a.tmp_bytes = vs::ivf_sel_temp_bytes(v->nlist);
             char* tmp = nullptr;
             CKS(arena_alloc(ctx, a.tmp_bytes, &tmp));
@@ -1883,6 +1887,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_pos));
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_key));
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_id));
+    CKS(arena_alloc(ctx, (size_t)job.nq, &rp.s_count));
     rp.out_ids = job.out_ids;
     rp.out_dist = job.out_dist;
     rp.out_ids32 = nullptr;

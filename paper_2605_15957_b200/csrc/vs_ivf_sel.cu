@@ -1,21 +1,26 @@
 // Phase A of the FILTERED IVF search, list-major over pre-selected rows.
 //
 // With a selective filter (config 3: 1 %), a probed list of ~610 rows holds
-// ~6 selected rows and is probed by ~20 queries: per list, a handful of rows
-// against a few dozen queries. The work is tiny (2 GFMA per batch); what
-// costs is latency, so:
+// ~6 selected rows, and the scan is a stream of tiny, independent units:
+// (list, <= 8 (query, probe) pairs) x (selected rows of the list). The
+// list-major kernel (vs_ivf_lmajor.cu) spent its time on dependent global
+// round trips per unit (work ticket, unit, pair codes, queries, bitmap words,
+// selected positions, rows). Here every unit needs ONE:
 //   1. once per search, the selected payload positions of every list are
 //      compacted in list order (k_list_sel_positions: one warp per list over
-//      the permuted bitmap);
-//   2. a work unit is a whole list (all its pairs, <= kSelUnitPairs): its
-//      selected rows are staged ONCE into shared memory (cp.async, one warp
-//      per row, 8 rows per chunk) while the previous chunk is scored - a
-//      double buffer across chunks and units;
-//   3. each warp takes the unit's pairs in turn, its query in registers (the
-//      next pair's query loaded while the current one is scored), one FFMA
-//      per element and row, an 8-row transpose-reduction, and appends the
-//      keys ||x||^2 - 2 q.x (dot form; error within eps_simt) to the pair's
-//      candidate buffer, which only this warp touches during the unit.
+//      the permuted bitmap), and every unit gets a 128-byte record with its
+//      list, pair codes, selected-row count and first 16 positions
+//      (k_make_recs);
+//   2. a CTA walks its units in a fixed stride (no work-counter atomics); the
+//      record of its NEXT unit is loaded while the current one is scored, so
+//      at the top of a unit the row positions and the queries are known: the
+//      selected rows (cp.async, 16 bytes, coalesced) and the unit's queries
+//      (into registers) are requested together and arrive in one round trip;
+//   3. scoring and candidate appends follow the list-major kernel: two
+//      queries per warp held in registers, staged rows from shared memory,
+//      fp32 (error bound eps_simt), one butterfly transpose-
+//      reduction per chunk, per-pair candidate buffers; the
+//      key is the dot form ||x||^2 - 2 q.x (one FFMA per element and query).
 // Reference: IvfIndex.search, vecindex.py:230-258, with the filtered
 // extension rows = rows[mask[rows]].
 #include <cub/cub.cuh>
@@ -26,11 +31,24 @@
 namespace vs {
 
 namespace {
-constexpr int NT = 256;
+constexpr int NT = 128;
 constexpr int NW = NT / 32;
-constexpr int RS = 8;          // staged rows per chunk (one warp stages one row)
+constexpr int QT = kIvfLmQT;   // pairs per unit: two per warp
+constexpr int RS = 8;          // staged rows per chunk
 constexpr int TMAX = kIvfLmDMax / 128;
-static_assert(RS == NW, "one staging warp per row");
+constexpr int RPOS = 15;       // row positions carried in a unit record
+static_assert(QT == 2 * NW, "two query slots per warp");
+
+// 128-byte unit record: the pairs' queries and probe ranks pre-split (no
+// integer division in the scan), the first RPOS selected row positions
+struct __align__(16) UnitRec {
+    int32_t list, np, nsel, first_pair;
+    uint32_t sel_off;
+    int32_t q[QT];
+    uint16_t sub[QT];
+    uint32_t pos[RPOS];
+};
+static_assert(sizeof(UnitRec) == 128, "one 128-byte record per unit");
 
 template <typename T>
 struct V4;
@@ -48,16 +66,14 @@ struct V4<__nv_bfloat16> {
     }
 };
 
-// v[r] (r < 8) partial sums per lane -> lanes 4r..4r+3 hold the warp total of
-// row r (r = (lane >> 2) & 7): three halving exchanges, then two folds
-__device__ __forceinline__ float transpose_reduce8(float (&v)[8], int lane) {
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 #pragma unroll
-    for (int s = 0; s < 3; ++s) {
+    for (int s = 0; s < 4; ++s) {
         const int o = 16 >> s;
-        const int n = 8 >> s;
+        const int n = 16 >> s;
         const bool upper = (lane & o) != 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
             if (i < n / 2) {
                 const float send = upper ? v[i] : v[i + n / 2];
                 const float keep = upper ? v[i + n / 2] : v[i];
@@ -65,8 +81,7 @@ __device__ __forceinline__ float transpose_reduce8(float (&v)[8], int lane) {
             }
         }
     }
-    float t = v[0] + __shfl_xor_sync(VS_FULL, v[0], 2);
-    return t + __shfl_xor_sync(VS_FULL, t, 1);
+    return v[0] + __shfl_xor_sync(VS_FULL, v[0], 1);
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -121,6 +136,36 @@ __global__ void k_list_sel_positions(const int64_t* __restrict__ list_off, int n
         }
     }
 }
+
+__global__ void k_make_recs(const int4* __restrict__ units, const int32_t* __restrict__ n_units, int64_t max_units,
+                            const int32_t* __restrict__ pair_codes, int nprobe, const int32_t* __restrict__ lsel,
+                            const int64_t* __restrict__ sel_off, const uint32_t* __restrict__ spos,
+                            UnitRec* __restrict__ recs) {
+    const int nu = *n_units;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < max_units && u < nu;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int4 un = units[u];
+        UnitRec r;
+        r.list = un.x;
+        r.np = un.z;
+        r.first_pair = un.y;
+        r.nsel = lsel[un.x];
+        r.sel_off = (uint32_t)sel_off[un.x];
+#pragma unroll
+        for (int s = 0; s < QT; ++s) {
+            const int code = s < un.z ? pair_codes[un.y + s] : 0;
+            r.q[s] = code / nprobe;
+            r.sub[s] = (uint16_t)(code % nprobe);
+        }
+#pragma unroll
+        for (int i = 0; i < RPOS; ++i) r.pos[i] = i < r.nsel ? spos[r.sel_off + i] : 0u;
+        recs[u] = r;
+    }
+}
+
+struct SelSmem {
+    UnitRec rec[2];
+};
 }  // namespace
 
 struct IvfSelParams {
@@ -129,11 +174,8 @@ struct IvfSelParams {
     int d, dp;
     const void* payload;
     int nprobe;
-    const int4* units;          // (list, first pair, pairs, 0), grouped by list
+    const UnitRec* recs;
     const int32_t* n_units;
-    const int32_t* pair_codes;  // q * nprobe + probe rank
-    const int32_t* lsel;        // selected rows per list
-    const int64_t* sel_off;
     const uint32_t* spos;
     const float* pnorm;
     const float* margin;
@@ -143,9 +185,10 @@ struct IvfSelParams {
 };
 
 template <typename T, bool IP>
-__global__ void __launch_bounds__(NT, 2) k_ivf_scan_sel(IvfSelParams p) {
+__global__ void __launch_bounds__(NT, 4) k_ivf_scan_sel(IvfSelParams p) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    T* xs = reinterpret_cast<T*>(smraw);   // [2][RS][dp]
+    SelSmem& S = *reinterpret_cast<SelSmem*>(smraw);
+    T* xs = reinterpret_cast<T*>(smraw + ((sizeof(SelSmem) + 127) & ~size_t(127)));   // [RS][dp]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = p.d, dp = p.dp, nt = dp / 128;
     const T* payload = reinterpret_cast<const T*>(p.payload);
@@ -153,124 +196,141 @@ __global__ void __launch_bounds__(NT, 2) k_ivf_scan_sel(IvfSelParams p) {
     const int n_units = *p.n_units;
     const int row_bytes = d * (int)sizeof(T);
     const bool v16 = (row_bytes & 15) == 0;
-    for (int i = tid; i < 2 * RS * dp; i += NT) xs[i] = T(0.f);   // zero tails [d, dp)
-    __syncthreads();
     unsigned long long visited = 0;
-    // chunk sequence of this CTA: (unit u, row chunk c); warp `warp` stages row
-    // `warp` of a chunk into buffer b
-    auto stage = [&](int u, int c, int b) {
-        if (u < n_units) {
-            const int4 un = __ldg(p.units + u);
-            const int ns = __ldg(p.lsel + un.x);
-            const int r = c * RS + warp;
-            if (r < ns) {
-                const uint32_t pos = __ldg(p.spos + __ldg(p.sel_off + un.x) + r);
-                const char* src = reinterpret_cast<const char*>(payload + (int64_t)pos * d);
-                char* dst = reinterpret_cast<char*>(xs + ((size_t)b * RS + warp) * dp);
-                if (v16)
-                    for (int o = lane * 16; o < row_bytes; o += 32 * 16) cp_async16(dst + o, src + o);
-                else
-                    for (int o = lane * 8; o < row_bytes; o += 32 * 8) cp_async8(dst + o, src + o);
-            }
+    for (int i = tid; i < RS * dp; i += NT) xs[i] = T(0.f);   // zero tail [d, dp) of every staged row
+    int u = blockIdx.x;
+    if (u < n_units && tid < 32) reinterpret_cast<uint32_t*>(&S.rec[0])[tid] = reinterpret_cast<const uint32_t*>(p.recs + u)[tid];
+    __syncthreads();
+    int cur = 0;
+    for (; u < n_units; u += gridDim.x, cur ^= 1) {
+        const UnitRec& R = S.rec[cur];
+        const int np = R.np, nsel = R.nsel;
+        const int64_t l_unused = R.list;
+        (void)l_unused;
+        // rows of the first chunk (positions in the record) ...
+        const int nr0 = min(RS, nsel);
+        for (int r = warp; r < nr0; r += NW) {   // a warp per row: coalesced, no index division
+            const char* src = reinterpret_cast<const char*>(payload + (int64_t)R.pos[r] * d);
+            char* dst = reinterpret_cast<char*>(xs + r * dp);
+            if (v16)
+                for (int o = lane * 16; o < row_bytes; o += 32 * 16) cp_async16(dst + o, src + o);
+            else
+                for (int o = lane * 8; o < row_bytes; o += 32 * 8) cp_async8(dst + o, src + o);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    int u = blockIdx.x, c = 0, buf = 0;
-    stage(u, 0, 0);
-    while (u < n_units) {
-        const int4 un = __ldg(p.units + u);
-        const int nsel = __ldg(p.lsel + un.x);
-        const int np = un.z;
-        const int nchunk = (nsel + RS - 1) / RS;
-        // the next chunk: this unit's next, else the next unit's first
-        const int nu = (c + 1 < nchunk) ? u : u + gridDim.x;
-        const int nc = (c + 1 < nchunk) ? c + 1 : 0;
-        stage(nu, nc, buf ^ 1);
-        if (tid == 0 && c == 0) visited += (unsigned long long)nsel * np;
-        const int nr = min(RS, nsel - c * RS);
-        const int64_t soff = __ldg(p.sel_off + un.x) + (int64_t)c * RS;
-        // this warp's first pair: its query is requested before the barrier
-        int slot = warp;
-        float4 qv[TMAX];
-        auto load_q = [&](int sl, float4 (&dst)[TMAX]) {
-            const int code = __ldg(p.pair_codes + un.y + sl);
-            const float* qg = p.Q + (int64_t)(code / p.nprobe) * d;
+        // ... and this warp's two queries, in the same round trip
+        int qidx[2], sub[2], cnt[2] = {0, 0}, ovf[2] = {0, 0};
+        float tau[2];
+        bool live[2];
+        float4 qv[2][TMAX];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int slot = warp + h * NW;
+            live[h] = slot < np;
+            qidx[h] = live[h] ? R.q[slot] : 0;
+            sub[h] = live[h] ? R.sub[slot] : 0;
+            tau[h] = __int_as_float(0x7f800000);
+            const float* qg = p.Q + (int64_t)qidx[h] * d;
 #pragma unroll
             for (int t = 0; t < TMAX; ++t) {
                 const int e = lane * 4 + 128 * t;
-                dst[t] = (t < nt && e < d) ? __ldg(reinterpret_cast<const float4*>(qg + e))
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                qv[h][t] = (live[h] && e < d) ? __ldg(reinterpret_cast<const float4*>(qg + e))
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-        };
-        if (nr > 0 && slot < np) load_q(slot, qv);
-        // my row of this chunk (lanes 4r..4r+3 own row r after the reduction)
-        const int myr = (lane >> 2) & 7;
-        uint32_t mypos = 0u;
-        float mynorm = 0.f;
-        if (nr > 0 && myr < nr) {
-            mypos = __ldg(p.spos + soff + myr);
-            if (!IP) mynorm = __ldg(p.pnorm + mypos);
         }
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();   // chunk `buf` landed for every warp
-        const T* xb = xs + (size_t)buf * RS * dp;
-        for (; nr > 0 && slot < np; slot += NW) {
-            float4 qn[TMAX];
-            const bool more = slot + NW < np;
-            if (more) load_q(slot + NW, qn);   // next pair's query, in flight during the dot products
-            float acc[8];
+        // the next unit's record, consumed after this unit
+        const int un = u + gridDim.x;
+        uint32_t nrec = 0u;
+        if (warp == 0 && un < n_units) nrec = reinterpret_cast<const uint32_t*>(p.recs + un)[lane];
+        if (tid == 0) visited += (unsigned long long)nsel * np;
+        for (int c0 = 0; c0 < nsel; c0 += RS) {
+            const int nr = min(RS, nsel - c0);
+            if (c0 > 0) {
+                // later chunks (lists with more than RS selected rows)
+                __syncthreads();   // the previous chunk's rows are consumed
+                for (int r = warp; r < nr; r += NW) {
+                    const int rr = c0 + r;
+                    const uint32_t pos = rr < RPOS ? R.pos[rr] : p.spos[R.sel_off + rr];
+                    const char* src = reinterpret_cast<const char*>(payload + (int64_t)pos * d);
+                    char* dst = reinterpret_cast<char*>(xs + r * dp);
+                    if (v16)
+                        for (int o = lane * 16; o < row_bytes; o += 32 * 16) cp_async16(dst + o, src + o);
+                    else
+                        for (int o = lane * 8; o < row_bytes; o += 32 * 8) cp_async8(dst + o, src + o);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            if (live[0]) {
+                // dot form (one FFMA per element and query): every t step updates
+                // 2 x RS independent accumulators; rows past nr hold stale data
+                // and are scored but never appended
+                float acc[16];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) acc[r] = 0.f;
+                for (int i = 0; i < 16; ++i) acc[i] = 0.f;
 #pragma unroll
-            for (int t = 0; t < TMAX; ++t) {
-                if (t < nt) {
+                for (int t = 0; t < TMAX; ++t) {
+                    if (t < nt) {
 #pragma unroll
-                    for (int r = 0; r < RS; ++r) {
-                        const float4 x = V4<T>::lds(xb + r * dp + lane * 4 + 128 * t);
-                        acc[r] = fmaf(qv[t].x, x.x, acc[r]);
-                        acc[r] = fmaf(qv[t].y, x.y, acc[r]);
-                        acc[r] = fmaf(qv[t].z, x.z, acc[r]);
-                        acc[r] = fmaf(qv[t].w, x.w, acc[r]);
+                        for (int r = 0; r < RS; ++r) {
+                            const float4 x = V4<T>::lds(xs + r * dp + lane * 4 + 128 * t);
+                            acc[r] = fmaf(qv[0][t].x, x.x, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].x, x.x, acc[RS + r]);
+                            acc[r] = fmaf(qv[0][t].y, x.y, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].y, x.y, acc[RS + r]);
+                            acc[r] = fmaf(qv[0][t].z, x.z, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].z, x.z, acc[RS + r]);
+                            acc[r] = fmaf(qv[0][t].w, x.w, acc[r]);
+                            acc[RS + r] = fmaf(qv[1][t].w, x.w, acc[RS + r]);
+                        }
                     }
                 }
-            }
-            const float dot = transpose_reduce8(acc, lane);
-            const float key = IP ? -dot : fmaf(-2.f, dot, mynorm);
-            const int code = __ldg(p.pair_codes + un.y + slot);
-            const int q = code / p.nprobe;
-            const int64_t bidx = (int64_t)q * p.cb.n_sub + code % p.nprobe;
-            float* ckey = p.cb.key + bidx * C;
-            uint32_t* cpos = p.cb.pos + bidx * C;
-            // the buffer belongs to this warp for the whole unit (pairs partition
-            // the units; the slot -> warp map is the same for every chunk)
-            int cnt = c == 0 ? 0 : __ldcg(p.cb.cnt + bidx);
-            bool adm = (lane & 3) == 0 && myr < nr;
-            unsigned b = __ballot_sync(VS_FULL, adm);
-            if (cnt + __popc(b) > C) {
-                float nthr;
-                int lov = 0;
-                cnt = compact_slow_sel(ckey, cpos, cnt, p.k, p.margin[q], C - 32, &nthr, &lov);
-                if (lov && lane == 0) p.cb.overflow[q] = 1;
-                adm = adm && key <= nthr;
-                b = __ballot_sync(VS_FULL, adm);
-            }
-            if (adm) {
-                const int s = cnt + __popc(b & lanemask_lt());
-                ckey[s] = key;
-                cpos[s] = mypos;
-            }
-            if (lane == 0) p.cb.cnt[bidx] = cnt + __popc(b);
-            if (more) {
+                const float dot = transpose_reduce16(acc, lane);   // (lane >> 1) = h * RS + r
+                const int myh = (lane >> 1) / RS, myr = (lane >> 1) % RS;
+                const int rr = c0 + myr;
+                const uint32_t mypos = (myr < nr) ? (rr < RPOS ? R.pos[rr] : p.spos[R.sel_off + rr]) : 0u;
+                // key: -q.x, or ||x||^2 - 2 q.x (the query's ||q||^2 is common to
+                // all its keys; the margin eps_simt covers this form too)
+                const float key = IP ? -dot : fmaf(-2.f, dot, myr < nr ? p.pnorm[mypos] : 0.f);
 #pragma unroll
-                for (int t = 0; t < TMAX; ++t) qv[t] = qn[t];
+                for (int h = 0; h < 2; ++h) {
+                    if (!live[h]) continue;
+                    const int q = qidx[h];
+                    const int64_t cbase = ((int64_t)q * p.cb.n_sub + sub[h]) * C;
+                    float* ckey = p.cb.key + cbase;
+                    uint32_t* cpos = p.cb.pos + cbase;
+                    bool adm = (lane & 1) == 0 && myh == h && myr < nr && key <= tau[h];
+                    unsigned b = __ballot_sync(VS_FULL, adm);
+                    if (b && cnt[h] + __popc(b) > C) {
+                        float nthr;
+                        int lov = 0;
+                        cnt[h] = compact_slow_sel(ckey, cpos, cnt[h], p.k, p.margin[q], C - 32, &nthr, &lov);
+                        tau[h] = nthr;
+                        ovf[h] |= lov;
+                        adm = adm && key <= tau[h];
+                        b = __ballot_sync(VS_FULL, adm);
+                    }
+                    if (adm) {
+                        const int slot = cnt[h] + __popc(b & lanemask_lt());
+                        ckey[slot] = key;
+                        cpos[slot] = mypos;
+                    }
+                    cnt[h] += __popc(b);
+                }
             }
         }
-        __syncthreads();   // chunk `buf` consumed before it is restaged
-        buf ^= 1;
-        u = nu;
-        c = nc;
+        if (lane == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!live[h]) continue;
+                p.cb.cnt[(int64_t)qidx[h] * p.cb.n_sub + sub[h]] = cnt[h];
+                if (ovf[h]) p.cb.overflow[qidx[h]] = 1;
+            }
+        }
+        if (warp == 0) reinterpret_cast<uint32_t*>(&S.rec[cur ^ 1])[lane] = nrec;
+        __syncthreads();   // next record visible; staged rows free
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid == 0 && visited) atomicAdd(p.visited, visited);
 }
 
@@ -300,6 +360,11 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
     if ((e = cub::DeviceScan::ExclusiveSum(a.tmp, tb, a.lsel64, a.sel_off, a.nlist + 1, s)) != cudaSuccess) return e;
     k_list_sel_positions<<<lb, 256, 0, s>>>(a.list_off, a.nlist, a.pbits, a.sel_off, a.spos);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    UnitRec* recs = reinterpret_cast<UnitRec*>(a.recs);
+    const int rb = (int)std::max<int64_t>(1, std::min<int64_t>((a.max_units + 255) / 256, 8192));
+    k_make_recs<<<rb, 256, 0, s>>>(a.units, a.n_units, a.max_units, a.pair_codes, a.nprobe, a.lsel, a.sel_off, a.spos,
+                                   recs);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     IvfSelParams p;
     p.Q = a.Q;
     p.nq = a.nq;
@@ -307,11 +372,8 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
     p.dp = (a.d + 127) / 128 * 128;
     p.payload = a.payload;
     p.nprobe = a.nprobe;
-    p.units = a.units;
+    p.recs = recs;
     p.n_units = a.n_units;
-    p.pair_codes = a.pair_codes;
-    p.lsel = a.lsel;
-    p.sel_off = a.sel_off;
     p.spos = a.spos;
     p.pnorm = a.pnorm;
     p.margin = a.margin;
@@ -319,7 +381,7 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
     p.k = a.k;
     p.cb = a.cb;
     p.visited = a.visited;
-    const size_t smem = (size_t)2 * RS * p.dp * sizeof(T);
+    const size_t smem = ((sizeof(SelSmem) + 127) & ~size_t(127)) + (size_t)RS * p.dp * sizeof(T);
     auto kern = a.ip ? k_ivf_scan_sel<T, true> : k_ivf_scan_sel<T, false>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;

@@ -160,7 +160,7 @@ struct IvfSelLaunch {
     const uint32_t* pbits;      // permuted filter bitmap (required)
     const float* pnorm;         // ||x||^2 per payload row
     int nprobe;
-    const int32_t* pair_codes;  // from launch_ivf_group (unit_pairs = kSelUnitPairs)
+    const int32_t* pair_codes;  // from launch_ivf_group (unit_pairs = kIvfLmQT)
     const int4* units;
     const int32_t* n_units;
     int64_t max_units;
@@ -168,16 +168,17 @@ struct IvfSelLaunch {
     int ip, k;
     CandBuf cb;                 // n_sub = nprobe
     unsigned long long* visited;
-    // scratch: lsel [nlist], lsel64 / sel_off [nlist + 1], spos [n_total]
+    // scratch: lsel [nlist], lsel64 / sel_off [nlist + 1], spos [n_total], recs [max_units] x 128 B
     int32_t* lsel;
     int64_t* lsel64;
     int64_t* sel_off;
     uint32_t* spos;
+    void* recs;
     void* tmp;
     size_t tmp_bytes;           // >= ivf_sel_temp_bytes(nlist)
     int sm_count;
 };
-constexpr int kSelUnitPairs = 64;   // filtered scan: a unit is a whole list (its pairs split past 64)
+constexpr size_t kIvfSelRecBytes = 128;
 size_t ivf_sel_temp_bytes(int nlist);
 template <typename T>
 cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s);
@@ -218,6 +219,7 @@ struct RerankParams {
     int64_t id_offset;
     int64_t s_cap;              // survivor capacity per query
     uint32_t* s_pos;            // [nq][s_cap]
+    int32_t* s_count = nullptr; // [nq] survivors (split phase B; nullable: one kernel)
     uint64_t* s_key;            // [nq][s_cap]
     int64_t* s_id;              // [nq][s_cap]
     int64_t* out_ids;           // [nq][k] (nullable)

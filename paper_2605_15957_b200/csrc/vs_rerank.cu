@@ -561,8 +561,11 @@ __device__ unsigned long long g_rr_prof[8];
 #define RR_MARK(i) do {} while (0)
 #endif
 
-template <typename T, bool IP, bool WIDE>
-__global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
+// PH: 0 the whole phase B in one kernel; 1 steps 0-2 only (live candidates ->
+// survivors, their count in p.s_count): no scorer registers, so more CTAs per
+// SM hide the latency-bound gather and select; 2 steps 3-5 from p.s_count
+template <typename T, bool IP, bool WIDE, int PH>
+__global__ void __launch_bounds__(NT, PH == 1 ? 5 : (WIDE ? 2 : 4)) k_rerank(RerankParams p) {
     constexpr int LCAP = lcap<WIDE>();
 #ifdef VS_RERANK_PROFILE
     long long rr_t = clock64();
@@ -571,10 +574,11 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
     Small& sm = *reinterpret_cast<Small*>(smraw);
     unsigned char* u = smraw + ((sizeof(Small) + 127) & ~size_t(127));       // union region
     // chain / leaf buffers of the staged scorer (absent on the register path)
+    const bool chains = !p.reg_path && PH != 1;
     double* cbuf = reinterpret_cast<double*>(u + p.ubytes);                  // [NWARP][8*MAXLEAF]
-    double* lbuf = cbuf + (p.reg_path ? 0 : NWARP * 8 * MAXLEAF);            // [NWARP][2*MAXLEAF]
-    float* qs = reinterpret_cast<float*>(lbuf + (p.reg_path ? 0 : NWARP * 2 * MAXLEAF));   // [q_stride] (skewed)
-    int* cnts = reinterpret_cast<int*>(qs + q_stride(p.d));                  // [nsub]
+    double* lbuf = cbuf + (chains ? NWARP * 8 * MAXLEAF : 0);                // [NWARP][2*MAXLEAF]
+    float* qs = reinterpret_cast<float*>(lbuf + (chains ? NWARP * 2 * MAXLEAF : 0));   // [q_stride] (skewed)
+    int* cnts = reinterpret_cast<int*>(qs + (PH == 1 ? 0 : q_stride(p.d)));  // [nsub]
     unsigned* hist = reinterpret_cast<unsigned*>(cnts + ((p.cb.n_sub + 3) & ~3));   // [HBINS]
     double* qd = reinterpret_cast<double*>(hist + HBINS);                    // [q_stride] float64, skewed
 
@@ -586,21 +590,23 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
     const int nsub = p.cb.sub_off ? (int)(p.cb.sub_off[q + 1] - bbase) : p.cb.n_sub;
     const int d = p.d;
     const bool warp_path = d >= 8 && d <= WARP_D_MAX;
-    if (warp_path) {
+    if (warp_path && PH != 1) {
         const int* src = reinterpret_cast<const int*>(&p.plan);
         int* dst = reinterpret_cast<int*>(static_cast<LeafPlan*>(&sm));
         for (int i = tid; i < (int)(sizeof(LeafPlan) / 4); i += NT) dst[i] = src[i];
     }
     __syncthreads();
     const float* qg = p.Q + q * (int64_t)d;
-    if (warp_path)
-        for (int i = tid; i < d; i += NT) {
-            const float v = qg[i];
-            qs[i + SHQ * sm.gsk[i / 8]] = v;
-            qd[i + SHQ * sm.gsk[i / 8]] = (double)v;
-        }
-    else
-        for (int i = tid; i < d; i += NT) qs[i] = qg[i];
+    if (PH != 1) {
+        if (warp_path)
+            for (int i = tid; i < d; i += NT) {
+                const float v = qg[i];
+                qs[i + SHQ * sm.gsk[i / 8]] = v;
+                qd[i + SHQ * sm.gsk[i / 8]] = (double)v;
+            }
+        else
+            for (int i = tid; i < d; i += NT) qs[i] = qg[i];
+    }
     long long tot = 0;
     for (int s = tid; s < nsub; s += NT) {
         const int c = p.cb.cnt[bbase + s];
@@ -626,142 +632,135 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
     const uint32_t ext_o = has_ext ? f2o(__fadd_ru(p.ext_thr[q], 0.5f * p.margin[q])) : 0xffffffffu;
     pre = min(pre, ext_o);
 
-    RR_MARK(0);
-    float* lkey = reinterpret_cast<float*>(u);
-    uint32_t* lpos = reinterpret_cast<uint32_t*>(u + LCAP * 4);
-    // -1. more candidates than shared memory holds (e.g. exhaustive buffers of
-    //    short splits): bound the union's k-th key from above by the k-th key
-    //    of a subset — the first m keys of every buffer — and tighten the live
-    //    filter to that bound + margin. The k smallest keys and every key within
-    //    the margin of the k-th stay live, so the result is unchanged.
-    if (tot > LCAP && tot > p.k) {
-        const int m = max(1, (LCAP / 2) / max(nsub, 1));
+    int64_t ns = 0;
+    if (PH == 2) {
+        ns = p.s_count[q];
+    } else {
+        RR_MARK(0);
+        float* lkey = reinterpret_cast<float*>(u);
+        uint32_t* lpos = reinterpret_cast<uint32_t*>(u + LCAP * 4);
+        // -1. more candidates than shared memory holds (e.g. exhaustive buffers of
+        //    short splits): bound the union's k-th key from above by the k-th key
+        //    of a subset — the first m keys of every buffer — and tighten the live
+        //    filter to that bound + margin. The k smallest keys and every key within
+        //    the margin of the k-th stay live, so the result is unchanged.
+        if (tot > LCAP && tot > p.k) {
+            const int m = max(1, (LCAP / 2) / max(nsub, 1));
+            if (tid == 0) sm.counter = 0;
+            __syncthreads();
+            for (int s = w; s < nsub; s += NWARP) {
+                const int cs = min(cnts[s], m);
+                const float* bk = ckey + (int64_t)s * C;
+                for (int j = lane; j - lane < cs; j += 32) {
+                    const float kv = j < cs ? bk[j] : 0.f;
+                    const bool live = j < cs && f2o(kv) <= pre;
+                    const unsigned b = __ballot_sync(VS_FULL, live);
+                    if (!b) continue;
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
+                    base = __shfl_sync(VS_FULL, base, 0);
+                    const int slot = base + __popc(b & lanemask_lt());
+                    if (live && slot < LCAP) lkey[slot] = kv;
+                }
+            }
+            __syncthreads();
+            const int nsamp = min(sm.counter, LCAP);
+            __syncthreads();
+            if (nsamp >= p.k) {
+                const uint32_t kth_s = block_radix_kth(
+                    [&](auto fn) {
+                        for (int i = tid; i < nsamp; i += NT) fn(f2o(lkey[i]));
+                    },
+                    (unsigned)p.k, hist, sm);
+                pre = min(pre, f2o(__fadd_ru(o2f(kth_s), p.margin[q])));
+            }
+            __syncthreads();
+        }
+        // 0. live candidates -> shared memory (one warp per buffer, coalesced)
         if (tid == 0) sm.counter = 0;
         __syncthreads();
         for (int s = w; s < nsub; s += NWARP) {
-            const int cs = min(cnts[s], m);
+            const int cs = cnts[s];
             const float* bk = ckey + (int64_t)s * C;
-            for (int j = lane; j - lane < cs; j += 32) {
-                const float kv = j < cs ? bk[j] : 0.f;
-                const bool live = j < cs && f2o(kv) <= pre;
-                const unsigned b = __ballot_sync(VS_FULL, live);
-                if (!b) continue;
-                int base = 0;
-                if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
-                base = __shfl_sync(VS_FULL, base, 0);
-                const int slot = base + __popc(b & lanemask_lt());
-                if (live && slot < LCAP) lkey[slot] = kv;
-            }
-        }
-        __syncthreads();
-        const int nsamp = min(sm.counter, LCAP);
-        __syncthreads();
-        if (nsamp >= p.k) {
-            const uint32_t kth_s = block_radix_kth(
-                [&](auto fn) {
-                    for (int i = tid; i < nsamp; i += NT) fn(f2o(lkey[i]));
-                },
-                (unsigned)p.k, hist, sm);
-            pre = min(pre, f2o(__fadd_ru(o2f(kth_s), p.margin[q])));
-        }
-        __syncthreads();
-    }
-    // 0. live candidates -> shared memory (one warp per buffer, coalesced)
-    if (tid == 0) sm.counter = 0;
-    __syncthreads();
-    for (int s = w; s < nsub; s += NWARP) {
-        const int cs = cnts[s];
-        const float* bk = ckey + (int64_t)s * C;
-        const uint32_t* bp = cpos + (int64_t)s * C;
-        for (int j0 = 0; j0 < cs; j0 += 128) {
-            // four independent key loads in flight, then the positions of the live ones
-            float kk[4];
-            uint32_t pp[4];
-            bool live[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int j = j0 + 32 * h + lane;
-                kk[h] = j < cs ? bk[j] : 0.f;
-            }
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int j = j0 + 32 * h + lane;
-                live[h] = j < cs && f2o(kk[h]) <= pre;
-                pp[h] = live[h] ? bp[j] : 0u;
-            }
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const unsigned b = __ballot_sync(VS_FULL, live[h]);
-                if (!b) continue;
-                int base = 0;
-                if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
-                base = __shfl_sync(VS_FULL, base, 0);
-                const int slot = base + __popc(b & lanemask_lt());
-                if (live[h] && slot < LCAP) {
-                    lkey[slot] = kk[h];
-                    lpos[slot] = pp[h];
+            const uint32_t* bp = cpos + (int64_t)s * C;
+            for (int j0 = 0; j0 < cs; j0 += 128) {
+                // four independent key loads in flight, then the positions of the live ones
+                float kk[4];
+                uint32_t pp[4];
+                bool live[4];
+    #pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int j = j0 + 32 * h + lane;
+                    kk[h] = j < cs ? bk[j] : 0.f;
+                }
+    #pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int j = j0 + 32 * h + lane;
+                    live[h] = j < cs && f2o(kk[h]) <= pre;
+                    pp[h] = live[h] ? bp[j] : 0u;
+                }
+    #pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const unsigned b = __ballot_sync(VS_FULL, live[h]);
+                    if (!b) continue;
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&sm.counter, __popc(b));
+                    base = __shfl_sync(VS_FULL, base, 0);
+                    const int slot = base + __popc(b & lanemask_lt());
+                    if (live[h] && slot < LCAP) {
+                        lkey[slot] = kk[h];
+                        lpos[slot] = pp[h];
+                    }
                 }
             }
         }
-    }
-    __syncthreads();
-    const int nl = sm.counter;
-    __syncthreads();
-#ifdef VS_RERANK_PROFILE
-    if (tid == 0) {
-        atomicAdd(&g_rr_prof[5], (unsigned long long)tot);   // candidates in the buffers
-        atomicAdd(&g_rr_prof[6], (unsigned long long)nl);    // live (key <= pre)
-    }
-#endif
-    int64_t ns = 0;
-    if (nl <= LCAP) {
-        RR_MARK(1);
-        // 1. k-th smallest approximate key  2. survivors (shared-memory path)
-        uint32_t thr_o = 0xffffffffu;
-        uint32_t kth = 0xffffffffu;
-        if (!p.band_ready && nl >= p.k && (nl > p.k || p.out_kth)) {
-            kth = block_radix_kth(
-                [&](auto fn) {
-                    for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
-                },
-                (unsigned)p.k, hist, sm);
-        }
-        if (p.out_kth) {   // this shard's k smallest approximate keys (+inf padded)
-            write_local_topk_keys(
-                [&](auto fn) {
-                    for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
-                },
-                kth, p.k, hist, sm, 0.5f * p.margin[q], p.out_kth + q * (int64_t)p.k);
-            return;
-        }
-        if (kth != 0xffffffffu && nl > p.k) thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
-        thr_o = min(thr_o, ext_o);
-        if (tid == 0) sm.counter = 0;
         __syncthreads();
-        for (int i = tid; i < nl; i += NT) {
-            if (f2o(lkey[i]) <= thr_o) {
-                const int slot = atomicAdd(&sm.counter, 1);
-                if (slot < p.s_cap) spos[slot] = lpos[i];
+        const int nl = sm.counter;
+        __syncthreads();
+    #ifdef VS_RERANK_PROFILE
+        if (tid == 0) {
+            atomicAdd(&g_rr_prof[5], (unsigned long long)tot);   // candidates in the buffers
+            atomicAdd(&g_rr_prof[6], (unsigned long long)nl);    // live (key <= pre)
+        }
+    #endif
+        if (nl <= LCAP) {
+            RR_MARK(1);
+            // 1. k-th smallest approximate key  2. survivors (shared-memory path)
+            uint32_t thr_o = 0xffffffffu;
+            uint32_t kth = 0xffffffffu;
+            if (!p.band_ready && nl >= p.k && (nl > p.k || p.out_kth)) {
+                kth = block_radix_kth(
+                    [&](auto fn) {
+                        for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
+                    },
+                    (unsigned)p.k, hist, sm);
             }
-        }
-        __syncthreads();
-        ns = sm.counter;
-    } else {
-        // global-memory path (very wide near-tie sets)
-        uint32_t thr_o = 0xffffffffu;
-        if (tot > p.k) {
-            // nl > LCAP >= k live keys (key <= pre): their k-th smallest
-            uint32_t kth = block_radix_kth(
-                [&](auto fn) {
-                    for (int s = w; s < nsub; s += NWARP)
-                        for (int j = lane; j < cnts[s]; j += 32) {
-                            const uint32_t o = f2o(ckey[(int64_t)s * C + j]);
-                            if (o <= pre) fn(o);
-                        }
-                },
-                (unsigned)p.k, hist, sm);
-            if (p.out_kth) {
+            if (p.out_kth) {   // this shard's k smallest approximate keys (+inf padded)
                 write_local_topk_keys(
+                    [&](auto fn) {
+                        for (int i = tid; i < nl; i += NT) fn(f2o(lkey[i]));
+                    },
+                    kth, p.k, hist, sm, 0.5f * p.margin[q], p.out_kth + q * (int64_t)p.k);
+                return;
+            }
+            if (kth != 0xffffffffu && nl > p.k) thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
+            thr_o = min(thr_o, ext_o);
+            if (tid == 0) sm.counter = 0;
+            __syncthreads();
+            for (int i = tid; i < nl; i += NT) {
+                if (f2o(lkey[i]) <= thr_o) {
+                    const int slot = atomicAdd(&sm.counter, 1);
+                    if (slot < p.s_cap) spos[slot] = lpos[i];
+                }
+            }
+            __syncthreads();
+            ns = sm.counter;
+        } else {
+            // global-memory path (very wide near-tie sets)
+            uint32_t thr_o = 0xffffffffu;
+            if (tot > p.k) {
+                // nl > LCAP >= k live keys (key <= pre): their k-th smallest
+                uint32_t kth = block_radix_kth(
                     [&](auto fn) {
                         for (int s = w; s < nsub; s += NWARP)
                             for (int j = lane; j < cnts[s]; j += 32) {
@@ -769,29 +768,43 @@ __global__ void __launch_bounds__(NT, WIDE ? 2 : 4) k_rerank(RerankParams p) {
                                 if (o <= pre) fn(o);
                             }
                     },
-                    kth, p.k, hist, sm, 0.5f * p.margin[q], p.out_kth + q * (int64_t)p.k);
-                return;
-            }
-            thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
-        }
-        thr_o = min(thr_o, ext_o);
-        if (tid == 0) sm.counter = 0;
-        __syncthreads();
-        for (int s = w; s < nsub; s += NWARP)
-            for (int j = lane; j < cnts[s]; j += 32)
-                if (f2o(ckey[(int64_t)s * C + j]) <= thr_o) {
-                    const int slot = atomicAdd(&sm.counter, 1);
-                    if (slot < p.s_cap) spos[slot] = cpos[(int64_t)s * C + j];
+                    (unsigned)p.k, hist, sm);
+                if (p.out_kth) {
+                    write_local_topk_keys(
+                        [&](auto fn) {
+                            for (int s = w; s < nsub; s += NWARP)
+                                for (int j = lane; j < cnts[s]; j += 32) {
+                                    const uint32_t o = f2o(ckey[(int64_t)s * C + j]);
+                                    if (o <= pre) fn(o);
+                                }
+                        },
+                        kth, p.k, hist, sm, 0.5f * p.margin[q], p.out_kth + q * (int64_t)p.k);
+                    return;
                 }
+                thr_o = f2o(__fadd_ru(o2f(kth), p.margin[q]));
+            }
+            thr_o = min(thr_o, ext_o);
+            if (tid == 0) sm.counter = 0;
+            __syncthreads();
+            for (int s = w; s < nsub; s += NWARP)
+                for (int j = lane; j < cnts[s]; j += 32)
+                    if (f2o(ckey[(int64_t)s * C + j]) <= thr_o) {
+                        const int slot = atomicAdd(&sm.counter, 1);
+                        if (slot < p.s_cap) spos[slot] = cpos[(int64_t)s * C + j];
+                    }
+            __syncthreads();
+            ns = sm.counter;
+        }
         __syncthreads();
-        ns = sm.counter;
+        if (ns > p.s_cap) {  // cannot re-rank all survivors: re-run with larger buffers
+            if (tid == 0) p.cb.overflow[q] = 1;
+            ns = p.s_cap;
+        }
+        if (PH == 1) {
+            if (tid == 0) p.s_count[q] = (int)ns;
+            return;
+        }
     }
-    __syncthreads();
-    if (ns > p.s_cap) {  // cannot re-rank all survivors: re-run with larger buffers
-        if (tid == 0) p.cb.overflow[q] = 1;
-        ns = p.s_cap;
-    }
-
     RR_MARK(2);
     // 3. exact float64 scores (bit-identical to the reference)
     const T* rows = reinterpret_cast<const T*>(p.rows);
@@ -1488,18 +1501,21 @@ __global__ void __launch_bounds__(NT) k_union_kth(const float* __restrict__ keys
     if (threadIdx.x == 0) out[q] = o2f(ukeys[k - 1]);
 }
 
-static size_t rerank_smem(int d, int nsub, bool wide) {
-    const size_t chains = reg_path_ok(d) ? 0 : (size_t)NWARP * 8 * MAXLEAF * 8 + (size_t)NWARP * 2 * MAXLEAF * 8;
-    return ((sizeof(Small) + 127) & ~size_t(127)) + union_bytes(d, wide) + chains + (size_t)q_stride(d) * 4 +
-           (size_t)((nsub + 3) & ~3) * 4 + (size_t)HBINS * 4 + (size_t)q_stride(d) * 8 + 16;
+static size_t rerank_smem(int d, int nsub, size_t ubytes, int ph) {
+    const size_t chains =
+        (reg_path_ok(d) || ph == 1) ? 0 : (size_t)NWARP * 8 * MAXLEAF * 8 + (size_t)NWARP * 2 * MAXLEAF * 8;
+    const size_t qbytes = ph == 1 ? 0 : (size_t)q_stride(d) * 12;   // float + float64 copies of the query
+    return ((sizeof(Small) + 127) & ~size_t(127)) + ubytes + chains + qbytes + (size_t)((nsub + 3) & ~3) * 4 +
+           (size_t)HBINS * 4 + 16;
 }
 
-template <typename T, bool IP, bool WIDE>
+template <typename T, bool IP, bool WIDE, int PH>
 static cudaError_t launch_rerank_v(const RerankParams& p, cudaStream_t s) {
-    const size_t smem = rerank_smem(p.d, p.cb.n_sub, WIDE);
-    cudaError_t e = cudaFuncSetAttribute(k_rerank<T, IP, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = rerank_smem(p.d, p.cb.n_sub, (size_t)p.ubytes, PH);
+    auto kern = k_rerank<T, IP, WIDE, PH>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_rerank<T, IP, WIDE><<<(unsigned)p.nq, NT, smem, s>>>(p);
+    kern<<<(unsigned)p.nq, NT, smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -1511,10 +1527,22 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     p.reg_path = reg_path_ok(p.d) ? 1 : 0;
     // large k (many survivors and live candidates per query): the wide build;
     // small k (probes, IVF lists, config 1): 4 CTAs/SM hide more latency (measured)
-    const bool wide = p.k > 64;
+    static const int wide_env = getenv("VS_RR_WIDE") ? atoi(getenv("VS_RR_WIDE")) : -1;
+    const bool wide = wide_env >= 0 ? wide_env == 1 : p.k > 64;
     p.ubytes = (int)union_bytes(p.d, wide);
-    if (wide) return p.ip ? launch_rerank_v<T, true, true>(p, s) : launch_rerank_v<T, false, true>(p, s);
-    return p.ip ? launch_rerank_v<T, true, false>(p, s) : launch_rerank_v<T, false, false>(p, s);
+    // split phase B (VS_RR_SPLIT, default on): the gather + select kernel runs at
+    // 5 CTAs/SM without the scorer's registers, then score + top-k
+    static const int split_env = getenv("VS_RR_SPLIT") ? atoi(getenv("VS_RR_SPLIT")) : 1;
+    if (split_env && p.s_count && !p.out_kth) {
+        RerankParams p1 = p;
+        p1.ubytes = (int)union_min<false>();   // live candidates only (LCAP of the narrow build)
+        cudaError_t e = p.ip ? launch_rerank_v<T, true, false, 1>(p1, s) : launch_rerank_v<T, false, false, 1>(p1, s);
+        if (e != cudaSuccess) return e;
+        if (wide) return p.ip ? launch_rerank_v<T, true, true, 2>(p, s) : launch_rerank_v<T, false, true, 2>(p, s);
+        return p.ip ? launch_rerank_v<T, true, false, 2>(p, s) : launch_rerank_v<T, false, false, 2>(p, s);
+    }
+    if (wide) return p.ip ? launch_rerank_v<T, true, true, 0>(p, s) : launch_rerank_v<T, false, true, 0>(p, s);
+    return p.ip ? launch_rerank_v<T, true, false, 0>(p, s) : launch_rerank_v<T, false, false, 0>(p, s);
 }
 #ifdef VS_RERANK_PROFILE
 extern "C" int vs_debug_rerank_profile(unsigned long long* out, int reset) {
