@@ -519,6 +519,38 @@ __device__ __forceinline__ void warp_np_score_reg2(const double* qpd, const floa
     ob = __shfl_sync(VS_FULL, sb, tl.root);
 }
 
+// the same for ONE row (the narrow build: 64 registers at 4 CTAs/SM; two rows
+// of registers spilled the row data to local memory there)
+template <bool IP, typename T>
+__device__ __forceinline__ double warp_np_score_reg1(const double* qpd, const float2 (&xa)[16], int M,
+                                                    const double* qtail, const T* xta, int ntail,
+                                                    const TreeLane& tl, int lane) {
+    double a0 = 0.0, a1 = 0.0;
+    if (M > 0) {
+        const double2 q = *reinterpret_cast<const double2*>(qpd);
+        a0 = term_dd<IP>(q.x, xa[0].x);
+        a1 = term_dd<IP>(q.y, xa[0].y);
+    }
+#pragma unroll
+    for (int m = 1; m < 16; ++m) {
+        if (m < M) {
+            const double2 q = *reinterpret_cast<const double2*>(qpd + 8 * m);
+            a0 = __dadd_rn(a0, term_dd<IP>(q.x, xa[m].x));
+            a1 = __dadd_rn(a1, term_dd<IP>(q.y, xa[m].y));
+        }
+    }
+    double va = __dadd_rn(a0, a1);
+    va = __dadd_rn(va, __shfl_xor_sync(VS_FULL, va, 1));
+    va = __dadd_rn(va, __shfl_xor_sync(VS_FULL, va, 2));
+    for (int i = 0; i < ntail; ++i) va = __dadd_rn(va, term_dd<IP>(qtail[i], ld_elem(xta + i)));
+    double sa = __shfl_sync(VS_FULL, va, (lane * 4) & 31);
+    for (int l = 0; l < tl.nlevels; ++l) {
+        const double pa = __shfl_sync(VS_FULL, sa, tl.na), qa = __shfl_sync(VS_FULL, sa, tl.nb);
+        if (tl.lvl == l) sa = __dadd_rn(pa, qa);
+    }
+    return __shfl_sync(VS_FULL, sa, tl.root);
+}
+
 // stage one row into shared memory (same element type) in the skewed leaf
 // layout, coalesced; 16-byte cp.async chunks when the row size allows, so the
 // copy overlaps compute. Leaves split at multiples of 8 elements, so a chunk
@@ -875,6 +907,31 @@ __global__ void __launch_bounds__(NT, PH == 1 ? 5 : (WIDE ? 2 : 4)) k_rerank(Rer
             if (j < ns) prefetch_row(row_at(j, ps));
             if (j + NWARP < ns) prefetch_row(row_at(j + NWARP, ps));
         };
+        if (!WIDE) {
+            // one row per warp and iteration (see warp_np_score_reg1)
+            for (int pd = 1; pd <= RR_PD; ++pd) {
+                uint32_t ps;
+                const int64_t j = w + pd * NWARP;
+                if (j < ns) prefetch_row(row_at(j, ps));
+            }
+            for (int64_t j = w; j < ns; j += NWARP) {
+                uint32_t ps;
+                const int64_t r = row_at(j, ps);
+                float2 xa[16];
+                fetch(xa, r);
+                {
+                    uint32_t ps2;
+                    const int64_t jn = j + (RR_PD + 1) * NWARP;
+                    if (jn < ns) prefetch_row(row_at(jn, ps2));
+                }
+                const double sc = warp_np_score_reg1<IP, T>(qpd, xa, M, qtail, rows + r * (int64_t)d + offL + 8 * M,
+                                                            ntail, tl, lane);
+                if (lane == 0) {
+                    skey[j] = d2o(IP ? -sc : sc);
+                    sid[j] = (p.id_map ? p.id_map[ps] : r) + p.id_offset;
+                }
+            }
+        } else {
         for (int pd = 1; pd <= RR_PD; ++pd) prefetch_iter(w + pd * 2 * NWARP);
         int64_t i = w;
         uint32_t psa = 0, psb = 0;
@@ -913,6 +970,7 @@ __global__ void __launch_bounds__(NT, PH == 1 ? 5 : (WIDE ? 2 : 4)) k_rerank(Rer
             rb = rb_n;
             psa = psa_n;
             psb = psb_n;
+        }
         }
     } else if (warp_path) {
         // double-buffered: the next survivor row is staged (cp.async-free plain
@@ -1530,10 +1588,13 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     static const int wide_env = getenv("VS_RR_WIDE") ? atoi(getenv("VS_RR_WIDE")) : -1;
     const bool wide = wide_env >= 0 ? wide_env == 1 : p.k > 64;
     p.ubytes = (int)union_bytes(p.d, wide);
-    // split phase B (VS_RR_SPLIT, default on): the gather + select kernel runs at
-    // 5 CTAs/SM without the scorer's registers, then score + top-k
-    static const int split_env = getenv("VS_RR_SPLIT") ? atoi(getenv("VS_RR_SPLIT")) : 1;
-    if (split_env && p.s_count && !p.out_kth) {
+    // split phase B (wide build; VS_RR_SPLIT=0/1 overrides): the gather + select
+    // kernel runs at 5 CTAs/SM without the scorer's registers, then score +
+    // top-k (measured: config 2 re-rank 2.06 -> 1.90 ms; the narrow build
+    // already runs 4 CTAs/SM and the split cost config 3 0.09 ms)
+    static const int split_env = getenv("VS_RR_SPLIT") ? atoi(getenv("VS_RR_SPLIT")) : -1;
+    const bool split = split_env >= 0 ? split_env == 1 : wide;
+    if (split && p.s_count && !p.out_kth) {
         RerankParams p1 = p;
         p1.ubytes = (int)union_min<false>();   // live candidates only (LCAP of the narrow build)
         cudaError_t e = p.ip ? launch_rerank_v<T, true, false, 1>(p1, s) : launch_rerank_v<T, false, false, 1>(p1, s);
