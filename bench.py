@@ -500,7 +500,8 @@ class ExactWorkload:
         return "weak" if (self.replicas or self.cfg.get("host")) else "strong"
 
     def roofline(self, kt, steps, ctx, N):
-        self.kernel_name = {1: "simt_fp32", 2: "tcgen05_bf16", 3: "wide"}.get(ctx.stats()[N.STAT_LAST_ENN_KERNEL], "?")
+        tc = "tcgen05_bf16" if os.environ.get("VS_TC_BF16") == "1" else "tcgen05_fp16"
+        self.kernel_name = {1: "simt_fp32", 2: tc, 3: "wide"}.get(ctx.stats()[N.STAT_LAST_ENN_KERNEL], "?")
         if self.cfg.get("host"):
             # streamed variant: the bound is the PCIe transfer of the selected rows
             byts = float(self.n_sel) * self.d * 4
@@ -521,7 +522,8 @@ class ExactWorkload:
         return {"bound": "tensor", "kernel": f"enn_scan ({kern})",
                 "achieved": round(achieved, 2) if achieved else None, "peak": peak, "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4) if achieved else None,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured)",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (of measured; dense fp16 runs at the "
+                               "bf16 rate)",
                 "algorithmic_flops_per_launch": flops, "traffic": traffic}
 
     def config(self):
@@ -540,8 +542,10 @@ class ExactWorkload:
                 "phase_a_kernel": getattr(self, "kernel_name", "?")}
 
     def dtype(self):
-        return "f32 storage; " + ("bf16 tcgen05 candidates" if getattr(self, "kernel_name", "") ==
-                                  "tcgen05_bf16" else "fp32 SIMT candidates") + "; f64 exact re-rank"
+        kern = getattr(self, "kernel_name", "")
+        cand = ("fp16 (power-of-two scaled) tcgen05 candidates" if kern == "tcgen05_fp16" else
+                "bf16 tcgen05 candidates" if kern == "tcgen05_bf16" else "fp32 SIMT candidates")
+        return "f32 storage; " + cand + "; f64 exact re-rank"
 
     def extras(self, ctx, N):
         st = ctx.stats()
