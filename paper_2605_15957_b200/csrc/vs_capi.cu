@@ -1772,9 +1772,14 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
         CK(cudaMemsetAsync(cb.overflow, 0, job.nq * sizeof(int), ctx->stream));
         static const int sel_env = getenv("VS_IVF_SEL") ? atoi(getenv("VS_IVF_SEL")) : 1;
         if (lmajor && job.pbits && sel_env && v->n_total < (int64_t)UINT32_MAX) {
-            // filtered: pre-selected rows per list, one round trip per unit (vs_ivf_sel.cu)
+            // filtered: pre-selected rows per list, one round trip per unit
+            // (vs_ivf_sel.cu); float32 lists with d % 16 == 0 score on the
+            // tensor cores (fp16 operands, tensor-core margins for phase B)
+            static const int mma_env = getenv("VS_IVF_MMA") ? atoi(getenv("VS_IVF_MMA")) : 1;
+            const bool mma = mma_env && v->dtype == VS_DTYPE_F32 && v->d % 16 == 0 && v->d <= 2048 &&
+                             ctx->opt_enn_kernel != 1;
             IvfGroups gr;
-            CKS(ivf_group(ctx, job, vs::kIvfLmQT, &gr));
+            CKS(ivf_group(ctx, job, mma ? vs::kMmaPairs : vs::kIvfLmQT, &gr));
             CK(cudaMemsetAsync(cb.cnt, 0, (size_t)job.nq * n_sub * sizeof(int), ctx->stream));
             vs::IvfSelLaunch a;
             a.Q = job.q;
@@ -1807,6 +1812,31 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
             CKS(arena_alloc(ctx, a.tmp_bytes, &tmp));
             a.tmp = tmp;
             a.sm_count = ctx->sm_count;
+            if (mma) {
+                unsigned* bounds = nullptr;
+                float* mmargin = nullptr;
+                __half* qh = nullptr;
+                float* kinv = nullptr;
+                CKS(arena_alloc(ctx, 2, &bounds));
+                CKS(arena_alloc(ctx, (size_t)job.nq, &mmargin));
+                CKS(arena_alloc(ctx, (size_t)job.nq * ((v->d + 7) / 8 * 8), &qh));
+                CKS(arena_alloc(ctx, (size_t)job.nq, &kinv));
+                CKS(arena_alloc(ctx, (size_t)job.nq * job.nprobe, &a.pq));
+                CKS(arena_alloc(ctx, (size_t)job.nq * job.nprobe, &a.psub));
+                {
+                    KTimer kt(ctx, VS_K_STAGE);
+                    CK(vs::launch_f16_row_bounds(v->pmax, v->d, bounds, ctx->stream));
+                    CKS(vs::tc_stage_queries_f16(ctx, job.q, job.nq, v->d, v->pmax, bounds, v->metric, qh, kinv,
+                                                 mmargin));
+                }
+                a.mma = 1;
+                a.Qh = qh;
+                a.kinv = kinv;
+                a.xscale = v->pmax;
+                a.margin = mmargin;
+                margin = mmargin;   // phase B re-ranks the tensor-core margin band
+                ctx->stats[VS_STAT_LAUNCHES] += 1;
+            }
             KTimer kt(ctx, VS_K_IVF_SCAN);
             if (v->dtype == VS_DTYPE_F32) CK(vs::launch_ivf_scan_sel<float>(a, ctx->stream));
             else CK(vs::launch_ivf_scan_sel<__nv_bfloat16>(a, ctx->stream));

@@ -24,6 +24,7 @@
 // Reference: IvfIndex.search, vecindex.py:230-258, with the filtered
 // extension rows = rows[mask[rows]].
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "vs_common.cuh"
 #include "vs_kernels.cuh"
@@ -334,6 +335,271 @@ __global__ void __launch_bounds__(NT, 4) k_ivf_scan_sel(IvfSelParams p) {
     if (tid == 0 && visited) atomicAdd(p.visited, visited);
 }
 
+// ---- tensor-core variant (mma.sync m16n8k16, fp16 operands) ---------------------------------
+// The same filtered scan with the dot products on the tensor cores: a unit is
+// (list, <= 16 pairs); its queries (fp16, per-query power-of-two scales, staged
+// once per search by k_stage_queries) are the MMA's A tile (16 x d), the
+// list's selected rows, converted to fp16 with the column scale while they
+// are staged, its B tiles (8 rows x d). The four warps split K, their fp32
+// partial tiles are summed through shared memory, and the keys
+// ||x||^2 - 2 (q~.x~) 2^-(eq+ex) go to the pairs' buffers. Keys carry the
+// tensor-core error bound (fp16 rounding of both operands, fp32 accumulation;
+// DESIGN.md §4.1); the IVF phase B uses that margin. Row-side rounding errors
+// are bounded a priori (|dx_i| <= 2^-11 |x_i| + 2^-25 / 2^ex), so no pass
+// over the rows is needed for the margin.
+namespace {
+constexpr int MQ = kMmaPairs;   // pairs per unit (MMA M)
+constexpr int MN = 8;           // rows per chunk (MMA N)
+constexpr int MW = 4;           // warps; K is split across them
+constexpr int MNT = MW * 32;
+constexpr int MPOS = 27;
+constexpr int MV = 2048 / 128;  // float4 loads per lane for a row of d <= 2048
+
+struct __align__(16) MmaRec {
+    int32_t list, np, nsel, first_pair;
+    uint32_t sel_off;
+    uint32_t pos[MPOS];
+};
+static_assert(sizeof(MmaRec) == 128, "one 128-byte record per unit");
+
+__global__ void k_make_mma_recs(const int4* __restrict__ units, const int32_t* __restrict__ n_units,
+                                int64_t max_units, const int32_t* __restrict__ lsel,
+                                const int64_t* __restrict__ sel_off, const uint32_t* __restrict__ spos,
+                                MmaRec* __restrict__ recs) {
+    const int nu = *n_units;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < max_units && u < nu;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int4 un = units[u];
+        MmaRec r;
+        r.list = un.x;
+        r.np = un.z;
+        r.first_pair = un.y;
+        r.nsel = lsel[un.x];
+        r.sel_off = (uint32_t)sel_off[un.x];
+#pragma unroll
+        for (int i = 0; i < MPOS; ++i) r.pos[i] = i < r.nsel ? spos[r.sel_off + i] : 0u;
+        recs[u] = r;
+    }
+}
+
+__global__ void k_split_pairs(const int32_t* __restrict__ pair_codes, int64_t npairs, int nprobe,
+                              int32_t* __restrict__ pq, int32_t* __restrict__ psub) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs; i += (int64_t)gridDim.x * blockDim.x) {
+        const int code = pair_codes[i];
+        pq[i] = code / nprobe;
+        psub[i] = code % nprobe;
+    }
+}
+
+__device__ __forceinline__ float mma_pow2_scale(float norm2) {
+    const float n = sqrtf(norm2);
+    if (!(n > 0.f) || !isfinite(n)) return 1.f;
+    int e;
+    frexpf(n * 1.001f, &e);
+    return ldexpf(1.f, max(-120, min(120, 14 - e)));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+}  // namespace
+
+struct IvfMmaParams {
+    const __half* Qh;           // [nq][d] fp16 queries
+    const float* kinv;          // [nq]
+    const unsigned* xscale;     // max ||x||^2 of the payload (row scale)
+    int d;
+    const float* payload;
+    int nprobe;
+    const MmaRec* recs;
+    const int32_t* n_units;
+    const int32_t* pq;
+    const int32_t* psub;
+    const uint32_t* spos;
+    const float* pnorm;
+    const float* margin;
+    int ip, k;
+    CandBuf cb;
+    unsigned long long* visited;
+};
+
+template <bool IP>
+__global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int d = p.d, ld = d + 8;   // staged row stride (halves): +16 B keeps ldmatrix conflict-free
+    __half* As = reinterpret_cast<__half*>(smraw);                   // [MQ][ld]
+    __half* Bs = As + MQ * ld;                                       // [MN][ld]
+    float* red = reinterpret_cast<float*>(Bs + MN * ld);             // [MW][32][4] partial tiles
+    float* keys = red + MW * 32 * 4;                                 // [MQ][MN]
+    float* xn_s = keys + MQ * MN;                                    // [MN]
+    uint32_t* pos_s = reinterpret_cast<uint32_t*>(xn_s + MN);        // [MN]
+    int* pq_s = reinterpret_cast<int*>(pos_s + MN);                  // [MQ]
+    int* psub_s = pq_s + MQ;                                         // [MQ]
+    float* ks_s = reinterpret_cast<float*>(psub_s + MQ);             // [MQ] -2 kinv (or -kinv for IP)
+    int* cnt_s = reinterpret_cast<int*>(ks_s + MQ);                  // [MQ]
+    MmaRec* rec = reinterpret_cast<MmaRec*>(cnt_s + MQ);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = p.cb.C;
+    const int n_units = *p.n_units;
+    const float sx = mma_pow2_scale(__uint_as_float(*p.xscale));
+    const int ksteps = d / 16;
+    unsigned long long visited = 0;
+    for (int i = tid; i < (MQ + MN) * ld; i += MNT) As[i] = __float2half(0.f);
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        __syncthreads();   // previous unit fully consumed
+        if (tid < 32) reinterpret_cast<uint32_t*>(rec)[tid] = reinterpret_cast<const uint32_t*>(p.recs + u)[tid];
+        __syncthreads();
+        const int np = rec->np, nsel = rec->nsel, first = rec->first_pair;
+        // A: the unit's queries (16-byte cp.async from the fp16 copy), pair info
+        for (int r = warp; r < np; r += MW) {   // a warp per query row, no index division
+            const __half* src = p.Qh + (int64_t)__ldg(p.pq + first + r) * d;
+            for (int c8 = lane; c8 < d / 8; c8 += 32) cp_async16(As + r * ld + c8 * 8, src + c8 * 8);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (tid < MQ) {
+            const bool live = tid < np;
+            const int q = live ? __ldg(p.pq + first + tid) : 0;
+            pq_s[tid] = q;
+            psub_s[tid] = live ? __ldg(p.psub + first + tid) : 0;
+            const float kv = live ? __ldg(p.kinv + q) : 0.f;   // 2^-(eq+ex): both scales
+            ks_s[tid] = IP ? -kv : -2.f * kv;
+            cnt_s[tid] = 0;
+        }
+        if (tid == 0) visited += (unsigned long long)nsel * np;
+        for (int c0 = 0; c0 < nsel; c0 += MN) {
+            const int nr = min(MN, nsel - c0);
+            if (c0 > 0) __syncthreads();   // previous chunk's B tile and keys consumed
+            // B: warp w converts rows w and w + 4 (float4 loads, scaled to fp16)
+            for (int r = warp; r < MN; r += MW) {
+                __half* dst = Bs + r * ld;
+                if (r < nr) {
+                    const int rr = c0 + r;
+                    const uint32_t pos = rr < MPOS ? rec->pos[rr] : __ldg(p.spos + rec->sel_off + rr);
+                    const float4* src = reinterpret_cast<const float4*>(p.payload + (int64_t)pos * d);
+                    // all of the lane's loads in flight before the first conversion
+                    float4 v[MV];
+#pragma unroll
+                    for (int j = 0; j < MV; ++j) {
+                        const int c4 = lane + 32 * j;
+                        v[j] = c4 < d / 4 ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int j = 0; j < MV; ++j) {
+                        const int c4 = lane + 32 * j;
+                        if (c4 < d / 4) {
+                            const __half2 a = __floats2half2_rn(v[j].x * sx, v[j].y * sx);
+                            const __half2 b = __floats2half2_rn(v[j].z * sx, v[j].w * sx);
+                            uint2 w2;
+                            w2.x = *reinterpret_cast<const uint32_t*>(&a);
+                            w2.y = *reinterpret_cast<const uint32_t*>(&b);
+                            *reinterpret_cast<uint2*>(dst + c4 * 4) = w2;
+                        }
+                    }
+                    if (lane == 0) {
+                        pos_s[r] = pos;
+                        xn_s[r] = IP ? 0.f : __ldg(p.pnorm + pos);
+                    }
+                }
+            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            // MMA: this warp's K slice
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int a_row = lane & 15, a_col = (lane >> 4) * 8;   // ldmatrix x4: 16 rows x (2 x 8) cols
+            const int b_row = lane & 7, b_col = ((lane >> 3) & 1) * 8;
+            for (int ks = warp; ks < ksteps; ks += MW) {
+                uint32_t a[4], b[2];
+                ldsm_x4(a, As + a_row * ld + ks * 16 + a_col);
+                ldsm_x2(b, Bs + b_row * ld + ks * 16 + b_col);
+                mma_16816(acc, a, b);
+            }
+            *reinterpret_cast<float4*>(red + (warp * 32 + lane) * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            __syncthreads();
+            if (warp == 0) {
+                float4 s4 = *reinterpret_cast<const float4*>(red + lane * 4);
+#pragma unroll
+                for (int w = 1; w < MW; ++w) {
+                    const float4 t4 = *reinterpret_cast<const float4*>(red + (w * 32 + lane) * 4);
+                    s4.x += t4.x; s4.y += t4.y; s4.z += t4.z; s4.w += t4.w;
+                }
+                // lane (g, t): pairs g and g + 8, rows 2t and 2t + 1
+                const int g = lane >> 2, t = lane & 3;
+                const float v[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int pr = g + (j >> 1) * 8, rw = 2 * t + (j & 1);
+                    keys[pr * MN + rw] = IP ? v[j] * ks_s[pr] : fmaf(ks_s[pr], v[j], xn_s[rw]);
+                }
+            }
+            __syncthreads();
+            // appends: warp w serves pairs w, w + 4, ...; lane r holds row r
+            for (int pr = warp; pr < np; pr += MW) {
+                const int q = pq_s[pr];
+                const int64_t bidx = (int64_t)q * p.cb.n_sub + psub_s[pr];
+                float* ckey = p.cb.key + bidx * C;
+                uint32_t* cpos = p.cb.pos + bidx * C;
+                int cnt = cnt_s[pr];
+                const float key = lane < nr ? keys[pr * MN + lane] : 0.f;
+                bool adm = lane < nr;
+                if (cnt + nr > C) {   // full: keep the local top-k + margin band first
+                    float nthr;
+                    int lov = 0;
+                    cnt = compact_slow_sel(ckey, cpos, cnt, p.k, p.margin[q], C - 32, &nthr, &lov);
+                    if (lov && lane == 0) p.cb.overflow[q] = 1;
+                    adm = adm && key <= nthr;
+                }
+                const unsigned b = __ballot_sync(VS_FULL, adm);
+                if (adm) {
+                    const int slot = cnt + __popc(b & lanemask_lt());
+                    ckey[slot] = key;
+                    cpos[slot] = pos_s[lane];
+                }
+                if (lane == 0) cnt_s[pr] = cnt + __popc(b);
+            }
+        }
+        __syncthreads();
+        if (tid < np) p.cb.cnt[(int64_t)pq_s[tid] * p.cb.n_sub + psub_s[tid]] = cnt_s[tid];
+    }
+    if (tid == 0 && visited) atomicAdd(p.visited, visited);
+}
+
+// a priori bounds of the fp16 rows: max ||x~||^2 and max ||dx||^2 (float bits)
+// for k_tc_margins, from the payload's max ||x||^2
+__global__ void k_f16_row_bounds(const unsigned* __restrict__ xmax, int d, unsigned* __restrict__ out) {
+    const float x2 = __uint_as_float(*xmax);
+    const float sx = mma_pow2_scale(x2);
+    const float xn = sqrtf(x2) * 1.0001f;
+    const float dx = (xn * 4.8828125e-4f + sqrtf((float)d) * 2.9802322e-8f / sx) * 1.0001f;   // 2^-11, 2^-25
+    const float xt = xn + dx;
+    out[0] = __float_as_uint(xt * xt);
+    out[1] = __float_as_uint(dx * dx);
+}
+
+size_t ivf_mma_smem(int d) {
+    const size_t ld = (size_t)d + 8;
+    return (MQ + MN) * ld * 2 + (size_t)MW * 32 * 4 * 4 + (size_t)MQ * MN * 4 + (size_t)MN * 8 + (size_t)MQ * 16 +
+           sizeof(MmaRec) + 64;
+}
+
+cudaError_t launch_f16_row_bounds(const unsigned* xmax, int d, unsigned* out, cudaStream_t s) {
+    k_f16_row_bounds<<<1, 1, 0, s>>>(xmax, d, out);
+    return cudaGetLastError();
+}
+
 // setup (per search) + the scan; counts / sel_off / spos / recs are scratch
 // sized by the caller (ivf_sel_scratch)
 size_t ivf_sel_temp_bytes(int nlist) {
@@ -360,6 +626,44 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
     if ((e = cub::DeviceScan::ExclusiveSum(a.tmp, tb, a.lsel64, a.sel_off, a.nlist + 1, s)) != cudaSuccess) return e;
     k_list_sel_positions<<<lb, 256, 0, s>>>(a.list_off, a.nlist, a.pbits, a.sel_off, a.spos);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (a.mma) {
+        if (std::is_same<T, float>::value == false) return cudaErrorInvalidValue;
+        MmaRec* mrecs = reinterpret_cast<MmaRec*>(a.recs);
+        const int rb = (int)std::max<int64_t>(1, std::min<int64_t>((a.max_units + 255) / 256, 8192));
+        k_make_mma_recs<<<rb, 256, 0, s>>>(a.units, a.n_units, a.max_units, a.lsel, a.sel_off, a.spos, mrecs);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        const int64_t npairs = a.nq * (int64_t)a.nprobe;
+        k_split_pairs<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((npairs + 255) / 256, 4096)), 256, 0, s>>>(
+            a.pair_codes, npairs, a.nprobe, a.pq, a.psub);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        IvfMmaParams m;
+        m.Qh = a.Qh;
+        m.kinv = a.kinv;
+        m.xscale = a.xscale;
+        m.d = a.d;
+        m.payload = reinterpret_cast<const float*>(a.payload);
+        m.nprobe = a.nprobe;
+        m.recs = mrecs;
+        m.n_units = a.n_units;
+        m.pq = a.pq;
+        m.psub = a.psub;
+        m.spos = a.spos;
+        m.pnorm = a.pnorm;
+        m.margin = a.margin;
+        m.ip = a.ip;
+        m.k = a.k;
+        m.cb = a.cb;
+        m.visited = a.visited;
+        const size_t smem = ivf_mma_smem(a.d);
+        auto kern = a.ip ? k_ivf_scan_mma<true> : k_ivf_scan_mma<false>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+            return e;
+        int per_sm = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, MNT, smem)) != cudaSuccess) return e;
+        const int64_t grid = std::min<int64_t>((int64_t)a.sm_count * std::max(per_sm, 1), a.max_units);
+        kern<<<(unsigned)std::max<int64_t>(grid, 1), MNT, smem, s>>>(m);
+        return cudaGetLastError();
+    }
     UnitRec* recs = reinterpret_cast<UnitRec*>(a.recs);
     const int rb = (int)std::max<int64_t>(1, std::min<int64_t>((a.max_units + 255) / 256, 8192));
     k_make_recs<<<rb, 256, 0, s>>>(a.units, a.n_units, a.max_units, a.pair_codes, a.nprobe, a.lsel, a.sel_off, a.spos,

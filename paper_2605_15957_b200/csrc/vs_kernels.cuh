@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace vs {
@@ -174,12 +175,25 @@ struct IvfSelLaunch {
     int64_t* sel_off;
     uint32_t* spos;
     void* recs;
+    // tensor-core variant (float payload, d % 16 == 0): the batch's queries as
+    // fp16 with per-query power-of-two scales (kinv = 2^-(eq+ex)), rows scaled
+    // by pow2_scale(*xscale) when staged; units of <= kMmaPairs pairs
+    int mma = 0;
+    const __half* Qh = nullptr;
+    const float* kinv = nullptr;
+    const unsigned* xscale = nullptr;
+    int32_t* pq = nullptr;      // [nq * nprobe] scratch: pair -> query, probe rank
+    int32_t* psub = nullptr;
     void* tmp;
     size_t tmp_bytes;           // >= ivf_sel_temp_bytes(nlist)
     int sm_count;
 };
 constexpr size_t kIvfSelRecBytes = 128;
+constexpr int kMmaPairs = 16;       // filtered tensor-core scan: pairs per unit (MMA M)
 size_t ivf_sel_temp_bytes(int nlist);
+size_t ivf_mma_smem(int d);
+// a priori max ||x~||^2 / ||dx||^2 of fp16-rounded rows (scaled by their max norm)
+cudaError_t launch_f16_row_bounds(const unsigned* xmax, int d, unsigned* out, cudaStream_t s);
 template <typename T>
 cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s);
 __global__ void k_list_selected(const int64_t* __restrict__ list_off, int nlist, const uint32_t* __restrict__ pbits,

@@ -1509,6 +1509,24 @@ int tc_dense_keys(vs_ctx* ctx, const float* Q, int64_t nq, int d, const float* X
     return VS_OK;
 }
 
+// fp16 copy of a query batch (per-query power-of-two scales against rows of
+// max norm^2 *xmax) and its tensor-core margins against rows bounded by xmax2
+// (the filtered tensor-core IVF scan, vs_ivf_sel.cu)
+int tc_stage_queries_f16(vs_ctx* ctx, const float* Q, int64_t nq, int d, const unsigned* xmax,
+                         const unsigned* xmax2, int ip, __half* out, float* kinv, float* margin) {
+    using namespace vs_internal;
+    float2* qerr = nullptr;
+    CKS(arena_alloc(ctx, (size_t)nq, &qerr));
+    const int dp = (d + 7) / 8 * 8;
+    tc::k_stage_queries<__half><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nq * 32 + 255) / 256, 148 * 16)), 256,
+                                  0, ctx->stream>>>(Q, nq, d, dp, out, qerr, xmax, kinv);
+    CK(cudaGetLastError());
+    tc::k_tc_margins<<<(unsigned)((nq + 255) / 256), 256, 0, ctx->stream>>>(qerr, nq, d, xmax, xmax2, ip, margin);
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 2;
+    return VS_OK;
+}
+
 int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out) {
     using namespace vs_internal;
     if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");

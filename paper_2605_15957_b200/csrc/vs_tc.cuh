@@ -84,6 +84,8 @@ struct TcIvfOut {
     bool exhaustive;
 };
 int tc_ivf_scan(vs_ctx* ctx, const TcIvfArgs& a, TcIvfOut* out);
+int tc_stage_queries_f16(vs_ctx* ctx, const float* Q, int64_t nq, int d, const unsigned* xmax,
+                         const unsigned* xmax2, int ip, __half* out, float* kinv, float* margin);
 
 }  // namespace bn256
 

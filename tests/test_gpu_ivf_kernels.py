@@ -219,3 +219,32 @@ def test_tensor_core_scan_long_lists_cut_into_row_chunks(chunk_rows):
                        "squared_l2", mask, 3)
     finally:
         ctx.set_option(N.OPT_IVF_CHUNK_ROWS, 0)
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+@pytest.mark.parametrize("scale", [1.0, 1e-6, 1e5])
+def test_filtered_scan_tensor_core_and_simt(simt, metric, scale):
+    """The filtered list-major scan over pre-selected rows: its tensor-core
+    variant (mma.sync, fp16 operands with power-of-two scales, tensor-core
+    margins) and the fp32 SIMT one (VS_OPT_ENN_KERNEL=1) both give the
+    reference's exact result, also for magnitudes outside fp16's range and
+    mixed query magnitudes; lists hold more selected rows than one 8-row chunk."""
+    rng = np.random.default_rng(int(simt) * 10 + int(np.log10(scale)) + 20)
+    n, d, nlist = 16000, 128, 24
+    idx, data, centroids, parts, payload = _index(rng, n, d, nlist, metric)
+    if scale != 1.0:
+        data = (data * scale).astype(np.float32)
+        centroids = (centroids * scale).astype(np.float32)
+        payload = [p * np.float32(scale) for p in payload]
+        idx = vs.IvfIndex(nlist, d, n, metric, "owning", centroids, parts, payload)
+    queries = (rng.standard_normal((90, d)) * scale).astype(np.float32)
+    queries[::5] *= np.float32(300.0)
+    mask = rng.random(n) < 0.15
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_ENN_KERNEL, 1 if simt else 0)
+    try:
+        for nprobe, k in ((3, 10), (10, 40)):
+            _check(idx, queries, centroids, parts, payload, nprobe, k, metric, mask, 2)
+    finally:
+        ctx.set_option(N.OPT_ENN_KERNEL, 0)
