@@ -337,6 +337,8 @@ int enn_phase_b(vs_ctx* ctx, const EnnJob& job, const PhaseA& st, int cshift, bo
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_key));
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_id));
     CKS(arena_alloc(ctx, (size_t)job.nq, &rp.s_count));
+    CKS(arena_alloc(ctx, (size_t)job.nq, &rp.fb_list));
+    CKS(arena_alloc(ctx, 1, &rp.fb_count));
     rp.out_ids = job.out_ids;
     rp.out_dist = job.out_dist;
     rp.out_ids32 = job.out_ids32;
@@ -1918,6 +1920,8 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_key));
     CKS(arena_alloc(ctx, (size_t)job.nq * rp.s_cap, &rp.s_id));
     CKS(arena_alloc(ctx, (size_t)job.nq, &rp.s_count));
+    CKS(arena_alloc(ctx, (size_t)job.nq, &rp.fb_list));
+    CKS(arena_alloc(ctx, 1, &rp.fb_count));
     rp.out_ids = job.out_ids;
     rp.out_dist = job.out_dist;
     rp.out_ids32 = nullptr;

@@ -464,6 +464,17 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
         if (tid < 32) reinterpret_cast<uint32_t*>(rec)[tid] = reinterpret_cast<const uint32_t*>(p.recs + u)[tid];
         __syncthreads();
         const int np = rec->np, nsel = rec->nsel, first = rec->first_pair;
+        // the next unit's rows -> L2 (one bulk prefetch per row), so its B
+        // staging below waits on L2 instead of HBM
+        if (warp == MW - 1 && u + (int)gridDim.x < n_units) {
+            const uint32_t wv = reinterpret_cast<const uint32_t*>(p.recs + u + gridDim.x)[lane];
+            const int nsel_n = __shfl_sync(VS_FULL, (int)wv, 2);
+            const int j = lane - 5;   // word 5 + j holds pos[j]
+            if (j >= 0 && j < min(nsel_n, MPOS))
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.payload + (int64_t)wv * d),
+                             "r"(d * 4)
+                             : "memory");
+        }
         // A: the unit's queries (16-byte cp.async from the fp16 copy), pair info
         for (int r = warp; r < np; r += MW) {   // a warp per query row, no index division
             const __half* src = p.Qh + (int64_t)__ldg(p.pq + first + r) * d;

@@ -248,6 +248,13 @@ struct RerankParams {
                                       //      exact key (distance, or -score) above this bound
     float* out_kth = nullptr;         // [nq][k] write this shard's k smallest approximate keys
                                       //      (ascending, +inf padded) and stop
+    // one-warp-per-query kernel for small k (k_rerank_warp): queries beyond its
+    // capacity are listed in fb_list / fb_count ([nq] + 1, caller-allocated,
+    // nullable: CTA kernel only) and re-ranked by the CTA kernel over q_list
+    int32_t* fb_list = nullptr;
+    int32_t* fb_count = nullptr;
+    const int32_t* q_list = nullptr;
+    const int32_t* q_count = nullptr;
     int band_ready = 0;         // the single buffer per query already holds exactly the
                                 //      margin band of its k-th key: every entry survives
     int ubytes;                 // filled by launch_rerank: shared-memory union size

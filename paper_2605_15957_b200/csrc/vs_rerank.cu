@@ -615,7 +615,8 @@ __global__ void __launch_bounds__(NT, PH == 1 ? 5 : (WIDE ? 2 : 4)) k_rerank(Rer
     double* qd = reinterpret_cast<double*>(hist + HBINS);                    // [q_stride] float64, skewed
 
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    const int64_t q = blockIdx.x;
+    if (p.q_list && (int)blockIdx.x >= *p.q_count) return;   // the whole CTA: no barrier is reached
+    const int64_t q = p.q_list ? (int64_t)p.q_list[blockIdx.x] : (int64_t)blockIdx.x;
     const int C = p.cb.C;
     // buffers of this query: fixed n_sub per query, or a flat range (IVF list chunks)
     const int64_t bbase = p.cb.sub_off ? p.cb.sub_off[q] : q * (int64_t)p.cb.n_sub;
@@ -1559,6 +1560,231 @@ __global__ void __launch_bounds__(NT) k_union_kth(const float* __restrict__ keys
     if (threadIdx.x == 0) out[q] = o2f(ukeys[k - 1]);
 }
 
+// ---- phase B for small k: one warp per query -----------------------------------------------
+// The IVF probes (k = nprobe), IVF lists and small exhaustive searches have
+// a few dozen to a few hundred candidates and ~k survivors per query: the
+// 256-thread CTA of k_rerank spent most of its time in barriers of its
+// radix passes and bitonic sort. Here a warp does the whole query with warp
+// primitives only: candidates -> shared memory (lane per buffer), k-th key
+// by a bitwise search (warp_kth), survivors, exact float64 scores (query
+// elements in registers, numpy's order as warp_np_score_reg1), a warp
+// bitonic sort under the tie rule, output. Queries whose candidates or
+// survivors exceed the warp's capacity are listed for the CTA kernel.
+namespace {
+constexpr int WW = 4;          // warps (queries) per CTA
+constexpr int WL = 512;        // candidates per warp
+constexpr int WS = 128;        // survivors per warp (sort capacity)
+
+struct WarpSmem {
+    uint32_t ck[WW][WL];       // orderable approximate keys
+    uint32_t cp[WW][WL];       // positions
+    uint64_t sk[WW][WS];       // orderable exact keys
+    int64_t si[WW][WS];        // output ids
+    int cnt[WW];
+};
+
+// exact float64 score of one register-held row against register-held query
+// elements (lane (L, p): elements off_L + 2p + {0, 1} + 8m of leaf L)
+template <bool IP>
+__device__ __forceinline__ double warp_score_regq(const float2 (&qv)[16], const float2 (&xa)[16], int M,
+                                                  const float* qt, const float* xt, int ntail, const TreeLane& tl,
+                                                  int lane) {
+    double a0 = 0.0, a1 = 0.0;
+    if (M > 0) {
+        a0 = term_d<IP>(qv[0].x, xa[0].x);
+        a1 = term_d<IP>(qv[0].y, xa[0].y);
+    }
+#pragma unroll
+    for (int m = 1; m < 16; ++m) {
+        if (m < M) {
+            a0 = __dadd_rn(a0, term_d<IP>(qv[m].x, xa[m].x));
+            a1 = __dadd_rn(a1, term_d<IP>(qv[m].y, xa[m].y));
+        }
+    }
+    double va = __dadd_rn(a0, a1);
+    va = __dadd_rn(va, __shfl_xor_sync(VS_FULL, va, 1));
+    va = __dadd_rn(va, __shfl_xor_sync(VS_FULL, va, 2));
+    for (int i = 0; i < ntail; ++i) va = __dadd_rn(va, term_d<IP>(qt[i], xt[i]));
+    double sa = __shfl_sync(VS_FULL, va, (lane * 4) & 31);
+    for (int l = 0; l < tl.nlevels; ++l) {
+        const double pa = __shfl_sync(VS_FULL, sa, tl.na), qa = __shfl_sync(VS_FULL, sa, tl.nb);
+        if (tl.lvl == l) sa = __dadd_rn(pa, qa);
+    }
+    return __shfl_sync(VS_FULL, sa, tl.root);
+}
+}  // namespace
+
+template <typename T, bool IP>
+__global__ void __launch_bounds__(WW * 32, 4) k_rerank_warp(RerankParams p, int32_t* fb_list, int32_t* fb_count) {
+    __shared__ LeafPlan plan;
+    __shared__ WarpSmem S;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        const int* src = reinterpret_cast<const int*>(&p.plan);
+        int* dst = reinterpret_cast<int*>(&plan);
+        for (int i = threadIdx.x; i < (int)(sizeof(LeafPlan) / 4); i += WW * 32) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int64_t q = (int64_t)blockIdx.x * WW + w;
+    if (q >= p.nq) return;   // warp-uniform; no block barriers below
+    const int d = p.d, C = p.cb.C;
+    uint32_t* ck = S.ck[w];
+    uint32_t* cp = S.cp[w];
+    // 1. live candidates (lane per buffer)
+    const int64_t bbase = p.cb.sub_off ? p.cb.sub_off[q] : q * (int64_t)p.cb.n_sub;
+    const int nsub = p.cb.sub_off ? (int)(p.cb.sub_off[q + 1] - bbase) : p.cb.n_sub;
+    const uint32_t pre = p.tau_g ? p.tau_g[q] : 0xffffffffu;
+    if (lane == 0) S.cnt[w] = 0;
+    __syncwarp();
+    bool ovf = false;
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int s0 = 0; s0 < nsub; s0 += 32) {
+        const int s = s0 + lane;
+        const int c = s < nsub ? p.cb.cnt[bbase + s] : 0;
+        const float* bk = p.cb.key + (bbase + s) * (int64_t)C;
+        const uint32_t* bp = p.cb.pos + (bbase + s) * (int64_t)C;
+        for (int j = 0; j < c; ++j) {
+            const uint32_t o = f2o(bk[j]);
+            if (o > pre) continue;
+            const int slot = atomicAdd(&S.cnt[w], 1);
+            if (slot < WL) {
+                ck[slot] = o;
+                cp[slot] = bp[j];
+                lo = min(lo, o);
+                hi = max(hi, o);
+            }
+        }
+    }
+    __syncwarp();
+    const int nl = S.cnt[w];
+    ovf = nl > WL;
+    int ns = 0;
+    if (!ovf) {
+        // 2. survivors: keys <= k-th key + margin (all of them for a ready band)
+        uint32_t thr = 0xffffffffu;
+        if (!p.band_ready && nl > p.k) {
+            lo = __reduce_min_sync(VS_FULL, lo);
+            hi = __reduce_max_sync(VS_FULL, hi);
+            const uint32_t kth = warp_kth(ck, nl, (unsigned)p.k, lo, hi, lane);
+            thr = f2o(__fadd_ru(o2f(kth), p.margin[q]));
+        }
+        for (int i0 = 0; i0 < nl; i0 += 32) {
+            const int i = i0 + lane;
+            const bool live = i < nl && ck[i] <= thr;
+            const unsigned b = __ballot_sync(VS_FULL, live);
+            const int slot = ns + __popc(b & lanemask_lt());
+            // compaction in place: slot <= i, and every lane reads before any writes
+            const uint32_t pos = live ? cp[i] : 0u;
+            __syncwarp();
+            if (live) cp[slot] = pos;
+            __syncwarp();
+            ns += __popc(b);
+        }
+        ovf = ns > WS;
+    }
+    if (ovf) {   // the CTA kernel takes this query
+        if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+        return;
+    }
+    // 3. exact float64 scores; the query's elements of this lane in registers
+    const int L = lane >> 2, pp = lane & 3;
+    const bool on = L < plan.nleaf;
+    const int offL = on ? plan.leaf_off[L] : 0, nL = on ? plan.leaf_n[L] : 0;
+    const int M = nL / 8;
+    const int ntail = pp == 0 ? nL - 8 * M : 0;
+    TreeLane tl;
+    {
+        const int sj = lane - plan.nleaf;
+        const bool isnode = sj >= 0 && sj < plan.nnode;
+        tl.na = isnode ? plan.node_a[sj] : lane;
+        tl.nb = isnode ? plan.node_b[sj] : lane;
+        tl.lvl = isnode ? plan.node_lvl[sj] : -1;
+        tl.nlevels = plan.nlevels;
+        tl.nleaf = plan.nleaf;
+        tl.root = plan.nnode ? plan.nleaf + plan.nnode - 1 : 0;
+    }
+    const float* qg = p.Q + q * (int64_t)d + offL + 2 * pp;
+    float2 qv[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) qv[m] = m < M ? *reinterpret_cast<const float2*>(qg + 8 * m) : make_float2(0.f, 0.f);
+    float qt[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qt[i] = i < ntail ? p.Q[q * (int64_t)d + offL + 8 * M + i] : 0.f;
+    const T* rows = reinterpret_cast<const T*>(p.rows);
+    const int row_bytes = d * (int)sizeof(T);
+    auto row_of = [&](int j) -> int64_t {
+        const uint32_t ps = cp[j];
+        return p.row_map ? p.row_map[ps] : (int64_t)ps;
+    };
+    auto prefetch_row = [&](int64_t r) {
+        const char* base = reinterpret_cast<const char*>(rows + r * (int64_t)d);
+        for (int o = lane * 128; o < row_bytes; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
+    };
+    constexpr int PD = 3;
+    for (int j = 1; j <= PD && j < ns; ++j) prefetch_row(row_of(j));
+    uint64_t* sk = S.sk[w];
+    int64_t* si = S.si[w];
+    for (int j = 0; j < ns; ++j) {
+        const uint32_t ps = cp[j];
+        const int64_t r = p.row_map ? p.row_map[ps] : (int64_t)ps;
+        const T* xg = rows + r * (int64_t)d + offL + 2 * pp;
+        float2 xa[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) xa[m] = m < M ? Pair2<T>::ld(xg + 8 * m) : make_float2(0.f, 0.f);
+        if (j + PD + 1 < ns) prefetch_row(row_of(j + PD + 1));
+        float xt[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xt[i] = i < ntail ? ld_elem(rows + r * (int64_t)d + offL + 8 * M + i) : 0.f;
+        const double sc = warp_score_regq<IP>(qv, xa, M, qt, xt, ntail, tl, lane);
+        if (lane == 0) {
+            sk[j] = d2o(IP ? -sc : sc);
+            si[j] = (p.id_map ? p.id_map[ps] : r) + p.id_offset;
+        }
+    }
+    __syncwarp();
+    // 4. tie-rule top-k: warp bitonic sort of (exact key, id)
+    int P = 1;
+    while (P < ns) P <<= 1;
+    for (int i = ns + lane; i < P; i += 32) {
+        sk[i] = ~0ull;
+        si[i] = 0x7fffffffffffffffll;
+    }
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = lane; i < P / 2; i += 32) {
+                const int lo_i = 2 * i - (i & (stride - 1));
+                const int hi_i = lo_i + stride;
+                const bool asc = ((lo_i & size) == 0);
+                const uint64_t ka = sk[lo_i], kb = sk[hi_i];
+                const int64_t ia = si[lo_i], ib = si[hi_i];
+                const bool gt = (ka > kb) || (ka == kb && ia > ib);
+                if (gt == asc) {
+                    sk[lo_i] = kb; sk[hi_i] = ka;
+                    si[lo_i] = ib; si[hi_i] = ia;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (p.n_survivors && lane == 0) atomicAdd(p.n_survivors, (unsigned long long)ns);
+    const int keff = min(p.k, ns);
+    for (int r = lane; r < p.k; r += 32) {
+        const int64_t o = q * (int64_t)p.k + r;
+        if (r < keff) {
+            const double key_d = o2d(sk[r]);
+            if (p.out_ids) p.out_ids[o] = si[r];
+            if (p.out_ids32) p.out_ids32[o] = (int32_t)si[r];
+            if (p.out_dist) p.out_dist[o] = IP ? -key_d : key_d;
+        } else {
+            if (p.out_ids) p.out_ids[o] = -1;
+            if (p.out_ids32) p.out_ids32[o] = -1;
+            if (p.out_dist) p.out_dist[o] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
+    if (lane == 0 && p.out_count) p.out_count[q] = keff;
+}
+
 static size_t rerank_smem(int d, int nsub, size_t ubytes, int ph) {
     const size_t chains =
         (reg_path_ok(d) || ph == 1) ? 0 : (size_t)NWARP * 8 * MAXLEAF * 8 + (size_t)NWARP * 2 * MAXLEAF * 8;
@@ -1601,6 +1827,20 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         if (wide) return p.ip ? launch_rerank_v<T, true, true, 2>(p, s) : launch_rerank_v<T, false, true, 2>(p, s);
         return p.ip ? launch_rerank_v<T, true, false, 2>(p, s) : launch_rerank_v<T, false, false, 2>(p, s);
+    }
+    // small k without verification or distributed hooks: one warp per query,
+    // the CTA kernel only for the queries it lists (VS_RR_WARP=0 disables)
+    static const int warp_env = getenv("VS_RR_WARP") ? atoi(getenv("VS_RR_WARP")) : 1;
+    if (warp_env && p.fb_list && p.fb_count && p.reg_path && p.k <= 64 && !p.verify && !p.out_bound && !p.out_kth &&
+        !p.ext_thr && !p.q_list) {
+        cudaError_t e = cudaMemsetAsync(p.fb_count, 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return e;
+        const unsigned grid = (unsigned)((p.nq + WW - 1) / WW);
+        if (p.ip) k_rerank_warp<T, true><<<grid, WW * 32, 0, s>>>(p, p.fb_list, p.fb_count);
+        else k_rerank_warp<T, false><<<grid, WW * 32, 0, s>>>(p, p.fb_list, p.fb_count);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        p.q_list = p.fb_list;
+        p.q_count = p.fb_count;
     }
     if (wide) return p.ip ? launch_rerank_v<T, true, true, 0>(p, s) : launch_rerank_v<T, false, true, 0>(p, s);
     return p.ip ? launch_rerank_v<T, true, false, 0>(p, s) : launch_rerank_v<T, false, false, 0>(p, s);
