@@ -1572,9 +1572,10 @@ __global__ void __launch_bounds__(NT) k_union_kth(const float* __restrict__ keys
 // survivors exceed the warp's capacity are listed for the CTA kernel.
 namespace {
 constexpr int WW = 4;          // warps (queries) per CTA
-constexpr int WL = 512;        // candidates per warp
 constexpr int WS = 128;        // survivors per warp (sort capacity)
 
+// WL: candidates per warp
+template <int WL>
 struct WarpSmem {
     uint32_t ck[WW][WL];       // orderable approximate keys
     uint32_t cp[WW][WL];       // positions
@@ -1614,10 +1615,11 @@ __device__ __forceinline__ double warp_score_regq(const float2 (&qv)[16], const 
 }
 }  // namespace
 
-template <typename T, bool IP>
+template <typename T, bool IP, int WL>
 __global__ void __launch_bounds__(WW * 32, 4) k_rerank_warp(RerankParams p, int32_t* fb_list, int32_t* fb_count) {
     __shared__ LeafPlan plan;
-    __shared__ WarpSmem S;
+    extern __shared__ __align__(16) unsigned char wsm[];
+    WarpSmem<WL>& S = *reinterpret_cast<WarpSmem<WL>*>(wsm);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {
         const int* src = reinterpret_cast<const int*>(&p.plan);
@@ -1818,6 +1820,14 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     // kernel runs at 5 CTAs/SM without the scorer's registers, then score +
     // top-k (measured: config 2 re-rank 2.06 -> 1.90 ms; the narrow build
     // already runs 4 CTAs/SM and the split cost config 3 0.09 ms)
+    // the distributed k-th-key pass (out_kth) is steps 0-2 only: the select
+    // kernel's occupancy without the scorer
+    static const int kth_env = getenv("VS_RR_KTH_SELECT") ? atoi(getenv("VS_RR_KTH_SELECT")) : 1;
+    if (p.out_kth && kth_env) {
+        RerankParams p1 = p;
+        p1.ubytes = (int)union_min<false>();
+        return p.ip ? launch_rerank_v<T, true, false, 1>(p1, s) : launch_rerank_v<T, false, false, 1>(p1, s);
+    }
     static const int split_env = getenv("VS_RR_SPLIT") ? atoi(getenv("VS_RR_SPLIT")) : -1;
     const bool split = split_env >= 0 ? split_env == 1 : wide;
     if (split && p.s_count && !p.out_kth) {
@@ -1831,13 +1841,18 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     // small k without verification or distributed hooks: one warp per query,
     // the CTA kernel only for the queries it lists (VS_RR_WARP=0 disables)
     static const int warp_env = getenv("VS_RR_WARP") ? atoi(getenv("VS_RR_WARP")) : 1;
-    if (warp_env && p.fb_list && p.fb_count && p.reg_path && p.k <= 64 && !p.verify && !p.out_bound && !p.out_kth &&
-        !p.ext_thr && !p.q_list) {
+    // (not for many buffers per query: config 4's 128 margin-band buffers hold
+    // more candidates than a warp stages, and the fallback then doubles the work)
+    if (warp_env && p.fb_list && p.fb_count && p.reg_path && p.k <= 64 && p.cb.n_sub <= 64 && !p.verify &&
+        !p.out_bound && !p.out_kth && !p.ext_thr && !p.q_list) {
         cudaError_t e = cudaMemsetAsync(p.fb_count, 0, sizeof(int32_t), s);
         if (e != cudaSuccess) return e;
         const unsigned grid = (unsigned)((p.nq + WW - 1) / WW);
-        if (p.ip) k_rerank_warp<T, true><<<grid, WW * 32, 0, s>>>(p, p.fb_list, p.fb_count);
-        else k_rerank_warp<T, false><<<grid, WW * 32, 0, s>>>(p, p.fb_list, p.fb_count);
+        auto kern = p.ip ? k_rerank_warp<T, true, 512> : k_rerank_warp<T, false, 512>;
+        const size_t smem = sizeof(WarpSmem<512>);
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+            return e;
+        kern<<<grid, WW * 32, smem, s>>>(p, p.fb_list, p.fb_count);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         p.q_list = p.fb_list;
         p.q_count = p.fb_count;
