@@ -1581,7 +1581,7 @@ struct WarpSmem {
     uint32_t cp[WW][WL];       // positions
     uint64_t sk[WW][WS];       // orderable exact keys
     int64_t si[WW][WS];        // output ids
-    int cnt[WW];
+    int pref[WW][65];          // buffer count prefix (<= 64 buffers)
 };
 
 // exact float64 score of one register-held row against register-held query
@@ -1632,33 +1632,56 @@ __global__ void __launch_bounds__(WW * 32, 4) k_rerank_warp(RerankParams p, int3
     const int d = p.d, C = p.cb.C;
     uint32_t* ck = S.ck[w];
     uint32_t* cp = S.cp[w];
-    // 1. live candidates (lane per buffer)
+    // 1. live candidates: the buffers' counts (a lane per buffer, <= 64 of
+    //    them), a warp prefix sum, then every lane walks flat entry indices
+    //    (f -> buffer by a search over the prefix), four loads in flight
     const int64_t bbase = p.cb.sub_off ? p.cb.sub_off[q] : q * (int64_t)p.cb.n_sub;
     const int nsub = p.cb.sub_off ? (int)(p.cb.sub_off[q + 1] - bbase) : p.cb.n_sub;
     const uint32_t pre = p.tau_g ? p.tau_g[q] : 0xffffffffu;
-    if (lane == 0) S.cnt[w] = 0;
-    __syncwarp();
-    bool ovf = false;
-    uint32_t lo = 0xffffffffu, hi = 0u;
+    int* pref = S.pref[w];   // [nsub + 1] exclusive prefix of the counts
+    int tot = 0;
     for (int s0 = 0; s0 < nsub; s0 += 32) {
         const int s = s0 + lane;
         const int c = s < nsub ? p.cb.cnt[bbase + s] : 0;
-        const float* bk = p.cb.key + (bbase + s) * (int64_t)C;
-        const uint32_t* bp = p.cb.pos + (bbase + s) * (int64_t)C;
-        for (int j = 0; j < c; ++j) {
-            const uint32_t o = f2o(bk[j]);
-            if (o > pre) continue;
-            const int slot = atomicAdd(&S.cnt[w], 1);
-            if (slot < WL) {
-                ck[slot] = o;
-                cp[slot] = bp[j];
-                lo = min(lo, o);
-                hi = max(hi, o);
-            }
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(VS_FULL, incl, o);
+            if (lane >= o) incl += t;
         }
+        if (s < nsub) pref[s] = tot + incl - c;
+        tot += __shfl_sync(VS_FULL, incl, 31);
+    }
+    if (lane == 0) pref[nsub] = tot;
+    __syncwarp();
+    bool ovf = false;
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    int nl = 0;
+    for (int f0 = 0; f0 < tot; f0 += 32) {
+        const int f = f0 + lane;
+        uint32_t o = 0xffffffffu, ps = 0u;
+        if (f < tot) {
+            int a = 0, b = nsub - 1;   // last buffer with pref <= f
+            while (a < b) {
+                const int m = (a + b + 1) >> 1;
+                if (pref[m] <= f) a = m; else b = m - 1;
+            }
+            const int64_t e = (bbase + a) * (int64_t)C + (f - pref[a]);
+            o = f2o(p.cb.key[e]);
+            if (o <= pre) ps = p.cb.pos[e];
+        }
+        const bool live = f < tot && o <= pre;
+        const unsigned bl = __ballot_sync(VS_FULL, live);
+        const int slot = nl + __popc(bl & lanemask_lt());
+        if (live && slot < WL) {
+            ck[slot] = o;
+            cp[slot] = ps;
+            lo = min(lo, o);
+            hi = max(hi, o);
+        }
+        nl += __popc(bl);
     }
     __syncwarp();
-    const int nl = S.cnt[w];
     ovf = nl > WL;
     int ns = 0;
     if (!ovf) {
