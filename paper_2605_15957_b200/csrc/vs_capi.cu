@@ -71,6 +71,23 @@ int stage_out(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& p
     pending.push_back(OutBuf{(void*)dst, (void*)d, count * sizeof(T)});
     return VS_OK;
 }
+// final outputs (written once by the last kernels, never read back): a
+// page-locked host buffer is written in place by the kernels over PCIe
+// (zero-copy), so the result transfer overlaps phase B instead of following
+// it (VS_ZERO_COPY_OUT=0 stages them like any host buffer)
+template <typename T>
+int stage_out_final(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& pending, bool allow) {
+    static const bool zc_env = !(getenv("VS_ZERO_COPY_OUT") && getenv("VS_ZERO_COPY_OUT")[0] == '0');
+    if (allow && zc_env && dst && !is_device_ptr(dst)) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, dst) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer) {
+            *dev = static_cast<T*>(a.devicePointer);
+            return VS_OK;
+        }
+        cudaGetLastError();
+    }
+    return stage_out(ctx, dst, count, dev, pending);
+}
 int flush_out(vs_ctx* ctx, std::vector<OutBuf>& pending) {
     for (auto& o : pending)
         if (o.bytes) CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -956,9 +973,10 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     job.ip = metric;
     job.k = k;
     job.id_offset = id_offset;
-    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending));
-    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
-    CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
+    const bool zc = !col->host_resident && k <= kTopkCap;   // outputs written once, by phase B
+    CKS(stage_out_final(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending, zc));
+    CKS(stage_out_final(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending, zc));
+    CKS(stage_out_final(ctx, out_count, (size_t)nq, &job.out_count, pending, zc));
     job.out_ids32 = nullptr;
     if (col->host_resident && k <= kTopkCap) {
         CKS(enn_search_streamed(ctx, col, dq, nq, d, sel, nsel, k, metric, id_offset, margin, job.out_ids,
@@ -2154,9 +2172,9 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     job.pbits = pbits;
     job.k = k;
     job.visited = vis;
-    CKS(stage_out(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending));
-    CKS(stage_out(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending));
-    CKS(stage_out(ctx, out_count, (size_t)nq, &job.out_count, pending));
+    CKS(stage_out_final(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending, k <= kTopkCap));
+    CKS(stage_out_final(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending, k <= kTopkCap));
+    CKS(stage_out_final(ctx, out_count, (size_t)nq, &job.out_count, pending, k <= kTopkCap));
     if (!job.out_ids) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_ids));
     if (!job.out_dist) CKS(arena_alloc(ctx, (size_t)nq * k, &job.out_dist));
     if (!job.out_count) CKS(arena_alloc(ctx, (size_t)nq, &job.out_count));

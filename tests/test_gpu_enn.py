@@ -238,3 +238,31 @@ def test_borrowed_column_mutation_invalidates_norms():
     ref = O.enn_search(q, t.cpu().numpy(), 10)
     assert np.array_equal(got.data_row, ref.data_row)
     assert np.array_equal(got.distance, ref.distance)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_pinned_host_outputs_written_in_place(kernel):
+    """Page-locked host output buffers are written by the kernels over PCIe
+    (zero-copy final outputs): same results as the oracle, with tensor-core
+    and SIMT phase A (their verification re-runs scatter into the same
+    buffers)."""
+    import torch
+    from paper_2605_15957_b200.vecindex import enn_search_raw
+    rng = np.random.default_rng(41 + kernel)
+    data = rng.standard_normal((20000, 96)).astype(np.float32)
+    q = rng.standard_normal((300, 96)).astype(np.float32)
+    mask = rng.random(20000) < 0.2
+    k = 24
+    out = (torch.full((300, k), 7, dtype=torch.int64).pin_memory(),
+           torch.zeros((300, k), dtype=torch.float64).pin_memory(),
+           torch.zeros(300, dtype=torch.int32).pin_memory())
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_ENN_KERNEL, kernel)
+    try:
+        enn_search_raw(torch.from_numpy(q).pin_memory(), data, k, row_filter=mask, out=out)
+    finally:
+        ctx.set_option(N.OPT_ENN_KERNEL, 0)
+    ref = O.enn_filtered(q, data, mask, k)
+    assert np.array_equal(out[2].numpy(), np.full(300, k, np.int32))
+    assert np.array_equal(out[0].numpy().reshape(-1), ref.data_row)
+    assert np.array_equal(out[1].numpy().reshape(-1), ref.distance)

@@ -248,3 +248,23 @@ def test_filtered_scan_tensor_core_and_simt(simt, metric, scale):
             _check(idx, queries, centroids, parts, payload, nprobe, k, metric, mask, 2)
     finally:
         ctx.set_option(N.OPT_ENN_KERNEL, 0)
+
+
+def test_ivf_pinned_host_outputs_written_in_place():
+    """IVF search into page-locked host buffers (zero-copy final outputs)."""
+    rng = np.random.default_rng(77)
+    n, d, nlist = 12000, 64, 32
+    idx, data, centroids, parts, payload = _index(rng, n, d, nlist)
+    queries = rng.standard_normal((150, d)).astype(np.float32)
+    mask = rng.random(n) < 0.3
+    k, nprobe = 12, 5
+    out = (torch.full((150, k), 7, dtype=torch.int64).pin_memory(),
+           torch.zeros((150, k), dtype=torch.float64).pin_memory(),
+           torch.zeros(150, dtype=torch.int32).pin_memory())
+    idx.search_raw(torch.from_numpy(queries).pin_memory(), k, nprobe, row_filter=mask, out=out)
+    ref = O.ivf_search(queries, centroids, parts, lambda c: payload[c], nprobe, k, mask=mask)
+    cnt = out[2].numpy()
+    ids = np.concatenate([out[0].numpy()[i, :cnt[i]] for i in range(150)])
+    dist = np.concatenate([out[1].numpy()[i, :cnt[i]] for i in range(150)])
+    assert np.array_equal(ids, ref.data_row)
+    assert np.array_equal(dist, ref.distance)
