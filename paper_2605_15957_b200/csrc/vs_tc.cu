@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int64_t it = unit; it < nitems; it += nunits) {
             const Item item = decode_item<MODE, QTILE>(p, it);
             const int64_t q = item.a_row + (int64_t)rank * BM + row;
-            float* krow = p.keys_out + (q < p.nq ? q : 0) * p.keys_ld;
+            float* krow = p.keys_out ? p.keys_out + (q < p.nq ? q : 0) * p.keys_ld : nullptr;   // nullable: minima only
             // key = ||x||^2 - 2 q.x (or -q.x) with q.x = acc x 2^-(scales): exact factor
             const float ks = (p.kinv && q < p.nq) ? __ldg(p.kinv + q) : 1.f;
             const float cmul = IP ? -ks : -2.f * ks;
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             if (cb0 + j < ncols) mn = fminf(mn, kv[j]);
                         p.mins_out[q * p.mins_ld + ((r0 + cb0) >> 5)] = mn;
                     }
-                    if (q < p.nq) {
+                    if (q < p.nq && krow) {
                         float* dst = krow + r0 + cb0;
                         if (cb0 + 32 <= ncols && ((p.keys_ld | r0) & 3) == 0) {
 #pragma unroll
@@ -1097,6 +1097,42 @@ __global__ void k_tc_margins(const float2* __restrict__ qerr, int64_t nq, int d,
     margin[i] = 2.f * e * 1.01f;
 }
 
+// admission-bound seed: U = k-th smallest of a query's chunk minima over a
+// sample of rows (the first `nch` x 32 staged rows, MODE 3 with minima only)
+// is an upper bound on its k-th smallest key over all rows (k rows of the
+// sample have key <= U), so phase A may start with tau_g = U instead of
+// +inf (phase B's verification covers it like any tau_g). One warp per query.
+__global__ void k_tau_seed(const float* __restrict__ mins, int64_t nq, int nch, int k, const float* __restrict__ margin,
+                           unsigned* __restrict__ tau) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (q >= nq) return;
+    const float* m = mins + q * (int64_t)nch;
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = lane; i < nch; i += 32) {
+        const uint32_t u = f2o(m[i]);
+        lo = min(lo, u);
+        hi = max(hi, u);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    uint32_t res = lo;
+    if (lo != hi) {
+        const int top = 31 - __clz(lo ^ hi);
+        res = lo & ~((top == 31 ? 0u : (2u << top)) - 1u);
+        for (int b = top; b >= 0; --b) {
+            const uint32_t t = res | (1u << b);
+            unsigned c = 0;
+            for (int i = lane; i < nch; i += 32) c += f2o(m[i]) < t ? 1u : 0u;
+            c = __reduce_add_sync(0xffffffffu, c);
+            if (c < (unsigned)k) res = t;
+        }
+    }
+    // + 1.5 margins: the verification (k-th exact key + margin/2 below tau_g
+    // - margin/2) then holds even when U is the k-th key itself
+    if (lane == 0) tau[q] = f2o(__fadd_ru(o2f(res), 1.5f * margin[q]));
+}
+
 }  // namespace tc
 
 // ---- host side ---------------------------------------------------------------------------------------------
@@ -1322,6 +1358,41 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
     static const int lim0_env = getenv("VS_TC_LIM0") ? atoi(getenv("VS_TC_LIM0")) : 0;
     pr.lim0 = lim0_env;
     pr.dense_direct = (per >= 8 && per < 128) ? 1 : 0;
+    // admission-bound seed from a row sample (short splits admit most of their
+    // first keys before their local k-th settles; VS_TC_TAU_SAMPLE = sample
+    // rows, 0 = off)
+    // (default 8192 rows when the selection has at least 4x that; measured on
+    // config 2: MMA wait on the epilogue 2.65 M -> 0.60 M cycles per CTA, phase
+    // A 17.3 -> 16.2 ms for 0.22 ms of sample GEMM; 8 row shards: 2.94 -> 1.95 ms)
+    const int64_t tau_sample = getenv("VS_TC_TAU_SAMPLE") ? atoll(getenv("VS_TC_TAU_SAMPLE")) : 8192;
+    const int64_t nch_s = nsel >= 4 * tau_sample ? tau_sample / 32 : 0;
+    if (topk_mode && !*exhaustive && nch_s >= sp.k && nch_s > 0) {
+        float* smins = nullptr;
+        CKS(arena_alloc(ctx, (size_t)nq * nch_s, &smins));
+        CUtensorMap mbs;
+        if (!make_map(&mbs, xb, nch_s * 32, d, dp, pair ? tc::BN / 2 : tc::BN, f16))
+            return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        tc::Params ps = pr;
+        ps.nsel = nch_s * 32;
+        ps.ntiles = (ps.nsel + tc::BN - 1) / tc::BN;
+        ps.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(ps.ntiles, (2 * sms + qtiles - 1) / qtiles));
+        ps.tiles_per_split = (ps.ntiles + ps.nsplit - 1) / ps.nsplit;
+        ps.nsplit = (int)((ps.ntiles + ps.tiles_per_split - 1) / ps.tiles_per_split);
+        ps.keys_out = nullptr;
+        ps.mins_out = smins;
+        ps.mins_ld = nch_s;
+        const int64_t items_s = (int64_t)qtiles * ps.nsplit;
+        const unsigned units_s = (unsigned)std::min<int64_t>(items_s, sms);
+        const unsigned grid_s = pair ? 2 * units_s : units_s;
+        {
+            KTimer kt(ctx, VS_K_STAGE);
+            if (sp.ip) CK((pair ? launch_tc<true, 3, true>(ma, mbs, ps, grid_s, st) : launch_tc<true, 3, false>(ma, mbs, ps, grid_s, st)));
+            else CK((pair ? launch_tc<false, 3, true>(ma, mbs, ps, grid_s, st) : launch_tc<false, 3, false>(ma, mbs, ps, grid_s, st)));
+            tc::k_tau_seed<<<(unsigned)((nq * 32 + 255) / 256), 256, 0, st>>>(smins, nq, (int)nch_s, sp.k, margin, tau_g);
+            CK(cudaGetLastError());
+        }
+        ctx->stats[VS_STAT_LAUNCHES] += 2;
+    }
     KTimer kt_scan(ctx, timer_class);
     if (sp.ip) {
         CK((pair ? launch_tc<true, 0, true>(ma, mb, pr, grid, st) : launch_tc<true, 0, false>(ma, mb, pr, grid, st)));

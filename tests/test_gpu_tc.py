@@ -158,3 +158,23 @@ def test_tc_fp16_operand_scaling(tc_kernel, scale, metric):
     nt = vs.enn_search(q, data, vs.SearchParams(k=12), metric=metric, row_filter=mask)
     assert N.Context.get().stats()[N.STAT_LAST_ENN_KERNEL] == 2
     assert_same(nt, O.enn_filtered(q, data, mask, 12, metric))
+
+
+@pytest.mark.parametrize("metric", ["squared_l2", "inner_product"])
+@pytest.mark.parametrize("dups", [False, True])
+def test_tc_sampled_admission_seed(tc_kernel, monkeypatch, metric, dups):
+    """Phase A seeded with the k-th smallest chunk minimum of a row sample
+    (VS_TC_TAU_SAMPLE): exact results, also when the sample holds the
+    whole top-k (the seed is then the k-th key itself) and with duplicated
+    rows (ties across the sample boundary)."""
+    monkeypatch.setenv("VS_TC_TAU_SAMPLE", "1024")
+    rng = np.random.default_rng(90 + dups)
+    data = rng.standard_normal((30000, 64)).astype(np.float32)
+    q = rng.standard_normal((200, 64)).astype(np.float32)
+    if dups:
+        data[15000:15400] = data[:400]          # copies of sample rows later in the column
+        q[:50] = data[:50] + 1e-3 * rng.standard_normal((50, 64)).astype(np.float32)
+    mask = rng.random(30000) < 0.6
+    for k in (10, 32):
+        nt = vs.enn_search(q, data, vs.SearchParams(k=k), metric=metric, row_filter=mask)
+        assert_same(nt, O.enn_filtered(q, data, mask, k, metric))
