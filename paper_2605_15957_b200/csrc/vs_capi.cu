@@ -116,6 +116,36 @@ int ensure_norms(vs_column* col, vs_ctx* ctx) {
     return VS_OK;
 }
 
+// The fp16 shadow (vs_column::f16): built on a column's second tensor-core
+// search, when its float32 rows live on the device and the shadow fits (an
+// allocation failure only disables it). Staging then reads 2 bytes per
+// element instead of 4 (config 2: 6 -> 4 GB per search). VS_F16_SHADOW=0 off.
+int ensure_f16_shadow(vs_ctx* ctx, vs_column* col, int64_t nq, int64_t nsel) {
+    static const bool env_off = getenv("VS_F16_SHADOW") && getenv("VS_F16_SHADOW")[0] == '0';
+    if (env_off || col->dtype != VS_DTYPE_F32 || col->host_resident || col->f16_failed) return VS_OK;
+    if (ctx->opt_enn_kernel == 1 || !vs::use_f16(col->dtype, col->max_norm_bits) ||
+        !(ctx->opt_enn_kernel == 2 || vs::tc_profitable(nq, nsel, col->d)))
+        return VS_OK;
+    if (++col->searches < 2 && !col->f16) return VS_OK;
+    if (col->f16_ready) return VS_OK;
+    const int dp = (col->d + 7) / 8 * 8;
+    if (!col->f16) {
+        if (cudaMalloc(&col->f16, (size_t)std::max<int64_t>(col->n, 1) * dp * 2) != cudaSuccess ||
+            cudaMalloc(&col->f16_stats, (size_t)std::max<int64_t>(col->n, 1) * sizeof(float2)) != cudaSuccess) {
+            cudaGetLastError();
+            if (col->f16) cudaFree(col->f16);
+            col->f16 = nullptr;
+            col->f16_stats = nullptr;
+            col->f16_failed = true;
+            return VS_OK;
+        }
+    }
+    CKS(vs::tc_build_f16_shadow(ctx, (const float*)col->data, col->n, col->d, col->max_norm_bits, col->f16,
+                                col->f16_stats));
+    col->f16_ready = true;
+    return VS_OK;
+}
+
 // error-bound constant of the fp32 SIMT scores: margin =
 // 2 x 2 (d + 2) 2^-24 x (|q| + X)^2   (|q| X for inner product)
 float eps_simt(int d) { return 4.0f * (float)(d + 2) / 16777216.0f; }
@@ -135,6 +165,8 @@ struct EnnJob {
     int k;
     int64_t id_offset;
     const int64_t* id_map = nullptr;   // staged position -> base row (streamed chunks)
+    const void* f16 = nullptr;         // nullable: the column's fp16 shadow (vs_column)
+    const float2* f16_stats = nullptr;
     bool narrow = false;               // 128-row tensor-core tiles (IVF coarse quantizer)
     cudaEvent_t q_ready = nullptr;     // queries still being copied in (copy stream)
     float* margin_todo = nullptr;      // SIMT margins to compute once the queries have landed
@@ -211,6 +243,8 @@ int enn_phase_a(vs_ctx* ctx, const EnnJob& job, const float* margin, int cshift,
     sp.k = job.k;
     sp.tau_g = nullptr;
     sp.q_ready = nullptr;
+    sp.f16 = job.f16;
+    sp.f16_stats = job.f16_stats;
     const bool use_tc = ctx->opt_enn_kernel != 1 && vs::tc_supported(job.d, job.dtype, job.ip) &&
                         (ctx->opt_enn_kernel == 2 || vs::tc_profitable(job.nq, job.nsel, job.d));
     if (job.q_ready) {
@@ -697,6 +731,8 @@ int vs_column_free(vs_column* col) {
     if (col->host_registered) cudaHostUnregister(col->host_ptr);
     if (col->norms) cudaFree(col->norms);
     if (col->max_norm_bits) cudaFree(col->max_norm_bits);
+    if (col->f16) cudaFree(col->f16);
+    if (col->f16_stats) cudaFree(col->f16_stats);
     vs_ctx* ctx = col->ctx;
     delete col;
     ctx_unref(ctx);
@@ -706,6 +742,7 @@ int vs_column_free(vs_column* col) {
 int vs_column_invalidate(vs_column* col) {
     if (!col) return set_err(VS_ERR_PARAMETER, "null column");
     col->norms_ready = false;   // recomputed (on the caller's stream) by the next search
+    col->f16_ready = false;     // the shadow too (rebuilt in place)
     return VS_OK;
 }
 
@@ -973,6 +1010,9 @@ int vs_enn_search(vs_ctx* ctx, const vs_column* data, const float* queries, int6
     job.ip = metric;
     job.k = k;
     job.id_offset = id_offset;
+    CKS(ensure_f16_shadow(ctx, col, nq, nsel));
+    job.f16 = col->f16_ready ? col->f16 : nullptr;
+    job.f16_stats = col->f16_ready ? col->f16_stats : nullptr;
     const bool zc = !col->host_resident && k <= kTopkCap;   // outputs written once, by phase B
     CKS(stage_out_final(ctx, out_ids, (size_t)nq * k, &job.out_ids, pending, zc));
     CKS(stage_out_final(ctx, out_dist, (size_t)nq * k, &job.out_dist, pending, zc));

@@ -165,6 +165,14 @@ struct vs_column {
     float* norms = nullptr;          // ||x||^2 per row (lazy)
     unsigned* max_norm_bits = nullptr;
     bool norms_ready = false;
+    // fp16 shadow for the tensor-core phase A (float32 device columns searched
+    // more than once): [n][dp] scaled fp16 rows + per-row (||x~||^2, ||dx||^2),
+    // built on the second search, dropped with the norms on invalidation
+    void* f16 = nullptr;
+    float2* f16_stats = nullptr;
+    bool f16_ready = false;
+    bool f16_failed = false;         // allocation failed once: never retried
+    int searches = 0;
 };
 
 struct vs_ivf {

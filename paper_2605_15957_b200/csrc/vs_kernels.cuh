@@ -64,6 +64,8 @@ struct EnnScanParams {
     unsigned* tau_g = nullptr;  // tensor-core path: per-query global admission bound
     int verify = 0;             // phase A kept local top-k only: phase B must verify
     int band_ready = 0;         // one buffer per query holding exactly the margin band (RerankParams)
+    const void* f16 = nullptr;  // nullable: the column's fp16 shadow [n][dp] (staging gathers from it)
+    const float2* f16_stats = nullptr;
     cudaEvent_t q_ready = nullptr;  // nullable: queries still in flight (host->device on a copy
                                     // stream); phase A stages the rows first, then waits
 };

@@ -1012,7 +1012,7 @@ template <typename T, typename O>
 __global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict__ sel, int64_t nsel, int d,
                              int dp, const float* __restrict__ norms, O* __restrict__ out,
                              float* __restrict__ xn, unsigned* __restrict__ xmax2,
-                             const unsigned* __restrict__ xs = nullptr) {
+                             const unsigned* __restrict__ xs = nullptr, float2* __restrict__ rowstats = nullptr) {
     const int lane = threadIdx.x & 31;
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1056,6 +1056,37 @@ __global__ void k_stage_rows(const T* __restrict__ x, const int64_t* __restrict_
         mb = fmaxf(mb, sn);
         me = fmaxf(me, se);
         if (lane == 0 && xn) xn[w] = norms[r];
+        if (lane == 0 && rowstats) rowstats[w] = make_float2(sn, se);
+    }
+    if (lane == 0) {
+        atomicMax(&xmax2[0], __float_as_uint(mb));
+        atomicMax(&xmax2[1], __float_as_uint(me));
+    }
+}
+
+// staging from the column's fp16 shadow (same scale, same rounding as
+// k_stage_rows, so keys and margins are identical): selected rows are copied
+// (16-byte vectors, a warp per row), their norms and the max of their stored
+// (||x~||^2, ||dx||^2) reduced into xmax2. 2 + 2 bytes per element instead of 4 + 2.
+__global__ void k_stage_rows_f16(const __half* __restrict__ sh, const float2* __restrict__ stats,
+                                 const int64_t* __restrict__ sel, int64_t nsel, int dp,
+                                 const float* __restrict__ norms, __half* __restrict__ out, float* __restrict__ xn,
+                                 unsigned* __restrict__ xmax2) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float mb = 0.f, me = 0.f;
+    for (; w < nsel; w += nw) {
+        const int64_t r = sel ? sel[w] : w;
+        const uint4* src = reinterpret_cast<const uint4*>(sh + r * (int64_t)dp);
+        uint4* dst = reinterpret_cast<uint4*>(out + w * (int64_t)dp);
+        for (int c = lane; c < dp / 8; c += 32) dst[c] = __ldcs(src + c);
+        if (lane == 0) {
+            const float2 st = stats[r];
+            mb = fmaxf(mb, st.x);
+            me = fmaxf(me, st.y);
+            if (xn) xn[w] = norms[r];
+        }
     }
     if (lane == 0) {
         atomicMax(&xmax2[0], __float_as_uint(mb));
@@ -1215,6 +1246,22 @@ bool use_f16(int dtype, const unsigned* xmax) {
     return dtype == VS_DTYPE_F32 && xmax != nullptr && !bf16_env;
 }
 
+// the fp16 shadow of a float32 column (k_stage_rows over all rows, scale from
+// its max norm, per-row stats kept)
+int tc_build_f16_shadow(vs_ctx* ctx, const float* x, int64_t n, int d, const unsigned* xmax, void* shadow,
+                        float2* stats) {
+    using namespace vs_internal;
+    const int dp = (d + 7) / 8 * 8;
+    unsigned* junk = nullptr;
+    CKS(arena_alloc(ctx, 2, &junk));
+    const unsigned blocks = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 148 * 64);
+    tc::k_stage_rows<float, __half><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, (__half*)shadow,
+                                                                     nullptr, junk, xmax, stats);
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
+    return VS_OK;
+}
+
 bool tc_profitable(int64_t nq, int64_t nsel, int d) {
     return nq >= 64 && (double)nq * (double)nsel * (double)d >= 4.0e9;
 }
@@ -1256,7 +1303,10 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
         // rows first: they do not need the queries, whose host->device copy may
         // still be in flight on the copy stream (sp.q_ready)
         const unsigned blocks = (unsigned)std::min<int64_t>((nsel * 32 + 255) / 256, 148 * 64);
-        if (f16)
+        if (f16 && sp.f16 && dp % 8 == 0)
+            tc::k_stage_rows_f16<<<blocks, 256, 0, st>>>((const __half*)sp.f16, sp.f16_stats, sp.sel, nsel, dp,
+                                                         sp.xnorm, (__half*)xb, sp.ip ? nullptr : xn, xmax2);
+        else if (f16)
             tc::k_stage_rows<float, __half><<<blocks, 256, 0, st>>>((const float*)sp.X, sp.sel, nsel, d, dp,
                                                                     sp.xnorm, (__half*)xb, sp.ip ? nullptr : xn,
                                                                     xmax2, xmax);

@@ -25,6 +25,8 @@ inline namespace bn256 {
 bool tc_supported(int d, int dtype, int ip);
 // whether phase A stages fp16 operands (float32 rows with a known max norm)
 bool use_f16(int dtype, const unsigned* xmax);
+int tc_build_f16_shadow(vs_ctx* ctx, const float* x, int64_t n, int d, const unsigned* xmax, void* shadow,
+                        float2* stats);
 // heuristic: enough work to amortise the bf16 staging pass
 bool tc_profitable(int64_t nq, int64_t nsel, int d);
 // runs phase A on the tensor cores; fills `cb` (allocated by the callee from

@@ -1,0 +1,9 @@
+#!/bin/bash
+set -u
+OUT=gpurun_out/r2v
+mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_tc.py tests/test_gpu_enn.py tests/test_gpu_scale_a.py tests/test_gpu_two_phase.py tests/test_gpu_group.py -q -x > $OUT/pytest_sel.txt 2>&1; echo "pytest rc=$?"; tail -2 $OUT/pytest_sel.txt
+for z in 1 0 1 0; do
+  VS_F16_SHADOW=$z timeout 600 python bench.py --config 2 --no-cpu --steps 20 > $OUT/cfg2_sh$z.json 2>/dev/null
+  python -c "import json;d=json.load(open('$OUT/cfg2_sh$z.json'));print('cfg2 shadow=$z', d['value'], d['ms_per_step'], d['e2e']['value'], d['kernel_ms_per_step'], d['clocks']['sm_mhz'])"
+done

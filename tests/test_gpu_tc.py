@@ -178,3 +178,30 @@ def test_tc_sampled_admission_seed(tc_kernel, monkeypatch, metric, dups):
     for k in (10, 32):
         nt = vs.enn_search(q, data, vs.SearchParams(k=k), metric=metric, row_filter=mask)
         assert_same(nt, O.enn_filtered(q, data, mask, k, metric))
+
+
+def test_tc_f16_shadow_repeated_searches_and_mutation(tc_kernel):
+    """The column's fp16 shadow (built on its second tensor-core search):
+    repeated searches, a new filter, an in-place update seen by torch's
+    version counter and one behind its back (invalidate()) all stay exact."""
+    import torch
+    rng = np.random.default_rng(23)
+    data = rng.standard_normal((24000, 96)).astype(np.float32)
+    t = torch.from_numpy(data).cuda()
+    col = vs.EmbeddingColumn.from_device(t)
+    q = rng.standard_normal((260, 96)).astype(np.float32)
+
+    def check(mask):
+        nt = vs.enn_search(q, col, vs.SearchParams(k=20), row_filter=mask)
+        assert_same(nt, O.enn_filtered(q, t.cpu().numpy(), mask, 20))
+
+    m1 = rng.random(24000) < 0.4
+    for _ in range(3):
+        check(m1)
+    check(rng.random(24000) < 0.1)
+    t[::5] *= -2.0
+    check(m1)
+    alias = torch.empty(0, device=t.device).set_(t.untyped_storage(), 0, t.shape, t.stride())
+    alias[100:900] = 0.5
+    col.invalidate()
+    check(m1)
