@@ -812,6 +812,8 @@ class IvfWorkload:
         import torch
         if self.world > 1:
             return {"overflow_requeries_total": int(ctx.stats()[N.STAT_OVERFLOW_QUERIES])}
+        # survivors of the last phase B (the IVF re-rank of the timed batch)
+        surv = round(ctx.stats()[N.STAT_SURVIVORS] / self.nq, 2)
         lat = {}
         for qn in (1, 100):
             q = self.queries[:qn].contiguous()
@@ -825,7 +827,8 @@ class IvfWorkload:
                 self._search(q, self.bits, out)
             torch.cuda.synchronize()
             lat[f"Q={qn}"] = round((time.perf_counter() - t0) / reps * 1e3, 3)
-        return {"batch_latency_ms": lat, "overflow_requeries_total": int(ctx.stats()[N.STAT_OVERFLOW_QUERIES])}
+        return {"batch_latency_ms": lat, "ivf_survivors_per_query": surv,
+                "overflow_requeries_total": int(ctx.stats()[N.STAT_OVERFLOW_QUERIES])}
 
     def cpu_baseline(self, args):
         """The reference IVF search path (oracle port of vecindex.py:230-258,

@@ -577,6 +577,8 @@ int vs_ctx_destroy(vs_ctx* ctx) {
         ctx->event_pool.clear();
         if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
         if (ctx->q_event) cudaEventDestroy(ctx->q_event);
+        for (auto& e : ctx->q_chunk_ev)
+            if (e) cudaEventDestroy(e);
         ctx->copy_stream = nullptr;
         ctx->q_event = nullptr;
     }
@@ -1984,7 +1986,10 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     rp.out_dist = job.out_dist;
     rp.out_ids32 = nullptr;
     rp.out_count = job.out_count;
-    rp.n_survivors = nullptr;
+    unsigned long long* d_surv = nullptr;
+    CKS(arena_alloc(ctx, 1, &d_surv));
+    CK(cudaMemsetAsync(d_surv, 0, sizeof(unsigned long long), ctx->stream));
+    rp.n_survivors = d_surv;
     {
         KTimer kt(ctx, VS_K_IVF_RERANK);
         if (v->dtype == VS_DTYPE_F32) CK(vs::launch_rerank<float>(rp, ctx->stream));
@@ -1995,8 +2000,11 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
     std::vector<int32_t> which;
     {
         std::vector<int> h(job.nq);
+        unsigned long long h_surv = 0;
+        CK(cudaMemcpyAsync(&h_surv, d_surv, sizeof(h_surv), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaMemcpyAsync(h.data(), cb.overflow, job.nq * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        if (cshift == 0) ctx->stats[VS_STAT_SURVIVORS] = (int64_t)h_surv;
         for (int64_t i = 0; i < job.nq; ++i)
             if (h[i] || (allow_force && ctx->opt_force_retry)) which.push_back((int32_t)i);
     }
@@ -2042,9 +2050,12 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
 // tie-rule top-nprobe, bit-identical probes). Replaces candidate buffers fed
 // by the GEMM epilogue, which made the coarse GEMM epilogue-bound and left
 // ~2,300 candidates per query for phase B to sort through.
-int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
+int coarse_dense(vs_ctx* ctx, const EnnJob& cj, float* simt_margin, int n_qchunks, const unsigned* cmax) {
     const int64_t ncols = cj.nsel;
-    const int64_t qc = std::max<int64_t>(256, std::min<int64_t>(cj.nq, ((int64_t)1 << 28) / std::max<int64_t>(ncols, 1)));
+    int64_t qc = std::max<int64_t>(256, std::min<int64_t>(cj.nq, ((int64_t)1 << 28) / std::max<int64_t>(ncols, 1)));
+    // queries still landing in n_qchunks chunks (copy stream): one coarse chunk each
+    const int64_t up = n_qchunks ? (cj.nq + n_qchunks - 1) / n_qchunks : 0;
+    if (n_qchunks) qc = std::min(qc, up);
     // per-chunk minima let the select read ~4 % of the keys (k_coarse_select)
     const bool chunked = vs::coarse_select_ok(ncols, cj.k) && !getenv("VS_COARSE_FULLSELECT");
     const int64_t nch = (ncols + 31) / 32;
@@ -2058,8 +2069,14 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, const float* simt_margin) {
     // fp16 operands: the tensor-core band is already about as tight as the fp32
     // SIMT margin, so the fp32 refinement pass would not shrink it
     const bool f16 = vs::use_f16(VS_DTYPE_F32, cj.xmax);
+    int waited = 0;
     for (int64_t q0 = 0; q0 < cj.nq; q0 += qc) {
         const int64_t n = std::min(qc, cj.nq - q0);
+        for (; waited < n_qchunks && (int64_t)waited * up < q0 + n; ++waited)
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->q_chunk_ev[waited], 0));
+        if (simt_margin)
+            CK(vs::launch_query_margins(cj.q + q0 * cj.d, n, cj.d, cmax, eps_simt(cj.d), 0, simt_margin + q0, nullptr,
+                                        ctx->stream));
         EnnJob sub = cj;
         sub.q = cj.q + q0 * cj.d;
         sub.nq = n;
@@ -2138,12 +2155,55 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     if (nq == 0) return VS_OK;
     const int d = ivf->d;
     const float* dq = nullptr;
-    CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+    // a large host query batch is copied in four chunks on the copy stream; the
+    // coarse quantizer (dense path) starts on chunk c as soon as it has landed
+    int n_qchunks = 0;
+    {
+        cudaPointerAttributes at{};
+        const bool host_q = queries && cudaPointerGetAttributes(&at, queries) == cudaSuccess &&
+                            at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged;
+        cudaGetLastError();
+        if (host_q && !probes_in && (size_t)nq * d * 4 >= ((size_t)1 << 23) && nq >= 4 * 256) {
+            float* buf = nullptr;
+            CKS(arena_alloc(ctx, (size_t)nq * d, &buf));
+            if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            if (!ctx->q_event) CK(cudaEventCreateWithFlags(&ctx->q_event, cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->q_event, ctx->stream));            // earlier work on the arena
+            CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->q_event, 0));
+            n_qchunks = 4;
+            const int64_t qc = (nq + n_qchunks - 1) / n_qchunks;
+            for (int c = 0; c < n_qchunks; ++c) {
+                if (!ctx->q_chunk_ev[c]) CK(cudaEventCreateWithFlags(&ctx->q_chunk_ev[c], cudaEventDisableTiming));
+                const int64_t q0 = c * qc, n = std::max<int64_t>(0, std::min(qc, nq - q0));
+                if (n) CK(cudaMemcpyAsync(buf + q0 * d, queries + q0 * d, (size_t)n * d * 4, cudaMemcpyHostToDevice,
+                                          ctx->copy_stream));
+                CK(cudaEventRecord(ctx->q_chunk_ev[c], ctx->copy_stream));
+            }
+            dq = buf;
+        } else {
+            CKS(stage_in(ctx, queries, (size_t)nq * d, &dq));
+        }
+    }
+    // permuted bitmap over payload positions (needs no query: runs while they land)
+    uint32_t* pbits = nullptr;
+    if (bitmap) {
+        const uint32_t* dbm = nullptr;
+        CKS(stage_in(ctx, bitmap, (size_t)(nbits + 31) / 32, &dbm));
+        CKS(arena_alloc(ctx, (size_t)(ivf->n_total + 31) / 32 + 2, &pbits));
+        CK(cudaMemsetAsync(pbits, 0, ((ivf->n_total + 31) / 32 + 2) * sizeof(uint32_t), ctx->stream));
+        KTimer kt(ctx, VS_K_SELECT);
+        CK(vs::launch_permute_bitmap(dbm, nbits, ivf->list_ids, ivf->n_total, pbits, ctx->stream));
+        ctx->stats[VS_STAT_LAUNCHES] += 1;
+    }
+    auto wait_all_queries = [&]() -> int {
+        for (int c = 0; c < n_qchunks; ++c) CK(cudaStreamWaitEvent(ctx->stream, ctx->q_chunk_ev[c], 0));
+        n_qchunks = 0;
+        return VS_OK;
+    };
     // coarse quantizer: exact tie-rule top-nprobe over float32 centroids, always
     // squared L2 (vecindex.py:238-243)
     float* cm = nullptr;
     CKS(arena_alloc(ctx, (size_t)nq, &cm));
-    CK(vs::launch_query_margins(dq, nq, d, ivf->cmax, eps_simt(d), 0, cm, nullptr, ctx->stream));
     int32_t* probes = nullptr;
     if (probes_in) {
         const int32_t* dp = nullptr;
@@ -2176,25 +2236,18 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
     // buffers, 2 dense keys whenever the tensor cores apply
     const bool dense_ok = nprobe <= kTopkCap && ctx->opt_enn_kernel != 1 && vs::tc_supported(d, VS_DTYPE_F32, 0);
     if (dense_ok && (ctx->opt_coarse == 2 || (ctx->opt_coarse == 0 && vs::tc_profitable(nq, ivf->nlist, d)))) {
-        CKS(coarse_dense(ctx, cj, cm));
+        CKS(coarse_dense(ctx, cj, cm, n_qchunks, ivf->cmax));
+        n_qchunks = 0;
     } else {
+        CKS(wait_all_queries());
+        CK(vs::launch_query_margins(dq, nq, d, ivf->cmax, eps_simt(d), 0, cm, nullptr, ctx->stream));
         CKS(run_enn(ctx, cj, cm, 0, false));
     }
     }
+    CKS(wait_all_queries());
     if (probe_only) {
         CKS(flush_out(ctx, pending));
         return VS_OK;
-    }
-    // permuted bitmap over payload positions
-    uint32_t* pbits = nullptr;
-    if (bitmap) {
-        const uint32_t* dbm = nullptr;
-        CKS(stage_in(ctx, bitmap, (size_t)(nbits + 31) / 32, &dbm));
-        CKS(arena_alloc(ctx, (size_t)(ivf->n_total + 31) / 32 + 2, &pbits));
-        CK(cudaMemsetAsync(pbits, 0, ((ivf->n_total + 31) / 32 + 2) * sizeof(uint32_t), ctx->stream));
-        KTimer kt(ctx, VS_K_SELECT);
-        CK(vs::launch_permute_bitmap(dbm, nbits, ivf->list_ids, ivf->n_total, pbits, ctx->stream));
-        ctx->stats[VS_STAT_LAUNCHES] += 1;
     }
     float* sm = nullptr;
     CKS(arena_alloc(ctx, (size_t)nq, &sm));

@@ -135,6 +135,7 @@ struct vs_ctx {
     int sm_reserve = 0;              // SMs left free by persistent kernels (streamed gathers)
     cudaStream_t copy_stream = nullptr;   // host-resident search: gathers over PCIe; query uploads
     cudaEvent_t q_event = nullptr;        // queries landed (copy stream)
+    cudaEvent_t q_chunk_ev[4] = {};       // IVF: query chunks landed (chunked upload, coarse overlaps it)
     // CUDA-event timing of kernel classes (resolved after each call's final sync)
     struct PendingTimer {
         int cls;

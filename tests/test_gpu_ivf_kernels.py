@@ -268,3 +268,32 @@ def test_ivf_pinned_host_outputs_written_in_place():
     dist = np.concatenate([out[1].numpy()[i, :cnt[i]] for i in range(150)])
     assert np.array_equal(ids, ref.data_row)
     assert np.array_equal(dist, ref.distance)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_ivf_large_host_query_batch_chunked_upload(pinned):
+    """A large host query batch is uploaded in chunks while the coarse
+    quantizer runs on the chunks that have landed: identical to the same
+    search with device-resident queries, and sampled queries equal the oracle."""
+    rng = np.random.default_rng(88)
+    n, d, nlist = 20000, 512, 256
+    idx, data, centroids, parts, payload = _index(rng, n, d, nlist)
+    queries = rng.standard_normal((4200, d)).astype(np.float32)     # 8.6 MB: the chunked path
+    mask = rng.random(n) < 0.25
+    ctx = N.Context.get()
+    ctx.set_option(N.OPT_COARSE, 2)
+    try:
+        hq = torch.from_numpy(queries).pin_memory() if pinned else queries
+        host = idx.search(hq, vs.SearchParams(k=10, nprobe=12), row_filter=mask)
+        dev = idx.search(torch.from_numpy(queries).cuda(), vs.SearchParams(k=10, nprobe=12), row_filter=mask)
+    finally:
+        ctx.set_option(N.OPT_COARSE, 0)
+    assert np.array_equal(host.probes, dev.probes)
+    assert np.array_equal(host.data_row, dev.data_row)
+    assert np.array_equal(host.distance, dev.distance)
+    sample = np.array([0, 1049, 1050, 2100, 4199])
+    ref = O.ivf_search(queries[sample], centroids, parts, lambda c: payload[c], 12, 10, mask=mask)
+    assert np.array_equal(host.probes[sample], ref.probes)
+    sel = np.isin(host.query_row, sample)
+    assert np.array_equal(host.data_row[sel], ref.data_row)
+    assert np.array_equal(host.distance[sel], ref.distance)
