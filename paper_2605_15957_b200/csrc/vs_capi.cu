@@ -2069,6 +2069,17 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, float* simt_margin, int n_qchunk
     // fp16 operands: the tensor-core band is already about as tight as the fp32
     // SIMT margin, so the fp32 refinement pass would not shrink it
     const bool f16 = vs::use_f16(VS_DTYPE_F32, cj.xmax);
+    // one margin-band buffer per query for the whole batch; the key matrix is
+    // produced and selected chunk by chunk, phase B runs once
+    vs::CandBuf cb;
+    cb.n_sub = 1;
+    cb.C = C;
+    CKS(arena_alloc(ctx, (size_t)cj.nq * C, &cb.key));
+    CKS(arena_alloc(ctx, (size_t)cj.nq * C, &cb.pos));
+    CKS(arena_alloc(ctx, (size_t)cj.nq, &cb.cnt));
+    CKS(arena_alloc(ctx, (size_t)cj.nq, &cb.overflow));
+    CK(cudaMemsetAsync(cb.overflow, 0, cj.nq * sizeof(int), ctx->stream));
+    const bool refine = !f16 && cj.ip == 0 && simt_margin != nullptr;
     int waited = 0;
     for (int64_t q0 = 0; q0 < cj.nq; q0 += qc) {
         const int64_t n = std::min(qc, cj.nq - q0);
@@ -2077,60 +2088,50 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, float* simt_margin, int n_qchunk
         if (simt_margin)
             CK(vs::launch_query_margins(cj.q + q0 * cj.d, n, cj.d, cmax, eps_simt(cj.d), 0, simt_margin + q0, nullptr,
                                         ctx->stream));
-        EnnJob sub = cj;
-        sub.q = cj.q + q0 * cj.d;
-        sub.nq = n;
-        if (sub.out_ids32) sub.out_ids32 += q0 * cj.k;
-        if (sub.out_ids) sub.out_ids += q0 * cj.k;
-        if (sub.out_dist) sub.out_dist += q0 * cj.k;
-        if (sub.out_count) sub.out_count += q0;
+        const float* qs = cj.q + q0 * cj.d;
         if (cj.narrow)
-            CKS(vs::bn128::tc_dense_keys(ctx, sub.q, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip,
+            CKS(vs::bn128::tc_dense_keys(ctx, qs, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip,
                                          keys, tm + q0, mins));
         else
-            CKS(vs::tc_dense_keys(ctx, sub.q, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip, keys,
+            CKS(vs::tc_dense_keys(ctx, qs, n, cj.d, (const float*)cj.rows, ncols, cj.xnorm, cj.xmax, cj.ip, keys,
                                   tm + q0, mins));
-        vs::CandBuf cb;
-        cb.n_sub = 1;
-        cb.C = C;
-        CKS(arena_alloc(ctx, (size_t)n * C, &cb.key));
-        CKS(arena_alloc(ctx, (size_t)n * C, &cb.pos));
-        CKS(arena_alloc(ctx, (size_t)n, &cb.cnt));
-        CKS(arena_alloc(ctx, (size_t)n, &cb.overflow));
-        CK(cudaMemsetAsync(cb.overflow, 0, n * sizeof(int), ctx->stream));
+        vs::CandBuf cbs = cb;   // this chunk's rows of the buffers
+        cbs.key += q0 * (int64_t)C;
+        cbs.pos += q0 * (int64_t)C;
+        cbs.cnt += q0;
+        cbs.overflow += q0;
         {
             KTimer kt(ctx, cj.cls_scan);   // candidate generation: part of the coarse phase A
-            if (chunked) CK(vs::launch_coarse_select(keys, mins, n, ncols, cj.k, tm + q0, cb, ctx->stream));
-            else CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cb, ctx->stream));
+            if (chunked) CK(vs::launch_coarse_select(keys, mins, n, ncols, cj.k, tm + q0, cbs, ctx->stream));
+            else CK(vs::launch_dense_select(keys, n, ncols, cj.k, tm + q0, cbs, ctx->stream));
         }
         ctx->stats[VS_STAT_LAUNCHES] += 1;
         // the bf16 band (~2x nprobe centroids) -> fp32 keys with the SIMT margin:
         // phase B re-scores ~nprobe centroids in float64 instead of the band
-        const bool refine = !f16 && cj.ip == 0 && simt_margin != nullptr;
         if (refine) {
             KTimer kt(ctx, cj.cls_rerank);
-            CK(vs::launch_refine32(cb, n, sub.q, cj.d, (const float*)cj.rows, ctx->stream));
+            CK(vs::launch_refine32(cbs, n, qs, cj.d, (const float*)cj.rows, ctx->stream));
             ctx->stats[VS_STAT_LAUNCHES] += 1;
         }
-        PhaseA st;
-        st.sp.Q = sub.q;
-        st.sp.nq = n;
-        st.sp.d = cj.d;
-        st.sp.X = cj.rows;
-        st.sp.sel = nullptr;
-        st.sp.nsel = ncols;
-        st.sp.xnorm = cj.xnorm;
-        st.sp.margin = refine ? simt_margin + q0 : tm + q0;
-        st.sp.ip = cj.ip;
-        st.sp.k = cj.k;
-        st.sp.cb = cb;
-        st.sp.tau_g = nullptr;
-        st.sp.verify = 0;
-        st.sp.band_ready = refine ? 0 : 1;   // the select wrote exactly the band of the k-th key
-        st.exhaustive = false;
-        ctx->stats[VS_STAT_LAST_ENN_KERNEL] = 2;
-        CKS(enn_phase_b(ctx, sub, st, 0, false, PhaseBHooks{}));
     }
+    PhaseA st;
+    st.sp.Q = cj.q;
+    st.sp.nq = cj.nq;
+    st.sp.d = cj.d;
+    st.sp.X = cj.rows;
+    st.sp.sel = nullptr;
+    st.sp.nsel = ncols;
+    st.sp.xnorm = cj.xnorm;
+    st.sp.margin = refine ? simt_margin : tm;
+    st.sp.ip = cj.ip;
+    st.sp.k = cj.k;
+    st.sp.cb = cb;
+    st.sp.tau_g = nullptr;
+    st.sp.verify = 0;
+    st.sp.band_ready = refine ? 0 : 1;   // the select wrote exactly the band of the k-th key
+    st.exhaustive = false;
+    ctx->stats[VS_STAT_LAST_ENN_KERNEL] = 2;
+    CKS(enn_phase_b(ctx, cj, st, 0, false, PhaseBHooks{}));
     return VS_OK;
 }
 
