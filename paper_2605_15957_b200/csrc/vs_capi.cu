@@ -1130,6 +1130,9 @@ int vs_enn_search_begin(vs_ctx* ctx, const vs_column* data, const float* queries
     CKS(ensure_norms(col, ctx));
     job.xnorm = col->norms;
     job.xmax = col->max_norm_bits;
+    CKS(ensure_f16_shadow(ctx, col, nq, nsel));
+    job.f16 = col->f16_ready ? col->f16 : nullptr;
+    job.f16_stats = col->f16_ready ? col->f16_stats : nullptr;
     float* margin = nullptr;
     CKS(arena_alloc(ctx, (size_t)nq, &margin));
     CK(vs::launch_query_margins(dq, nq, d, col->max_norm_bits, eps_simt(d), metric, margin, nullptr,
