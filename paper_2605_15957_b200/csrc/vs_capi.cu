@@ -1870,7 +1870,7 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
             CKS(arena_alloc(ctx, (size_t)v->nlist + 1, &a.sel_off));
             CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(v->n_total, 1), &a.spos));
             char* recs = nullptr;
-            CKS(arena_alloc(ctx, (size_t)gr.max_units * vs::kIvfSelRecBytes, &recs));
+            CKS(arena_alloc(ctx, (size_t)gr.max_units * (mma ? 2 : 1) * vs::kIvfSelRecBytes, &recs));
             a.recs = recs;
             a.tmp_bytes = vs::ivf_sel_temp_bytes(v->nlist);
             char* tmp = nullptr;
@@ -1886,8 +1886,6 @@ int run_ivf_scan(vs_ctx* ctx, const IvfJob& job, const float* margin, int cshift
                 CKS(arena_alloc(ctx, (size_t)job.nq, &mmargin));
                 CKS(arena_alloc(ctx, (size_t)job.nq * ((v->d + 7) / 8 * 8), &qh));
                 CKS(arena_alloc(ctx, (size_t)job.nq, &kinv));
-                CKS(arena_alloc(ctx, (size_t)job.nq * job.nprobe, &a.pq));
-                CKS(arena_alloc(ctx, (size_t)job.nq * job.nprobe, &a.psub));
                 {
                     KTimer kt(ctx, VS_K_STAGE);
                     CK(vs::launch_f16_row_bounds(v->pmax, v->d, bounds, ctx->stream));

@@ -352,20 +352,28 @@ constexpr int MQ = kMmaPairs;   // pairs per unit (MMA M)
 constexpr int MN = 8;           // rows per chunk (MMA N)
 constexpr int MW = 4;           // warps; K is split across them
 constexpr int MNT = MW * 32;
-constexpr int MPOS = 27;
+constexpr int MPOS = 19;
 constexpr int MV = 2048 / 128;  // float4 loads per lane for a row of d <= 2048
 
+// 256-byte unit record: everything a unit needs before its first load (the
+// pairs' queries, probe ranks and key factors, the first MPOS row positions),
+// so staging starts without dependent global loads; the next unit's record is
+// read while this one is scored
 struct __align__(16) MmaRec {
     int32_t list, np, nsel, first_pair;
     uint32_t sel_off;
+    int32_t q[MQ];
+    uint16_t sub[MQ];
+    float ks[MQ];               // -2 kinv (L2) or -kinv (IP)
     uint32_t pos[MPOS];
 };
-static_assert(sizeof(MmaRec) == 128, "one 128-byte record per unit");
+static_assert(sizeof(MmaRec) == 256, "one 256-byte record per unit");
 
 __global__ void k_make_mma_recs(const int4* __restrict__ units, const int32_t* __restrict__ n_units,
                                 int64_t max_units, const int32_t* __restrict__ lsel,
                                 const int64_t* __restrict__ sel_off, const uint32_t* __restrict__ spos,
-                                MmaRec* __restrict__ recs) {
+                                const int32_t* __restrict__ pair_codes, int nprobe, const float* __restrict__ kinv,
+                                int ip, MmaRec* __restrict__ recs) {
     const int nu = *n_units;
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < max_units && u < nu;
          u += (int64_t)gridDim.x * blockDim.x) {
@@ -377,17 +385,17 @@ __global__ void k_make_mma_recs(const int4* __restrict__ units, const int32_t* _
         r.nsel = lsel[un.x];
         r.sel_off = (uint32_t)sel_off[un.x];
 #pragma unroll
+        for (int s = 0; s < MQ; ++s) {
+            const bool live = s < un.z;
+            const int code = live ? pair_codes[un.y + s] : 0;
+            r.q[s] = code / nprobe;
+            r.sub[s] = (uint16_t)(code % nprobe);
+            const float kv = live ? kinv[r.q[s]] : 0.f;
+            r.ks[s] = ip ? -kv : -2.f * kv;
+        }
+#pragma unroll
         for (int i = 0; i < MPOS; ++i) r.pos[i] = i < r.nsel ? spos[r.sel_off + i] : 0u;
         recs[u] = r;
-    }
-}
-
-__global__ void k_split_pairs(const int32_t* __restrict__ pair_codes, int64_t npairs, int nprobe,
-                              int32_t* __restrict__ pq, int32_t* __restrict__ psub) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs; i += (int64_t)gridDim.x * blockDim.x) {
-        const int code = pair_codes[i];
-        pq[i] = code / nprobe;
-        psub[i] = code % nprobe;
     }
 }
 
@@ -427,8 +435,6 @@ struct IvfMmaParams {
     int nprobe;
     const MmaRec* recs;
     const int32_t* n_units;
-    const int32_t* pq;
-    const int32_t* psub;
     const uint32_t* spos;
     const float* pnorm;
     const float* margin;
@@ -447,11 +453,8 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
     float* keys = red + MW * 32 * 4;                                 // [MQ][MN]
     float* xn_s = keys + MQ * MN;                                    // [MN]
     uint32_t* pos_s = reinterpret_cast<uint32_t*>(xn_s + MN);        // [MN]
-    int* pq_s = reinterpret_cast<int*>(pos_s + MN);                  // [MQ]
-    int* psub_s = pq_s + MQ;                                         // [MQ]
-    float* ks_s = reinterpret_cast<float*>(psub_s + MQ);             // [MQ] -2 kinv (or -kinv for IP)
-    int* cnt_s = reinterpret_cast<int*>(ks_s + MQ);                  // [MQ]
-    MmaRec* rec = reinterpret_cast<MmaRec*>(cnt_s + MQ);
+    int* cnt_s = reinterpret_cast<int*>(pos_s + MN);                 // [MQ]
+    MmaRec* recb = reinterpret_cast<MmaRec*>(cnt_s + MQ);            // [2]: this unit's and the next one's
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.cb.C;
     const int n_units = *p.n_units;
@@ -459,36 +462,36 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
     const int ksteps = d / 16;
     unsigned long long visited = 0;
     for (int i = tid; i < (MQ + MN) * ld; i += MNT) As[i] = __float2half(0.f);
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        __syncthreads();   // previous unit fully consumed
-        if (tid < 32) reinterpret_cast<uint32_t*>(rec)[tid] = reinterpret_cast<const uint32_t*>(p.recs + u)[tid];
-        __syncthreads();
-        const int np = rec->np, nsel = rec->nsel, first = rec->first_pair;
-        // the next unit's rows -> L2 (one bulk prefetch per row), so its B
-        // staging below waits on L2 instead of HBM
-        if (warp == MW - 1 && u + (int)gridDim.x < n_units) {
-            const uint32_t wv = reinterpret_cast<const uint32_t*>(p.recs + u + gridDim.x)[lane];
-            const int nsel_n = __shfl_sync(VS_FULL, (int)wv, 2);
-            const int j = lane - 5;   // word 5 + j holds pos[j]
-            if (j >= 0 && j < min(nsel_n, MPOS))
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.payload + (int64_t)wv * d),
-                             "r"(d * 4)
-                             : "memory");
-        }
-        // A: the unit's queries (16-byte cp.async from the fp16 copy), pair info
-        for (int r = warp; r < np; r += MW) {   // a warp per query row, no index division
-            const __half* src = p.Qh + (int64_t)__ldg(p.pq + first + r) * d;
+    constexpr int RW = (int)(sizeof(MmaRec) / 4);   // record words (64: two per lane)
+    if (warp == 0 && (int)blockIdx.x < n_units)
+        for (int i = lane; i < RW; i += 32)
+            reinterpret_cast<uint32_t*>(&recb[0])[i] = reinterpret_cast<const uint32_t*>(p.recs + blockIdx.x)[i];
+    int cur = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, cur ^= 1) {
+        __syncthreads();   // previous unit consumed; this unit's record in recb[cur]
+        const MmaRec* rec = &recb[cur];
+        const int np = rec->np, nsel = rec->nsel;
+        // A: the unit's queries (16-byte cp.async from the fp16 copy)
+        for (int r = warp; r < np; r += MW) {   // a warp per query row
+            const __half* src = p.Qh + (int64_t)rec->q[r] * d;
             for (int c8 = lane; c8 < d / 8; c8 += 32) cp_async16(As + r * ld + c8 * 8, src + c8 * 8);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
-        if (tid < MQ) {
-            const bool live = tid < np;
-            const int q = live ? __ldg(p.pq + first + tid) : 0;
-            pq_s[tid] = q;
-            psub_s[tid] = live ? __ldg(p.psub + first + tid) : 0;
-            const float kv = live ? __ldg(p.kinv + q) : 0.f;   // 2^-(eq+ex): both scales
-            ks_s[tid] = IP ? -kv : -2.f * kv;
-            cnt_s[tid] = 0;
+        if (tid < MQ) cnt_s[tid] = 0;
+        // the next unit's record (registers, stored to recb[cur ^ 1] after this
+        // unit) and its rows -> L2 (one bulk prefetch per row)
+        const int un = u + gridDim.x;
+        uint32_t nw0 = 0u, nw1 = 0u;
+        if (warp == MW - 1 && un < n_units) {
+            const uint32_t* nr = reinterpret_cast<const uint32_t*>(p.recs + un);
+            nw0 = nr[lane];
+            nw1 = nr[lane + 32];
+            const int nsel_n = __shfl_sync(VS_FULL, (int)nw0, 2);
+            const int j = lane + 32 - (int)(offsetof(MmaRec, pos) / 4);   // word lane + 32 holds pos[j]
+            if (j >= 0 && j < min(nsel_n, MPOS))
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.payload + (int64_t)nw1 * d),
+                             "r"(d * 4)
+                             : "memory");
         }
         if (tid == 0) visited += (unsigned long long)nsel * np;
         for (int c0 = 0; c0 < nsel; c0 += MN) {
@@ -553,14 +556,15 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int pr = g + (j >> 1) * 8, rw = 2 * t + (j & 1);
-                    keys[pr * MN + rw] = IP ? v[j] * ks_s[pr] : fmaf(ks_s[pr], v[j], xn_s[rw]);
+                    const float ks = pr < np ? rec->ks[pr] : 0.f;
+                    keys[pr * MN + rw] = IP ? v[j] * ks : fmaf(ks, v[j], xn_s[rw]);
                 }
             }
             __syncthreads();
             // appends: warp w serves pairs w, w + 4, ...; lane r holds row r
             for (int pr = warp; pr < np; pr += MW) {
-                const int q = pq_s[pr];
-                const int64_t bidx = (int64_t)q * p.cb.n_sub + psub_s[pr];
+                const int q = rec->q[pr];
+                const int64_t bidx = (int64_t)q * p.cb.n_sub + rec->sub[pr];
                 float* ckey = p.cb.key + bidx * C;
                 uint32_t* cpos = p.cb.pos + bidx * C;
                 int cnt = cnt_s[pr];
@@ -583,7 +587,11 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
             }
         }
         __syncthreads();
-        if (tid < np) p.cb.cnt[(int64_t)pq_s[tid] * p.cb.n_sub + psub_s[tid]] = cnt_s[tid];
+        if (tid < np) p.cb.cnt[(int64_t)rec->q[tid] * p.cb.n_sub + rec->sub[tid]] = cnt_s[tid];
+        if (warp == MW - 1 && un < n_units) {
+            reinterpret_cast<uint32_t*>(&recb[cur ^ 1])[lane] = nw0;
+            reinterpret_cast<uint32_t*>(&recb[cur ^ 1])[lane + 32] = nw1;
+        }
     }
     if (tid == 0 && visited) atomicAdd(p.visited, visited);
 }
@@ -603,7 +611,7 @@ __global__ void k_f16_row_bounds(const unsigned* __restrict__ xmax, int d, unsig
 size_t ivf_mma_smem(int d) {
     const size_t ld = (size_t)d + 8;
     return (MQ + MN) * ld * 2 + (size_t)MW * 32 * 4 * 4 + (size_t)MQ * MN * 4 + (size_t)MN * 8 + (size_t)MQ * 16 +
-           sizeof(MmaRec) + 64;
+           2 * sizeof(MmaRec) + 64;
 }
 
 cudaError_t launch_f16_row_bounds(const unsigned* xmax, int d, unsigned* out, cudaStream_t s) {
@@ -641,11 +649,8 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
         if (std::is_same<T, float>::value == false) return cudaErrorInvalidValue;
         MmaRec* mrecs = reinterpret_cast<MmaRec*>(a.recs);
         const int rb = (int)std::max<int64_t>(1, std::min<int64_t>((a.max_units + 255) / 256, 8192));
-        k_make_mma_recs<<<rb, 256, 0, s>>>(a.units, a.n_units, a.max_units, a.lsel, a.sel_off, a.spos, mrecs);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        const int64_t npairs = a.nq * (int64_t)a.nprobe;
-        k_split_pairs<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((npairs + 255) / 256, 4096)), 256, 0, s>>>(
-            a.pair_codes, npairs, a.nprobe, a.pq, a.psub);
+        k_make_mma_recs<<<rb, 256, 0, s>>>(a.units, a.n_units, a.max_units, a.lsel, a.sel_off, a.spos, a.pair_codes,
+                                           a.nprobe, a.kinv, a.ip, mrecs);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         IvfMmaParams m;
         m.Qh = a.Qh;
@@ -656,8 +661,6 @@ cudaError_t launch_ivf_scan_sel(const IvfSelLaunch& a, cudaStream_t s) {
         m.nprobe = a.nprobe;
         m.recs = mrecs;
         m.n_units = a.n_units;
-        m.pq = a.pq;
-        m.psub = a.psub;
         m.spos = a.spos;
         m.pnorm = a.pnorm;
         m.margin = a.margin;

@@ -184,8 +184,6 @@ struct IvfSelLaunch {
     const __half* Qh = nullptr;
     const float* kinv = nullptr;
     const unsigned* xscale = nullptr;
-    int32_t* pq = nullptr;      // [nq * nprobe] scratch: pair -> query, probe rank
-    int32_t* psub = nullptr;
     void* tmp;
     size_t tmp_bytes;           // >= ivf_sel_temp_bytes(nlist)
     int sm_count;
