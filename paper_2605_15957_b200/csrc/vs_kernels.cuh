@@ -257,6 +257,7 @@ struct RerankParams {
     const int32_t* q_count = nullptr;
     int band_ready = 0;         // the single buffer per query already holds exactly the
                                 //      margin band of its k-th key: every entry survives
+    int prefetch_iters = 4;     // scorer iterations of L2 prefetch ahead (VS_RR_PD)
     int ubytes;                 // filled by launch_rerank: shared-memory union size
     int reg_path;               // filled by launch_rerank: register-resident scorer
 };

@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(NT, PH == 1 ? 5 : (WIDE ? 2 : 4)) k_rerank(Rer
             for (int o = lane * 128; o < row_bytes; o += 32 * 128)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
         };
-        constexpr int RR_PD = 4;
+        const int RR_PD = p.prefetch_iters;
         int64_t* ridx = reinterpret_cast<int64_t*>(u);
         uint32_t* rps = reinterpret_cast<uint32_t*>(u + (size_t)ns * 8);
         const bool staged = ns * 12 <= (int64_t)p.ubytes;   // block-uniform
@@ -1834,6 +1834,8 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     RerankParams p = p0;
     if (p.d >= 8 && p.d <= WARP_D_MAX) np_leaves(p.d, p.plan);
     p.reg_path = reg_path_ok(p.d) ? 1 : 0;
+    static const int pd_env = getenv("VS_RR_PD") ? atoi(getenv("VS_RR_PD")) : -1;
+    if (pd_env >= 0) p.prefetch_iters = pd_env;
     // large k (many survivors and live candidates per query): the wide build;
     // small k (probes, IVF lists, config 1): 4 CTAs/SM hide more latency (measured)
     static const int wide_env = getenv("VS_RR_WIDE") ? atoi(getenv("VS_RR_WIDE")) : -1;
