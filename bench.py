@@ -656,10 +656,14 @@ class IvfWorkload:
         log(f"[rank {rank}] generated {n} x {d} ({'bf16' if self.bf16 else 'f32'}) in {time.time() - t0:.1f}s")
         t0 = time.time()
         col = vs.EmbeddingColumn.from_device(data)
+        from paper_2605_15957_b200 import _native as N
+        ties0 = N.Context.get().stats()[N.STAT_NEAR_TIES]
         self.index = vs.IvfIndex.build(col, cfg["nlist"], seed=0, max_iters=cfg.get("iters", 20))
         torch.cuda.synchronize()
         self.build_s = time.time() - t0
-        log(f"[rank {rank}] IVF build nlist={cfg['nlist']} in {self.build_s:.1f}s")
+        self.build_ties = int(N.Context.get().stats()[N.STAT_NEAR_TIES] - ties0)
+        log(f"[rank {rank}] IVF build nlist={cfg['nlist']} in {self.build_s:.1f}s "
+            f"({self.build_ties} near-tie rows re-checked exactly over all iterations)")
         sizes = np.array([len(p) for p in self.index.partitions], np.int64)
         self.list_sizes = sizes
         self.owned = None
@@ -798,6 +802,7 @@ class IvfWorkload:
                 "n_selected": self.n_sel_total, "unique_probed_lists": getattr(self, "unique_lists", None),
                 "pairs_per_list": getattr(self, "list_pairs", None),
                 "build_s": round(self.build_s, 2),
+                "build_near_tie_rechecks": self.build_ties,
                 "list_rows": {"mean": round(float(np.mean(self.list_sizes)), 1),
                               "p99": int(np.percentile(self.list_sizes, 99)),
                               "max": int(np.max(self.list_sizes))},

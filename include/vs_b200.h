@@ -86,6 +86,7 @@ enum vs_stat {
     VS_STAT_OVERFLOW_QUERIES = 1,/* queries re-run with a larger buffer         */
     VS_STAT_SURVIVORS = 2,       /* candidates re-ranked in float64 (last call) */
     VS_STAT_LAST_ENN_KERNEL = 3, /* which phase-A kernel ran last               */
+    VS_STAT_NEAR_TIES = 4,       /* k-means / assign rows re-checked exactly    */
     VS_STAT_N = 8
 };
 

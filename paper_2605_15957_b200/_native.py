@@ -30,6 +30,7 @@ OPT_COARSE = 8
 KERNEL_CLASSES = ("select", "enn_scan", "rerank", "coarse", "ivf_scan", "ivf_rerank", "merge", "stage",
                   "coarse_rerank")
 STAT_LAUNCHES, STAT_OVERFLOW_QUERIES, STAT_SURVIVORS, STAT_LAST_ENN_KERNEL = 0, 1, 2, 3
+STAT_NEAR_TIES = 4
 
 _vp = C.c_void_p
 _i32 = C.c_int32

@@ -2138,6 +2138,37 @@ int coarse_dense(vs_ctx* ctx, const EnnJob& cj, float* simt_margin, int n_qchunk
 
 }  // namespace
 
+namespace vs {
+// exact tie-rule nearest row (squared L2, float64 phase B) of each of m float32
+// queries among nrows float32 rows: the k-means near-tie recheck (vs_kmeans.cu)
+int exact_top1(vs_ctx* ctx, const float* q, int64_t m, int d, const float* rows, int64_t nrows, const float* rnorm,
+               const unsigned* rmax, int32_t* out_ids, double* out_dist) {
+    float* margin = nullptr;
+    int32_t* cnt = nullptr;
+    CKS(arena_alloc(ctx, (size_t)m, &margin));
+    CKS(arena_alloc(ctx, (size_t)m, &cnt));
+    CK(vs::launch_query_margins(q, m, d, rmax, eps_simt(d), 0, margin, nullptr, ctx->stream));
+    EnnJob job;
+    job.q = q;
+    job.nq = m;
+    job.d = d;
+    job.rows = rows;
+    job.dtype = VS_DTYPE_F32;
+    job.sel = nullptr;
+    job.nsel = nrows;
+    job.xnorm = rnorm;
+    job.xmax = rmax;
+    job.ip = 0;
+    job.k = 1;
+    job.id_offset = 0;
+    job.out_ids = nullptr;
+    job.out_dist = out_dist;
+    job.out_ids32 = out_ids;
+    job.out_count = cnt;
+    return run_enn(ctx, job, margin, 0, false);
+}
+}  // namespace vs
+
 // IVF search; probes_in (nullable, [nq][nprobe]) skips the coarse quantizer
 // (multi-GPU: each rank probes a slice of the queries, the probes are
 // all-gathered); probe_only stops after the coarse quantizer.

@@ -92,6 +92,19 @@ struct Arena {
         need = 0;
         return cudaSuccess;
     }
+    // scratch of a nested, synchronous step (stream idle): rewinding frees
+    // everything allocated after the mark, extras included
+    struct Mark {
+        size_t used, extras;
+    };
+    Mark mark() const { return Mark{used, extra.size()}; }
+    void rewind(const Mark& m) {
+        while (extra.size() > m.extras) {
+            cudaFree(extra.back());
+            extra.pop_back();
+        }
+        used = m.used;
+    }
     cudaError_t alloc(size_t n, void** out) {
         n = (n + 255) & ~size_t(255);
         need += n;

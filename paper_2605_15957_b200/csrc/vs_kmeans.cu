@@ -11,9 +11,13 @@
 //             centroids stored as float32, lists = ascending row ids (stable
 //             radix sort of (list, row)), payload gathered list-major (owning)
 //
-// The assignment compares bf16 tensor-core keys ||c||^2 - 2 x.c; the
-// reference compares float64 BLAS-expansion keys. Both are approximations of
-// the same argmin; build parity is property-level (tests/test_gpu_ivf_build.py).
+// The assignment compares bf16 tensor-core keys ||c||^2 - 2 x.c with a
+// rigorous error bound; every row whose best and second-best keys lie within
+// it is re-assigned by the exact tie-rule search (float64 phase B over the
+// float32 centroids, near_tie_recheck), so the assignment is the first-min
+// argmin of exact distances (the reference's float64 BLAS expansion can only
+// differ on ties at its own rounding level; tests/test_gpu_ivf_build.py: the
+// small reference build is reproduced row for row).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -51,6 +55,52 @@ __global__ void k_unpack(const unsigned long long* __restrict__ packed, const fl
         const unsigned long long v = packed[i];
         assign[i] = (int)(v & 0xffffffffu);
         dist[i] = fmaxf(o2f((uint32_t)(v >> 32)) + xnorm[i], 0.f);
+    }
+}
+
+// near ties of the tensor-core assignment: a row whose best and second-best
+// keys (over both column halves) lie within the keys' error bound (the
+// k_tc_margins formula with the row as the query and the centroids as rows)
+// may be assigned differently by exact arithmetic: listed for the recheck
+__global__ void k_near_ties(const unsigned long long* __restrict__ top2, const float2* __restrict__ rowstats,
+                            const unsigned* __restrict__ cst, const unsigned* __restrict__ cmax, int64_t n, int d,
+                            int* __restrict__ list, int* __restrict__ count) {
+    const float Ct = sqrtf(__uint_as_float(cst[0])) * 1.0001f;   // max ||c~||
+    const float Dc = sqrtf(__uint_as_float(cst[1])) * 1.0001f;   // max ||dc||
+    const float C2 = __uint_as_float(*cmax) * 1.0002f;           // max ||c||^2
+    const float acc_u = fmaxf(6.103515625e-05f, (float)((d + 15) / 16 + 4) * 9.5367431640625e-07f);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long b0 = top2[i * 4], s0 = top2[i * 4 + 1];
+        const unsigned long long b1 = top2[i * 4 + 2], s1 = top2[i * 4 + 3];
+        const bool h1 = b1 < b0;
+        const uint32_t best = (uint32_t)((h1 ? b1 : b0) >> 32);
+        const uint32_t other = (uint32_t)((h1 ? b0 : b1) >> 32);
+        const uint32_t second = min((uint32_t)(h1 ? s1 : s0), other);
+        const float2 rs = rowstats[i];
+        const float qx = sqrtf(rs.x) * 1.0001f, dx = sqrtf(rs.y) * 1.0001f;
+        const float edot = qx * Dc + dx * Ct + dx * Dc + acc_u * qx * Ct;
+        const float e = 2.f * edot + (float)(d + 2) * 5.9604645e-08f * C2 + 1.1920929e-07f * (C2 + 2.f * qx * Ct);
+        const float m = 2.f * e * 1.01f;
+        if (second == 0xffffffffu || !(o2f(second) - o2f(best) > m)) list[atomicAdd(count, 1)] = (int)i;
+    }
+}
+
+template <typename T>
+__global__ void k_gather_rows_f32(const T* __restrict__ x, const int* __restrict__ rows, int m, int d,
+                                  float* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)m * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / d, c = i - r * d;
+        out[i] = ld_elem(x + (int64_t)rows[r] * d + c);
+    }
+}
+
+__global__ void k_scatter_assign(const int* __restrict__ rows, const int32_t* __restrict__ ids,
+                                 const double* __restrict__ dd, int m, int* __restrict__ assign,
+                                 float* __restrict__ dist) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        assign[rows[i]] = ids[i];
+        dist[rows[i]] = (float)dd[i];
     }
 }
 
@@ -137,6 +187,55 @@ unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<in
 
 }  // namespace
 
+// Rows whose tensor-core assignment is within the keys' error bound of a
+// different centroid get the exact tie-rule nearest centroid (squared L2,
+// float64 phase B over the float32 centroids, first minimum on ties), so the
+// assignment equals the reference's first-min argmin up to the rounding of
+// its own float64 expansion. Chunks of 2^18 rows; arena space is reused.
+int near_tie_recheck(vs_ctx* ctx, const vs_column* data, int64_t n, int d, const unsigned long long* top2,
+                     const float2* rowstats, const unsigned* cst, const unsigned* cmax, const float* c32, int nlist,
+                     const float* cnorm, int* assign, float* dist, int64_t* n_rechecked) {
+    using namespace vs_internal;
+    cudaStream_t st = ctx->stream;
+    int* list = nullptr;
+    int* cnt = nullptr;
+    CKS(arena_alloc(ctx, (size_t)std::max<int64_t>(n, 1), &list));
+    CKS(arena_alloc(ctx, 1, &cnt));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+    k_near_ties<<<grid_for(n), 256, 0, st>>>(top2, rowstats, cst, cmax, n, d, list, cnt);
+    CK(cudaGetLastError());
+    int m = 0;
+    CK(cudaMemcpyAsync(&m, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n_rechecked) *n_rechecked += m;
+    ctx->stats[VS_STAT_NEAR_TIES] += m;
+    const int64_t chunk = (int64_t)1 << 16;
+    for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+        const int mc = (int)std::min<int64_t>(chunk, m - r0);
+        const auto mark = ctx->arena.mark();
+        float* qbuf = nullptr;
+        int32_t* ids = nullptr;
+        double* dd = nullptr;
+        CKS(arena_alloc(ctx, (size_t)mc * d, &qbuf));
+        CKS(arena_alloc(ctx, (size_t)mc, &ids));
+        CKS(arena_alloc(ctx, (size_t)mc, &dd));
+        if (data->dtype == VS_DTYPE_F32)
+            k_gather_rows_f32<float><<<grid_for((int64_t)mc * d), 256, 0, st>>>((const float*)data->data, list + r0,
+                                                                                 mc, d, qbuf);
+        else
+            k_gather_rows_f32<__nv_bfloat16><<<grid_for((int64_t)mc * d), 256, 0, st>>>(
+                (const __nv_bfloat16*)data->data, list + r0, mc, d, qbuf);
+        CK(cudaGetLastError());
+        CKS(exact_top1(ctx, qbuf, mc, d, c32, nlist, cnorm, cmax, ids, dd));
+        k_scatter_assign<<<grid_for(mc), 256, 0, st>>>(list + r0, ids, dd, mc, assign, dist);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        ctx->arena.rewind(mark);   // the chunk's scratch (and run_enn's) is free again
+        ctx->stats[VS_STAT_LAUNCHES] += 2;
+    }
+    return VS_OK;
+}
+
 int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows, uint64_t seed,
                   int32_t metric, int32_t max_iters, vs_ivf** out) {
     using namespace vs_internal;
@@ -206,8 +305,15 @@ int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64
     // row staging for the tensor-core assignment, allocated once for all iterations
     __nv_bfloat16* xb_scratch = nullptr;
     unsigned* junk = nullptr;
+    unsigned* cst = nullptr;
+    unsigned long long* top2 = nullptr;
+    float2* rowstats = nullptr;
     CKS(arena_alloc(ctx, (size_t)tc_argmin_chunk(n) * dp, &xb_scratch));
     CKS(arena_alloc(ctx, 2, &junk));
+    CKS(arena_alloc(ctx, 2, &cst));
+    CKS(arena_alloc(ctx, (size_t)n * 4, &top2));
+    CKS(arena_alloc(ctx, (size_t)n, &rowstats));
+    int64_t n_rechecked = 0;
 
     const float* xf = data->dtype == VS_DTYPE_F32 ? (const float*)data->data : nullptr;
     const __nv_bfloat16* xbf = data->dtype == VS_DTYPE_BF16 ? (const __nv_bfloat16*)data->data : nullptr;
@@ -224,12 +330,16 @@ int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64
         CK(cudaGetLastError());
         CK(cudaMemsetAsync(cmax, 0, sizeof(unsigned), st));
         CK(launch_row_norms<float>(c32, nlist, d, cnorm, cmax, st));
-        CKS(tc_stage_bf16(ctx, c32, nlist, d, cb, junk));
-        CKS(tc_argmin_rows(ctx, data->data, data->dtype, n, d, cb, cnorm, nlist, packed, xb_scratch, junk));
+        CK(cudaMemsetAsync(cst, 0, 2 * sizeof(unsigned), st));
+        // fp16 operands (~6x narrower error bound than bf16: fewer near-tie rechecks)
+        CKS(tc_stage_f16(ctx, c32, nlist, d, cmax, cb, cst));
+        CKS(tc_argmin_rows(ctx, data->data, data->dtype, n, d, cb, cnorm, nlist, packed, xb_scratch, junk, top2,
+                           rowstats, data->max_norm_bits, cmax));
         k_unpack<<<grid_for(n), 256, 0, st>>>(packed, data->norms, n, assign, dist);
         CK(cudaGetLastError());
         ctx->stats[VS_STAT_LAUNCHES] += 4;
-        return VS_OK;
+        return near_tie_recheck(ctx, data, n, d, top2, rowstats, cst, cmax, c32, nlist, cnorm, assign, dist,
+                                &n_rechecked);
     };
     // counts + reseed of empty lists (vecindex.py:286-294), host-driven: empty
     // lists are rare and the reference's loop is inherently sequential
@@ -327,10 +437,20 @@ int ivf_assign_gpu(vs_ctx* ctx, const vs_ivf* v, const vs_column* col, int32_t* 
     CKS(arena_alloc(ctx, (size_t)n, &packed));
     CKS(arena_alloc(ctx, (size_t)n, &assign));
     CKS(arena_alloc(ctx, (size_t)n, &dist));
-    CKS(tc_stage_bf16(ctx, v->centroids, nlist, d, cb, junk));
-    CKS(tc_argmin_rows(ctx, col->data, col->dtype, n, d, cb, v->cnorms, nlist, packed, xb, junk));
+    unsigned* cst = nullptr;
+    unsigned long long* top2 = nullptr;
+    float2* rowstats = nullptr;
+    CKS(arena_alloc(ctx, 2, &cst));
+    CKS(arena_alloc(ctx, (size_t)n * 4, &top2));
+    CKS(arena_alloc(ctx, (size_t)n, &rowstats));
+    CK(cudaMemsetAsync(cst, 0, 2 * sizeof(unsigned), st));
+    CKS(tc_stage_f16(ctx, v->centroids, nlist, d, v->cmax, cb, cst));
+    CKS(tc_argmin_rows(ctx, col->data, col->dtype, n, d, cb, v->cnorms, nlist, packed, xb, junk, top2, rowstats,
+                       col->max_norm_bits, v->cmax));
     k_unpack<<<grid_for(n), 256, 0, st>>>(packed, col->norms, n, assign, dist);
     CK(cudaGetLastError());
+    CKS(near_tie_recheck(ctx, col, n, d, top2, rowstats, cst, v->cmax, v->centroids, nlist, v->cnorms, assign, dist,
+                         nullptr));
     CK(cudaMemcpyAsync(out, assign, (size_t)n * sizeof(int32_t), cudaMemcpyDefault, st));
     CK(cudaStreamSynchronize(st));
     ctx->stats[VS_STAT_LAUNCHES] += 3;

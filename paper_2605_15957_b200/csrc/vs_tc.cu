@@ -123,6 +123,13 @@ struct Params {
     const float* kinv;              // nullable: [nq] 2^-(query scale + row scale) of the fp16 operands
     float* mins_out;                // MODE 3, nullable: min key of every 32-column chunk [nq][mins_ld]
     int64_t mins_ld;
+    // MODE 1, nullable: per (row, column half) its packed best and second key,
+    // [nq][2][2] (the near-tie check of the k-means assignment)
+    unsigned long long* top2_out;
+    // MODE 1 with fp16 operands: the rows' and the columns' max norm^2 (their
+    // power-of-two scales; the key factor is -2 / (s_rows s_cols))
+    const unsigned* a_scale_src;
+    const unsigned* b_scale_src;
 };
 
 // one work item: A tile rows [a_row, a_row + QTILE), B tiles of BN rows from
@@ -336,6 +343,8 @@ __device__ __forceinline__ float sel32(const float (&v)[32], int j) {
     return (j & 16) ? a[1] : a[0];
 }
 
+__device__ __forceinline__ float pow2_scale(float norm2);   // fp16 operand scales (below)
+
 // ---- the kernel --------------------------------------------------------------------------------------
 template <bool IP, int MODE, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -515,10 +524,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int quad = warp & 3;
         float* xw = xn_w[warp - EPI_WARP0];
         uint32_t tcount = 0;
+        const float cmul1 = p.a_scale_src ? -2.f / (pow2_scale(__uint_as_float(*p.a_scale_src)) *
+                                                    pow2_scale(__uint_as_float(*p.b_scale_src)))
+                                          : -2.f;
         for (int64_t it = unit; it < nitems; it += nunits) {
             const Item item = decode_item<MODE, QTILE>(p, it);
             const int64_t q = item.a_row + (int64_t)rank * BM + row;
-            uint32_t best_o = 0xffffffffu, best_i = 0u;
+            uint32_t best_o = 0xffffffffu, best_i = 0u, second_o = 0xffffffffu;
             for (int64_t t = 0; t < item.ntile; ++t, ++tcount) {
                 const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                 const int64_t r0 = item.b_row0 + t * BN;
@@ -545,11 +557,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float a = __uint_as_float(r[j]);
-                        const float key = IP ? -a : fmaf(-2.f, a, xw[ch * 32 + j]);
+                        const float key = IP ? -a : fmaf(cmul1, a, xw[ch * 32 + j]);
                         const uint32_t ko = f2o(key);
-                        if (cb0 + j < ncols && ko < best_o) {
-                            best_o = ko;
-                            best_i = (uint32_t)(r0 + cb0 + j);
+                        if (cb0 + j < ncols) {
+                            if (ko < best_o) {
+                                second_o = best_o;
+                                best_o = ko;
+                                best_i = (uint32_t)(r0 + cb0 + j);
+                            } else if (ko < second_o) {
+                                second_o = ko;
+                            }
                         }
                     }
                 }
@@ -557,7 +574,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (PAIR) mbar_arrive_leader(&S.tempty[acc]);
                 else mbar_arrive(&S.tempty[acc]);
             }
-            if (q < p.nq) atomicMin(&p.argmin_out[q], ((unsigned long long)best_o << 32) | best_i);
+            if (q < p.nq) {
+                const unsigned long long pk = ((unsigned long long)best_o << 32) | best_i;
+                atomicMin(&p.argmin_out[q], pk);
+                if (p.top2_out) {
+                    p.top2_out[(q * 2 + half) * 2] = pk;
+                    p.top2_out[(q * 2 + half) * 2 + 1] = second_o;
+                }
+            }
         }
     } else if (warp >= EPI_WARP0 && MODE == 3) {
         // ===== epilogue (dense keys): TMEM -> approximate keys -> global =====
@@ -1481,7 +1505,11 @@ int64_t tc_argmin_chunk(int64_t n) { return std::min<int64_t>(n, (int64_t)1 << 2
 
 int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, const __nv_bfloat16* cb,
                    const float* cnorm, int64_t ncols, unsigned long long* out, __nv_bfloat16* xb,
-                   unsigned* junk) {
+                   unsigned* junk, unsigned long long* top2, float2* rowstats, const unsigned* row_xmax,
+                   const unsigned* col_xmax) {
+    // fp16 operands (both scales known; columns staged by tc_stage_f16; bf16
+    // rows convert exactly unless far below the column's max norm)
+    const bool f16 = row_xmax && col_xmax;
     using namespace vs_internal;
     if (!get_encode()) return set_err(VS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cudaStream_t st = ctx->stream;
@@ -1490,20 +1518,30 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
     CK(cudaMemsetAsync(out, 0xff, n * sizeof(unsigned long long), st));
     const bool pair = use_pair(n);
     CUtensorMap mb;
-    if (!make_map(&mb, cb, ncols, d, dp, pair ? tc::BN / 2 : tc::BN))
+    if (!make_map(&mb, cb, ncols, d, dp, pair ? tc::BN / 2 : tc::BN, f16))
         return set_err(VS_ERR_CUDA, "tensor map (columns)");
     for (int64_t r0 = 0; r0 < n; r0 += chunk) {
         const int64_t m = std::min(chunk, n - r0);
         const unsigned blocks = (unsigned)std::min<int64_t>((m * 32 + 255) / 256, 148 * 64);
-        if (dtype == VS_DTYPE_F32)
-            tc::k_stage_rows<float, __nv_bfloat16><<<blocks, 256, 0, st>>>((const float*)x + r0 * (int64_t)d, nullptr,
-                                                                           m, d, dp, nullptr, xb, nullptr, junk);
+        if (f16 && dtype == VS_DTYPE_F32)
+            tc::k_stage_rows<float, __half><<<blocks, 256, 0, st>>>(
+                (const float*)x + r0 * (int64_t)d, nullptr, m, d, dp, nullptr, (__half*)xb, nullptr, junk, row_xmax,
+                rowstats ? rowstats + r0 : nullptr);
+        else if (f16)
+            tc::k_stage_rows<__nv_bfloat16, __half><<<blocks, 256, 0, st>>>(
+                (const __nv_bfloat16*)x + r0 * (int64_t)d, nullptr, m, d, dp, nullptr, (__half*)xb, nullptr, junk,
+                row_xmax, rowstats ? rowstats + r0 : nullptr);
+        else if (dtype == VS_DTYPE_F32)
+            tc::k_stage_rows<float, __nv_bfloat16><<<blocks, 256, 0, st>>>(
+                (const float*)x + r0 * (int64_t)d, nullptr, m, d, dp, nullptr, xb, nullptr, junk, nullptr,
+                rowstats ? rowstats + r0 : nullptr);
         else
             tc::k_stage_rows<__nv_bfloat16, __nv_bfloat16><<<blocks, 256, 0, st>>>(
-                (const __nv_bfloat16*)x + r0 * (int64_t)d, nullptr, m, d, dp, nullptr, xb, nullptr, junk);
+                (const __nv_bfloat16*)x + r0 * (int64_t)d, nullptr, m, d, dp, nullptr, xb, nullptr, junk, nullptr,
+                rowstats ? rowstats + r0 : nullptr);
         CK(cudaGetLastError());
         CUtensorMap ma;
-        if (!make_map(&ma, xb, m, d, dp, tc::BM)) return set_err(VS_ERR_CUDA, "tensor map (rows)");
+        if (!make_map(&ma, xb, m, d, dp, tc::BM, f16)) return set_err(VS_ERR_CUDA, "tensor map (rows)");
         tc::Params pr{};
         pr.nq = m;
         pr.d = d;
@@ -1515,12 +1553,29 @@ int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, cons
         pr.tiles_per_split = pr.ntiles;
         pr.xn = cnorm;
         pr.argmin_out = out + r0;
+        pr.top2_out = top2 ? top2 + r0 * 4 : nullptr;
+        pr.f16 = f16 ? 1 : 0;
+        pr.a_scale_src = f16 ? row_xmax : nullptr;
+        pr.b_scale_src = f16 ? col_xmax : nullptr;
         const unsigned units = (unsigned)std::min<int64_t>(pr.qtiles, pair ? ctx->sm_count / 2 : ctx->sm_count);
         CK((pair ? launch_tc<false, 1, true>(ma, mb, pr, 2 * units, st)
                  : launch_tc<false, 1, false>(ma, mb, pr, units, st)));
         CK(cudaGetLastError());
         ctx->stats[VS_STAT_LAUNCHES] += 2;
     }
+    return VS_OK;
+}
+
+// stage a float32 matrix to fp16 [n][dp] scaled by pow2_scale(*xmax) (the
+// k-means centroids for an fp16 argmin); max (||x~||^2, ||dx||^2) into stats
+int tc_stage_f16(vs_ctx* ctx, const float* x, int64_t n, int d, const unsigned* xmax, void* out, unsigned* stats) {
+    using namespace vs_internal;
+    const int dp = (d + 7) / 8 * 8;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n * 32 + 255) / 256, 148 * 64);
+    tc::k_stage_rows<float, __half><<<blocks, 256, 0, ctx->stream>>>(x, nullptr, n, d, dp, nullptr, (__half*)out,
+                                                                     nullptr, stats, xmax);
+    CK(cudaGetLastError());
+    ctx->stats[VS_STAT_LAUNCHES] += 1;
     return VS_OK;
 }
 

@@ -38,9 +38,14 @@ int tc_enn_scan(vs_ctx* ctx, EnnScanParams& sp, int dtype, const unsigned* xmax,
 // `scratch` = tc_argmin_scratch() bf16 elements + 2 words, allocated once by
 // the caller (the k-means loop calls this every iteration).
 int64_t tc_argmin_chunk(int64_t n);
+// top2 (nullable, [n][2][2]) and rowstats (nullable, [n] (||x~||^2, ||dx||^2))
+// feed the near-tie recheck (vs_kmeans.cu)
 int tc_argmin_rows(vs_ctx* ctx, const void* x, int dtype, int64_t n, int d, const __nv_bfloat16* cb,
                    const float* cnorm, int64_t ncols, unsigned long long* out, __nv_bfloat16* xb,
-                   unsigned* junk);
+                   unsigned* junk, unsigned long long* top2 = nullptr, float2* rowstats = nullptr,
+                   const unsigned* row_xmax = nullptr, const unsigned* col_xmax = nullptr);
+// fp16 staging of float32 columns scaled by pow2_scale(*xmax) (for the fp16 argmin)
+int tc_stage_f16(vs_ctx* ctx, const float* x, int64_t n, int d, const unsigned* xmax, void* out, unsigned* stats);
 int tc_stage_bf16(vs_ctx* ctx, const float* x, int64_t n, int d, __nv_bfloat16* out, unsigned* junk);
 // dense approximate keys [nq][ncols] of float32 rows X on the tensor cores
 // (MODE 3; the IVF coarse quantizer) and their per-query margins
@@ -93,6 +98,9 @@ int tc_stage_queries_f16(vs_ctx* ctx, const float* Q, int64_t nq, int d, const u
 
 // GPU IVF build / assignment (vs_kmeans.cu)
 int ivf_assign_gpu(vs_ctx* ctx, const vs_ivf* v, const vs_column* col, int32_t* out);
+// exact tie-rule nearest row of each query (vs_capi.cu; the k-means near-tie recheck)
+int exact_top1(vs_ctx* ctx, const float* q, int64_t m, int d, const float* rows, int64_t nrows, const float* rnorm,
+               const unsigned* rmax, int32_t* out_ids, double* out_dist);
 int ivf_build_gpu(vs_ctx* ctx, const vs_column* data, int32_t nlist, const int64_t* init_rows, uint64_t seed,
                   int32_t metric, int32_t max_iters, vs_ivf** out);
 

@@ -1,9 +1,7 @@
 #!/bin/bash
 set -u
-OUT=gpurun_out/r2ae
+OUT=gpurun_out/r2ah
 mkdir -p $OUT
-timeout 600 python -m pytest tests/test_gpu_enn.py -q -x > $OUT/pytest_sel.txt 2>&1; echo "pytest rc=$?"; tail -1 $OUT/pytest_sel.txt
-for pd in 4 2 1 0 8 4; do
-  VS_RR_PD=$pd timeout 600 python bench.py --config 2 --no-cpu --steps 20 > $OUT/cfg2_pd$pd.json 2>/dev/null
-  python -c "import json;d=json.load(open('$OUT/cfg2_pd$pd.json'));print('cfg2 pd=$pd', d['ms_per_step'], d['kernel_ms_per_step']['rerank'], d['clocks']['sm_mhz'])"
-done
+timeout 900 python -m pytest tests/test_gpu_ivf_build.py tests/test_gpu_ivf_kernels.py tests/test_gpu_ivf.py -q -x -s > $OUT/pytest_sel.txt 2>&1; echo "pytest rc=$?"; tail -2 $OUT/pytest_sel.txt; grep -i "agreement" $OUT/pytest_sel.txt
+timeout 900 python bench.py --config 3 --no-cpu --steps 5 > $OUT/cfg3.json 2> $OUT/cfg3.err; grep -E "build" $OUT/cfg3.err | head -2
+timeout 1200 python bench.py --config 4 --no-cpu --steps 5 > $OUT/cfg4.json 2> $OUT/cfg4.err; grep -E "build" $OUT/cfg4.err | head -2
