@@ -88,10 +88,13 @@ __global__ void k_near_ties(const unsigned long long* __restrict__ top2, const f
 template <typename T>
 __global__ void k_gather_rows_f32(const T* __restrict__ x, const int* __restrict__ rows, int m, int d,
                                   float* __restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)m * d;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / d, c = i - r * d;
-        out[i] = ld_elem(x + (int64_t)rows[r] * d + c);
+    // a warp per row, coalesced, no index division
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const T* src = x + (int64_t)rows[r] * d;
+        float* dst = out + r * d;
+        for (int c = lane; c < d; c += 32) dst[c] = ld_elem(src + c);
     }
 }
 
@@ -209,7 +212,7 @@ int near_tie_recheck(vs_ctx* ctx, const vs_column* data, int64_t n, int d, const
     CK(cudaStreamSynchronize(st));
     if (n_rechecked) *n_rechecked += m;
     ctx->stats[VS_STAT_NEAR_TIES] += m;
-    const int64_t chunk = (int64_t)1 << 16;
+    const int64_t chunk = (int64_t)1 << 18;
     for (int64_t r0 = 0; r0 < m; r0 += chunk) {
         const int mc = (int)std::min<int64_t>(chunk, m - r0);
         const auto mark = ctx->arena.mark();
@@ -220,10 +223,10 @@ int near_tie_recheck(vs_ctx* ctx, const vs_column* data, int64_t n, int d, const
         CKS(arena_alloc(ctx, (size_t)mc, &ids));
         CKS(arena_alloc(ctx, (size_t)mc, &dd));
         if (data->dtype == VS_DTYPE_F32)
-            k_gather_rows_f32<float><<<grid_for((int64_t)mc * d), 256, 0, st>>>((const float*)data->data, list + r0,
-                                                                                 mc, d, qbuf);
+            k_gather_rows_f32<float><<<grid_for((int64_t)mc * 32), 256, 0, st>>>((const float*)data->data, list + r0,
+                                                                                  mc, d, qbuf);
         else
-            k_gather_rows_f32<__nv_bfloat16><<<grid_for((int64_t)mc * d), 256, 0, st>>>(
+            k_gather_rows_f32<__nv_bfloat16><<<grid_for((int64_t)mc * 32), 256, 0, st>>>(
                 (const __nv_bfloat16*)data->data, list + r0, mc, d, qbuf);
         CK(cudaGetLastError());
         CKS(exact_top1(ctx, qbuf, mc, d, c32, nlist, cnorm, cmax, ids, dd));
