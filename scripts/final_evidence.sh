@@ -1,7 +1,7 @@
 #!/bin/bash
 # round-2 final evidence: full gpu suite, smoke, all configs, reference arm, launch lists
 set -u
-OUT=gpurun_out/r2w
+OUT=gpurun_out/final
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $OUT/gpu.txt 2>&1
 timeout 1800 python -m pytest tests -q -m gpu -x --durations=10 > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest_gpu.txt
