@@ -709,10 +709,60 @@ __global__ void __launch_bounds__(NT, PH == 1 ? 5 : (WIDE ? 2 : 4)) k_rerank(Rer
             }
             __syncthreads();
         }
-        // 0. live candidates -> shared memory (one warp per buffer, coalesced)
+        // 0. live candidates -> shared memory. Many short buffers (IVF: a few
+        //    entries per (pair, column half)): all threads walk the flat entry
+        //    index space (buffer by a search over the counts' prefix, in the
+        //    histogram region), one round of loads; else one warp per buffer
         if (tid == 0) sm.counter = 0;
+        const bool flat = nsub > 2 * NWARP && nsub < HBINS && tot < (long long)nsub * 24;
+        if (flat && w == 0) {
+            int run = 0;
+            for (int s0 = 0; s0 < nsub; s0 += 32) {
+                const int s = s0 + lane;
+                const int c = s < nsub ? cnts[s] : 0;
+                int incl = c;
+    #pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(VS_FULL, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (s < nsub) hist[s] = (unsigned)(run + incl - c);
+                run += __shfl_sync(VS_FULL, incl, 31);
+            }
+        }
         __syncthreads();
-        for (int s = w; s < nsub; s += NWARP) {
+        if (flat) {
+            const int ntot = (int)tot;
+            for (int f0 = w * 32; f0 < ntot; f0 += NT) {
+                const int f = f0 + lane;
+                float kv = 0.f;
+                uint32_t pv = 0u;
+                bool live = false;
+                if (f < ntot) {
+                    int a = 0, b = nsub - 1;   // last buffer whose prefix <= f
+                    while (a < b) {
+                        const int m = (a + b + 1) >> 1;
+                        if ((int)hist[m] <= f) a = m; else b = m - 1;
+                    }
+                    const int64_t e = (int64_t)a * C + (f - (int)hist[a]);
+                    kv = ckey[e];
+                    live = f2o(kv) <= pre;
+                    if (live) pv = cpos[e];
+                }
+                const unsigned bl = __ballot_sync(VS_FULL, live);
+                if (bl) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&sm.counter, __popc(bl));
+                    base = __shfl_sync(VS_FULL, base, 0);
+                    const int slot = base + __popc(bl & lanemask_lt());
+                    if (live && slot < LCAP) {
+                        lkey[slot] = kv;
+                        lpos[slot] = pv;
+                    }
+                }
+            }
+        }
+        for (int s = flat ? nsub : w; s < nsub; s += NWARP) {
             const int cs = cnts[s];
             const float* bk = ckey + (int64_t)s * C;
             const uint32_t* bp = cpos + (int64_t)s * C;
