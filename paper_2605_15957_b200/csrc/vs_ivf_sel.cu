@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
                     const int rr = c0 + r;
                     const uint32_t pos = rr < MPOS ? rec->pos[rr] : __ldg(p.spos + rec->sel_off + rr);
                     const float4* src = reinterpret_cast<const float4*>(p.payload + (int64_t)pos * d);
-                    // all of the lane's loads in flight before the first conversion
+                    // the row norm and all of the lane's loads in flight before the first conversion
+                    const float xnv = IP || lane != 0 ? 0.f : __ldg(p.pnorm + pos);
                     float4 v[MV];
 #pragma unroll
                     for (int j = 0; j < MV; ++j) {
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
                     }
                     if (lane == 0) {
                         pos_s[r] = pos;
-                        xn_s[r] = IP ? 0.f : __ldg(p.pnorm + pos);
+                        xn_s[r] = xnv;
                     }
                 }
             }

@@ -1100,17 +1100,36 @@ __global__ void k_stage_rows_f16(const __half* __restrict__ sh, const float2* __
     int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     float mb = 0.f, me = 0.f;
+    const int n16 = dp / 8;
+    int64_t r = w < nsel ? (sel ? sel[w] : w) : 0;
     for (; w < nsel; w += nw) {
-        const int64_t r = sel ? sel[w] : w;
+        // the next row's index, this row's stats and four 16-byte loads per
+        // lane are all in flight before the first store
+        const int64_t rn = w + nw < nsel ? (sel ? sel[w + nw] : w + nw) : 0;
         const uint4* src = reinterpret_cast<const uint4*>(sh + r * (int64_t)dp);
         uint4* dst = reinterpret_cast<uint4*>(out + w * (int64_t)dp);
-        for (int c = lane; c < dp / 8; c += 32) dst[c] = __ldcs(src + c);
+        float2 st = make_float2(0.f, 0.f);
+        float nv = 0.f;
         if (lane == 0) {
-            const float2 st = stats[r];
+            st = stats[r];
+            if (xn) nv = norms[r];
+        }
+        int c = lane;
+        for (; c + 96 < n16; c += 128) {
+            const uint4 v0 = __ldcs(src + c), v1 = __ldcs(src + c + 32), v2 = __ldcs(src + c + 64),
+                        v3 = __ldcs(src + c + 96);
+            dst[c] = v0;
+            dst[c + 32] = v1;
+            dst[c + 64] = v2;
+            dst[c + 96] = v3;
+        }
+        for (; c < n16; c += 32) dst[c] = __ldcs(src + c);
+        if (lane == 0) {
             mb = fmaxf(mb, st.x);
             me = fmaxf(me, st.y);
-            if (xn) xn[w] = norms[r];
+            if (xn) xn[w] = nv;
         }
+        r = rn;
     }
     if (lane == 0) {
         atomicMax(&xmax2[0], __float_as_uint(mb));
