@@ -1891,6 +1891,10 @@ cudaError_t launch_rerank(const RerankParams& p0, cudaStream_t s) {
     static const int wide_env = getenv("VS_RR_WIDE") ? atoi(getenv("VS_RR_WIDE")) : -1;
     const bool wide = wide_env >= 0 ? wide_env == 1 : p.k > 64;
     p.ubytes = (int)union_bytes(p.d, wide);
+    // the wide scorer's two rows per warp and iteration: two iterations of L2
+    // prefetch lead (four put ~95 MB of rows in flight and re-read 0.8 GB of
+    // them from HBM in config 2 at the same time, profiles/r2/rerank_pd_sweep)
+    if (wide && pd_env < 0) p.prefetch_iters = 2;
     // split phase B (wide build; VS_RR_SPLIT=0/1 overrides): the gather + select
     // kernel runs at 5 CTAs/SM without the scorer's registers, then score +
     // top-k (measured: config 2 re-rank 2.06 -> 1.90 ms; the narrow build
