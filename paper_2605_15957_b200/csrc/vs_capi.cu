@@ -74,11 +74,15 @@ int stage_out(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& p
 // final outputs (written once by the last kernels, never read back): a
 // page-locked host buffer is written in place by the kernels over PCIe
 // (zero-copy), so the result transfer overlaps phase B instead of following
-// it (VS_ZERO_COPY_OUT=0 stages them like any host buffer)
+// it (VS_ZERO_COPY_OUT=0 stages them like any host buffer). Only for buffers
+// up to VS_ZERO_COPY_MAX bytes (default 2 MiB): config 2's 8 MB id and
+// distance buffers written over PCIe slowed its phase B by ~0.3 ms end to end,
+// config 3's 0.8 MB ones gain 0.04 ms (profiles/r2/e2e_transfers)
 template <typename T>
 int stage_out_final(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& pending, bool allow) {
     static const bool zc_env = !(getenv("VS_ZERO_COPY_OUT") && getenv("VS_ZERO_COPY_OUT")[0] == '0');
-    if (allow && zc_env && dst && !is_device_ptr(dst)) {
+    const size_t zc_max = getenv("VS_ZERO_COPY_MAX") ? (size_t)atoll(getenv("VS_ZERO_COPY_MAX")) : ((size_t)2 << 20);
+    if (allow && zc_env && dst && count * sizeof(T) <= zc_max && !is_device_ptr(dst)) {
         cudaPointerAttributes a;
         if (cudaPointerGetAttributes(&a, dst) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer) {
             *dev = static_cast<T*>(a.devicePointer);
@@ -2196,7 +2200,11 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
         const bool host_q = queries && cudaPointerGetAttributes(&at, queries) == cudaSuccess &&
                             at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged;
         cudaGetLastError();
-        if (host_q && !probes_in && (size_t)nq * d * 4 >= ((size_t)1 << 23) && nq >= 4 * 256) {
+        // off unless VS_Q_CHUNKS > 0 (read per call): measured on config 3 (41 MB
+        // of queries), four coarse chunks of 2,500 queries cost more than the
+        // overlap saves (e2e 2.85 vs 2.61 ms, profiles/r2/e2e_transfers)
+        const int qchunk_env = getenv("VS_Q_CHUNKS") ? atoi(getenv("VS_Q_CHUNKS")) : 0;
+        if (qchunk_env > 0 && host_q && !probes_in && (size_t)nq * d * 4 >= ((size_t)1 << 23) && nq >= 4 * 256) {
             float* buf = nullptr;
             CKS(arena_alloc(ctx, (size_t)nq * d, &buf));
             if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));

@@ -266,3 +266,24 @@ def test_pinned_host_outputs_written_in_place(kernel):
     assert np.array_equal(out[2].numpy(), np.full(300, k, np.int32))
     assert np.array_equal(out[0].numpy().reshape(-1), ref.data_row)
     assert np.array_equal(out[1].numpy().reshape(-1), ref.distance)
+
+
+@pytest.mark.gpu
+def test_large_pinned_host_outputs_staged():
+    """Page-locked output buffers above the zero-copy limit (2 MiB) are
+    staged in device memory and copied back once: same results as the oracle."""
+    import torch
+    from paper_2605_15957_b200.vecindex import enn_search_raw
+    rng = np.random.default_rng(52)
+    data = rng.standard_normal((20000, 32)).astype(np.float32)
+    q = rng.standard_normal((3000, 32)).astype(np.float32)
+    mask = rng.random(20000) < 0.3
+    k = 100                                           # 3000 x 100 x 8 B = 2.4 MB per buffer
+    out = (torch.full((3000, k), 7, dtype=torch.int64).pin_memory(),
+           torch.zeros((3000, k), dtype=torch.float64).pin_memory(),
+           torch.zeros(3000, dtype=torch.int32).pin_memory())
+    enn_search_raw(torch.from_numpy(q).pin_memory(), data, k, row_filter=mask, out=out)
+    ref = O.enn_filtered(q, data, mask, k)
+    assert np.array_equal(out[2].numpy(), np.full(3000, k, np.int32))
+    assert np.array_equal(out[0].numpy().reshape(-1), ref.data_row)
+    assert np.array_equal(out[1].numpy().reshape(-1), ref.distance)

@@ -272,10 +272,12 @@ def test_ivf_pinned_host_outputs_written_in_place():
 
 
 @pytest.mark.parametrize("pinned", [False, True])
-def test_ivf_large_host_query_batch_chunked_upload(pinned):
+def test_ivf_large_host_query_batch_chunked_upload(pinned, monkeypatch):
     """A large host query batch is uploaded in chunks while the coarse
-    quantizer runs on the chunks that have landed: identical to the same
-    search with device-resident queries, and sampled queries equal the oracle."""
+    quantizer runs on the chunks that have landed (opt-in, VS_Q_CHUNKS):
+    identical to the same search with device-resident queries, and sampled
+    queries equal the oracle."""
+    monkeypatch.setenv("VS_Q_CHUNKS", "4")
     rng = np.random.default_rng(88)
     n, d, nlist = 20000, 512, 256
     idx, data, centroids, parts, payload = _index(rng, n, d, nlist)
