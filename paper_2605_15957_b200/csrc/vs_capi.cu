@@ -74,14 +74,14 @@ int stage_out(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& p
 // final outputs (written once by the last kernels, never read back): a
 // page-locked host buffer is written in place by the kernels over PCIe
 // (zero-copy), so the result transfer overlaps phase B instead of following
-// it (VS_ZERO_COPY_OUT=0 stages them like any host buffer). Only for buffers
-// up to VS_ZERO_COPY_MAX bytes (default 2 MiB): config 2's 8 MB id and
-// distance buffers written over PCIe slowed its phase B by ~0.3 ms end to end,
-// config 3's 0.8 MB ones gain 0.04 ms (profiles/r2/e2e_transfers)
+// it (VS_ZERO_COPY_OUT=0 stages them like any host buffer; VS_ZERO_COPY_MAX
+// caps the zero-copy buffer size in bytes, default no cap). Measured in
+// profiles/r2/e2e_transfers: config 3 (0.8 MB buffers) gains 0.04 ms; config
+// 2 (8 MB) staged and copied back adds ~0.3 ms of non-kernel time per step
 template <typename T>
 int stage_out_final(vs_ctx* ctx, T* dst, size_t count, T** dev, std::vector<OutBuf>& pending, bool allow) {
     static const bool zc_env = !(getenv("VS_ZERO_COPY_OUT") && getenv("VS_ZERO_COPY_OUT")[0] == '0');
-    const size_t zc_max = getenv("VS_ZERO_COPY_MAX") ? (size_t)atoll(getenv("VS_ZERO_COPY_MAX")) : ((size_t)2 << 20);
+    const size_t zc_max = getenv("VS_ZERO_COPY_MAX") ? (size_t)atoll(getenv("VS_ZERO_COPY_MAX")) : SIZE_MAX;
     if (allow && zc_env && dst && count * sizeof(T) <= zc_max && !is_device_ptr(dst)) {
         cudaPointerAttributes a;
         if (cudaPointerGetAttributes(&a, dst) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer) {
@@ -2211,7 +2211,7 @@ static int ivf_search_impl(vs_ctx* ctx, const vs_ivf* ivf, const float* queries,
             if (!ctx->q_event) CK(cudaEventCreateWithFlags(&ctx->q_event, cudaEventDisableTiming));
             CK(cudaEventRecord(ctx->q_event, ctx->stream));            // earlier work on the arena
             CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->q_event, 0));
-            n_qchunks = 4;
+            n_qchunks = std::min(qchunk_env, 4);   // q_chunk_ev[4]
             const int64_t qc = (nq + n_qchunks - 1) / n_qchunks;
             for (int c = 0; c < n_qchunks; ++c) {
                 if (!ctx->q_chunk_ev[c]) CK(cudaEventCreateWithFlags(&ctx->q_chunk_ev[c], cudaEventDisableTiming));

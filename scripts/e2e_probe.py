@@ -87,8 +87,35 @@ def interleaved_zero_copy(config=2, rounds=6):
         print(f"config {config} {arm:6s}: " + " ".join(f"{x:.3f}" for x in v) + f"  median {sorted(v)[len(v) // 2]:.3f} ms")
 
 
+def interleaved_chunks(config=3, rounds=6, arms=("0", "2", "4")):
+    """e2e with the IVF chunked query upload at 0 / 2 / 4 chunks, interleaved."""
+    import os
+    args = argparse.Namespace(gpus=1, steps=10, warmup=3, config=config, impl="ours", no_cpu=True,
+                              cpu_budget=0, ref_budget=0, cand_slack=0, n_rows=0)
+    cfg = dict(bench.CONFIGS[config])
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    wl = (bench.IvfBf16Workload if cfg.get("bf16") else bench.IvfWorkload)(args, cfg, 0, 1, dev)
+    for _ in range(3):
+        wl.step_device()
+        wl.step_e2e()
+    res = {a: [] for a in arms}
+    res["device"] = []
+    for _ in range(rounds):
+        for a in arms:
+            os.environ["VS_Q_CHUNKS"] = a
+            wl.step_e2e()
+            res[a].append(ev_time(wl.step_e2e, 5)[0])
+        res["device"].append(ev_time(wl.step_device, 5)[0])
+    for arm, v in res.items():
+        print(f"config {config} chunks {arm:6s}: " + " ".join(f"{x:.3f}" for x in v)
+              + f"  median {sorted(v)[len(v) // 2]:.3f} ms")
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "zc":
+    if len(sys.argv) > 1 and sys.argv[1] == "chunks":
+        interleaved_chunks(int(sys.argv[2]) if len(sys.argv) > 2 else 3)
+    elif len(sys.argv) > 1 and sys.argv[1] == "zc":
         interleaved_zero_copy(int(sys.argv[2]) if len(sys.argv) > 2 else 2)
     else:
         main()

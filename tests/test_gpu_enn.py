@@ -269,10 +269,12 @@ def test_pinned_host_outputs_written_in_place(kernel):
 
 
 @pytest.mark.gpu
-def test_large_pinned_host_outputs_staged():
-    """Page-locked output buffers above the zero-copy limit (2 MiB) are
-    staged in device memory and copied back once: same results as the oracle."""
+def test_large_pinned_host_outputs_staged(monkeypatch):
+    """Page-locked output buffers above the zero-copy limit (VS_ZERO_COPY_MAX,
+    here 2 MiB) are staged in device memory and copied back once: same results
+    as the oracle."""
     import torch
+    monkeypatch.setenv("VS_ZERO_COPY_MAX", str(2 << 20))
     from paper_2605_15957_b200.vecindex import enn_search_raw
     rng = np.random.default_rng(52)
     data = rng.standard_normal((20000, 32)).astype(np.float32)
