@@ -1795,7 +1795,7 @@ __global__ void __launch_bounds__(WW * 32, 4) k_rerank_warp(RerankParams p, int3
         const char* base = reinterpret_cast<const char*>(rows + r * (int64_t)d);
         for (int o = lane * 128; o < row_bytes; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
     };
-    constexpr int PD = 3;
+    const int PD = max(0, p.prefetch_iters - 1);   // rows of L2 prefetch lead (default 3)
     for (int j = 1; j <= PD && j < ns; ++j) prefetch_row(row_of(j));
     uint64_t* sk = S.sk[w];
     int64_t* si = S.si[w];
