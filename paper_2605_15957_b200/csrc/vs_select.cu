@@ -141,21 +141,32 @@ cudaError_t launch_select_write(const uint32_t* bitmap, int64_t nwords, int64_t 
 __global__ void k_permute_bitmap(const uint32_t* __restrict__ bm, int64_t nbits,
                                  const int64_t* __restrict__ ids, int64_t n_total,
                                  uint32_t* __restrict__ pbits) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one thread per position
+    // a warp owns 4 x 32 consecutive positions (4 output words): its four
+    // coalesced id loads are in flight together before the bitmap gathers
+    constexpr int PW = 4;
     const int lane = threadIdx.x & 31;
-    bool bit = false;
-    if (i < n_total) {
-        int64_t r = ids[i];
-        bit = (r >= 0 && r < nbits) ? ((bm[r >> 5] >> (r & 31)) & 1u) : false;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t base = w * (32 * PW);
+    int64_t r[PW];
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+        const int64_t i = base + 32 * j + lane;
+        r[j] = i < n_total ? __ldcs(ids + i) : -1;
     }
-    unsigned b = __ballot_sync(VS_FULL, bit);
-    if (lane == 0 && (i >> 5) < (n_total + 31) / 32) pbits[i >> 5] = b;
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+        const bool bit = r[j] >= 0 && r[j] < nbits && ((__ldg(bm + (r[j] >> 5)) >> (r[j] & 31)) & 1u);
+        const unsigned b = __ballot_sync(VS_FULL, bit);
+        const int64_t word = (base >> 5) + j;
+        if (lane == 0 && word < (n_total + 31) / 32) pbits[word] = b;
+    }
 }
 
 cudaError_t launch_permute_bitmap(const uint32_t* bitmap, int64_t nbits, const int64_t* ids,
                                   int64_t n_total, uint32_t* pbits, cudaStream_t s) {
     if (n_total == 0) return cudaSuccess;
-    int64_t blocks = (n_total + 255) / 256;
+    const int64_t warps = (n_total + 127) / 128;
+    const int64_t blocks = (warps * 32 + 255) / 256;
     k_permute_bitmap<<<(unsigned)blocks, 256, 0, s>>>(bitmap, nbits, ids, n_total, pbits);
     return cudaGetLastError();
 }
