@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(MNT, 4) k_ivf_scan_mma(IvfMmaParams p) {
                     ckey[slot] = key;
                     cpos[slot] = pos_s[lane];
                 }
+                __syncwarp();   // every lane's read of cnt_s[pr] is ordered before lane 0's write
                 if (lane == 0) cnt_s[pr] = cnt + __popc(b);
             }
         }
