@@ -535,6 +535,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                 const int64_t r0 = item.b_row0 + t * BN;
                 const int ncols = (int)min((int64_t)BN, p.nsel - r0);
+                __syncwarp();   // the previous tile's reads of xw come first
                 if (lane * 4 < BN / 2) {
                     const int64_t i = r0 + half * (BN / 2) + lane * 4;
                     float4 v;
@@ -744,6 +745,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t acc = tcount % NACC, aph = (tcount / NACC) & 1;
                 const int64_t r0 = item.b_row0 + t * BN;
                 const int ncols = (int)min((int64_t)BN, item.b_end - r0);
+                __syncwarp();   // the previous tile's reads of xw come first
                 if (!IP && lane * 4 < BN / 2) *reinterpret_cast<float4*>(xw + lane * 4) = pf;
                 __syncwarp();
                 if (qv) tau = fminf(tau, o2f(pf_tau));
